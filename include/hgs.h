@@ -1,0 +1,252 @@
+/*
+ * hgs.h -- C ABI of libhgs.so, the B200 (sm_100a) hybrid Gaussian-splat +
+ * textured-mesh renderer.  This is the drop-in boundary: every entry point
+ * replaces one function of the reference operator API (gsmesh 0.1.0,
+ * /root/reference/pkg/src/gsmesh; file:line cited per function).  The
+ * reference's own "FFI" is the Numba kernel ABI (flat C-contiguous arrays,
+ * outputs preallocated by the Python wrapper and mutated in place); this ABI
+ * keeps that shape: plain device pointers + sizes, caller-owned outputs,
+ * explicit stream, int status.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless the parameter says "host".
+ *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *    and stream-ordered; nothing synchronises unless stated.
+ *  - Return 0 on success; HGS_ERR_INVALID for argument errors (the Python
+ *    layer raises ValueError, like the reference's shape checks);
+ *    HGS_ERR_CUDA for launch/runtime errors (RuntimeError).  hgs_last_error()
+ *    returns the message of the last failure on the calling thread.
+ *  - Parameters are fp32 (N x 3 etc., row-major).  Every decision the
+ *    reference makes (culling, tile rectangles, depth order, blend
+ *    skip/clamp/stop, z-buffer, texel taps) is computed in fp64.
+ */
+#ifndef HGS_H_
+#define HGS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGS_OK 0
+#define HGS_ERR_INVALID 1
+#define HGS_ERR_CUDA 2
+
+#define HGS_ABI_VERSION 1
+
+/* Pinhole camera, Camera (scene.py:144-203).  Derived fields are computed by
+   the host exactly as the reference computes them:
+   center = -R^T t (scene.py:190-192); limx/limy = 1.3 * (W / (2 fx))
+   (splat/project.py:97-98). */
+typedef struct hgs_camera {
+  double fx, fy, cx, cy;
+  int64_t width, height;
+  double R[9]; /* world_to_camera[:3,:3], row-major */
+  double T[3]; /* world_to_camera[:3,3] */
+  double near_, far_;
+  double center[3];
+  double limx, limy;
+} hgs_camera;
+
+/* GaussianSet (scene.py:37-57): fp32 device arrays, N rows.
+   colors_rest (N,3,3) [i][k][c] may be NULL (SH degree 0). */
+typedef struct hgs_gaussians {
+  const float* centers;     /* N x 3 */
+  const float* rotations;   /* N x 4 (w,x,y,z), not necessarily unit */
+  const float* log_scales;  /* N x 3 */
+  const float* logits;      /* N */
+  const float* colors_dc;   /* N x 3 */
+  const float* colors_rest; /* N x 3 x 3 or NULL */
+  int64_t n;
+} hgs_gaussians;
+
+/* Mutable twin of hgs_gaussians for parameter gradients (same layout). */
+typedef struct hgs_gaussian_grads {
+  float* centers;
+  float* rotations;
+  float* log_scales;
+  float* logits;
+  float* colors_dc;
+  float* colors_rest; /* NULL iff colors_rest is NULL */
+  float* densify_norm; /* N, may be NULL */
+  uint8_t* visible;    /* N, may be NULL */
+} hgs_gaussian_grads;
+
+/* Per-Gaussian projection state, indexed by ORIGINAL row (uncompacted).
+   rec: N x 80 B fp64 blend records {mean2d x,y; conic xx,xy,yy; alpha;
+   depth; colour r,g,b}.  count[i] = tile count (tiles.py:45-50), 0 iff the
+   row is culled by project (project.py:80-83,118-119).  The optional fields
+   (NULL to skip) are ProjectedGaussians extras (project.py:38-50). */
+typedef struct hgs_projected {
+  void* rec;
+  int32_t* count;
+  uint16_t* rect; /* N x 4: x0, x1, y0, y1 (inclusive tile rectangle) */
+  double* cov2d;     /* N x 3, optional */
+  double* radius;    /* N, optional */
+  double* t_cam;     /* N x 3, optional */
+  double* color_pre; /* N x 3, optional */
+  double* view_dir;  /* N x 3, optional (SH degree 1 only) */
+  double* view_dist; /* N, optional (SH degree 1 only) */
+} hgs_projected;
+
+/* TileBins (splat/tiles.py:19-32).  entries hold ORIGINAL Gaussian rows in
+   (tile, depth, row) order == np.lexsort((kept, depth, tile)) (tiles.py:65).
+   counters (device, int64[4]): [0] M visible rows, [1] K entries, [2]
+   overflow flag (K > capacity; entries/tile_starts are then invalid). */
+typedef struct hgs_tiles {
+  int32_t tiles_x, tiles_y, tile_px;
+  int32_t reserved;
+  int64_t capacity;
+  uint32_t* entries;    /* capacity */
+  int64_t* tile_starts; /* tiles_x * tiles_y + 1 */
+  int64_t* counters;    /* 4 */
+  void* scratch;
+  size_t scratch_bytes; /* >= hgs_tiles_scratch_bytes(n, capacity, tiles) */
+} hgs_tiles;
+
+/* MeshLayer (splat/render.py:26-41).  color == NULL means "no mesh". */
+typedef struct hgs_mesh_layer {
+  const float* color;          /* H x W x 3 */
+  const double* depth;         /* H x W, +inf where uncovered */
+  const int32_t* triangle_id;  /* H x W, -1 where uncovered */
+} hgs_mesh_layer;
+
+/* rasterize_forward outputs (splat/render.py:90-109). */
+typedef struct hgs_blend_out {
+  float* color;         /* H x W x 3 */
+  float* depth;         /* H x W (NaN where undefined) */
+  float* transmittance; /* H x W */
+  double* final_t;      /* H x W fp64 residual T, backward state (may be NULL) */
+  int32_t* last;        /* H x W global entry index or -1 (may be NULL) */
+  float* mask;          /* H x W transmittance_mask(T) (losses.py:79-91), may be NULL */
+  int64_t* stats;       /* device int64[2]: += evaluations walked, += blended (may be NULL) */
+} hgs_blend_out;
+
+/* TexturedMesh geometry (scene.py:206-237). */
+typedef struct hgs_mesh {
+  const float* vertices;    /* V x 3 */
+  const int32_t* triangles; /* F x 3 */
+  const float* uvs;         /* F x 3 x 2 or NULL */
+  int64_t n_vertices, n_faces;
+} hgs_mesh;
+
+/* MeshFragmentBuffer (meshraster.py:25-42), H x W. */
+typedef struct hgs_fragments {
+  int32_t* triangle_id; /* -1 uncovered */
+  double* depth;        /* +inf uncovered */
+  double* bary;         /* H x W x 3, may be NULL */
+  double* uv;           /* H x W x 2 */
+} hgs_fragments;
+
+/* One parameter group of the fused Adam step (train/adam.py:28-42). */
+typedef struct hgs_adam_group {
+  float* param;
+  float* m;
+  float* v;
+  const float* grad;
+  int64_t n;
+  float lr;
+  int32_t mode; /* 0 plain; 1 renormalise rows of 4 (loop.py:139-140); 2 clamp [0,1] (loop.py:144-145) */
+} hgs_adam_group;
+
+#define HGS_MAX_ADAM_GROUPS 8
+
+/* ---------------- library ---------------- */
+const char* hgs_last_error(void);
+int hgs_abi_version(void);
+int hgs_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---------------- splat forward ---------------- */
+
+/* project (splat/project.py:70-140) + evaluate_colors (:56-67) + per-row
+   tile rectangle/count (splat/tiles.py:45-50).  cam is a DEVICE pointer;
+   width/height (host) must equal cam->width/height. */
+int hgs_preprocess(const hgs_camera* cam, int32_t width, int32_t height, const hgs_gaussians* gs, int32_t tile_px,
+                   hgs_projected* out, void* stream);
+
+/* build_tiles (splat/tiles.py:35-69): visible-row compaction, fp64 depth
+   radix sort, tile-entry emission in depth order, stable tile radix sort,
+   CSR ranges.  All counts stay on the device (tiles->counters). */
+size_t hgs_tiles_scratch_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
+int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* tiles, void* stream);
+
+/* rasterize_forward (splat/render.py:74-109) / forward_kernel
+   (splat/kernels.py:12-74), with the transmittance mask epilogue
+   (train/losses.py:79-91; variant 0 sigmoid,1 identity_t,2 one,3 zero). */
+int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* tiles, int32_t width, int32_t height,
+                      const hgs_mesh_layer* mesh, const double* bg_host3, int32_t mask_variant, double mask_k,
+                      hgs_blend_out* out, void* stream);
+
+/* ---------------- splat backward ---------------- */
+
+/* backward_kernel (splat/kernels.py:77-160) + np.add.at reduction
+   (splat/render.py:155-157): accumulates per-row screen gradients into
+   screen_grads (N x 9 fp64, caller-zeroed): mean2d 2, cov 3 (full-matrix
+   convention), alpha, rgb 3.  mesh_color_grad (may be NULL) receives
+   grad_color * T * valid (render.py:180-181), accumulated when
+   accumulate_mesh != 0. */
+int hgs_blend_backward(const hgs_projected* proj, const hgs_tiles* tiles, int32_t width, int32_t height,
+                       const hgs_mesh_layer* mesh, const double* bg_host3, const double* final_t,
+                       const int32_t* last, const float* grad_color, const float* grad_t, double* screen_grads,
+                       float* mesh_color_grad, int32_t accumulate_mesh, void* stream);
+
+/* _chain_to_parameters (splat/render.py:185-313) + densify statistic and
+   visibility (render.py:171-178).  Writes (accumulate=0) or adds
+   (accumulate=1) scale * d/dparam into grads; densify_norm is written or
+   added the same way. */
+int hgs_project_backward(const hgs_camera* cam, const hgs_gaussians* gs, const hgs_projected* proj,
+                         const double* screen_grads, hgs_gaussian_grads* grads, float scale, int32_t accumulate,
+                         void* stream);
+
+/* ---------------- mesh ---------------- */
+
+/* rasterize_fragments (meshraster.py:119-136) / _raster_kernel (:45-116):
+   z-buffer with the reference's (depth, triangle index) resolution,
+   top-left rule, near-plane cull, perspective-correct bary/uv. */
+size_t hgs_raster_scratch_bytes(int64_t n_vertices, int64_t n_faces, int32_t width, int32_t height);
+int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int32_t height, const hgs_mesh* mesh,
+                            hgs_fragments* out, void* scratch, size_t scratch_bytes, void* stream);
+
+/* sample_texture (meshraster.py:139-166): bilinear, clamp-to-edge, invalid
+   pixels -> 0.  texture is Ht x Wt x 3 fp32. */
+int hgs_sample_texture(const float* texture, int32_t th, int32_t tw, const double* uv, const int32_t* triangle_id,
+                       int64_t npix, float* out, void* stream);
+
+/* texture_backward (meshraster.py:169-184): bilinear adjoint, added into
+   grad_texture (Ht x Wt x 3 fp32). */
+int hgs_texture_backward(const double* uv, const int32_t* triangle_id, const float* grad_image, int64_t npix,
+                         int32_t th, int32_t tw, float* grad_texture, void* stream);
+
+/* ---------------- losses (train/losses.py) ---------------- */
+
+/* transmittance_mask (losses.py:79-91). */
+int hgs_transmittance_mask(const float* t, int64_t n, double k, int32_t variant, float* out, void* stream);
+
+/* composite_loss (losses.py:139-174): L1 (:41-44) + D-SSIM (:47-76,
+   11-tap sigma 1.5 zero-padded) + texture loss (:103-116) when
+   texture_active.  Writes grad_ih (H x W x 3), grad_im (if non-NULL and
+   texture_active), grad_t (H x W) and, into scalars (device double[6]):
+   l1, dssim, l_c, l_t, total, mean_T_on_mesh.  grads are scaled by
+   grad_scale (1 for the reference semantics). */
+size_t hgs_loss_scratch_bytes(int32_t height, int32_t width);
+int hgs_composite_loss(const float* i_gt, const float* i_h, const float* i_m, const int32_t* triangle_id,
+                       const float* t, int32_t height, int32_t width, double lam_dssim, int32_t texture_active,
+                       double texture_weight, double mask_k, int32_t mask_variant, const double* window11_host,
+                       double grad_scale, float* grad_ih, float* grad_im, float* grad_t, double* scalars,
+                       void* scratch, size_t scratch_bytes, void* stream);
+
+/* ---------------- optimiser ---------------- */
+
+/* Adam.step (train/adam.py:28-42) over up to HGS_MAX_ADAM_GROUPS groups in
+   one launch, with quaternion renormalisation (loop.py:139-140) and texture
+   clamp (loop.py:144-145) fused.  step is the post-increment step count;
+   grads are multiplied by grad_scale first (view-batch mean). */
+int hgs_adam_step(const hgs_adam_group* groups_host, int32_t n_groups, int64_t step, float beta1, float beta2,
+                  float eps, float grad_scale, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGS_H_ */

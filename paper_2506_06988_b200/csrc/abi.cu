@@ -1,0 +1,38 @@
+// Library-level entry points of libhgs.so: error reporting and device query.
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace {
+thread_local char g_last_error[512] = "";
+}
+
+int hgs_set_error(int code, const char* msg) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
+  return code;
+}
+
+int hgs_set_cuda_error(cudaError_t e, const char* file, int line) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "CUDA error %s (%s) at %s:%d", cudaGetErrorName(e),
+                cudaGetErrorString(e), file, line);
+  return HGS_ERR_CUDA;
+}
+
+extern "C" const char* hgs_last_error(void) { return g_last_error; }
+
+extern "C" int hgs_abi_version(void) { return HGS_ABI_VERSION; }
+
+extern "C" int hgs_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return hgs_set_cuda_error(e, __FILE__, __LINE__);
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (sm_count) *sm_count = v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_major) *cc_major = v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev);
+  if (cc_minor) *cc_minor = v;
+  return HGS_OK;
+}

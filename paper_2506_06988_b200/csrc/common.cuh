@@ -1,0 +1,70 @@
+// Shared definitions for the hybrid GS+mesh CUDA path (sm_100a).
+//
+// Numerics: every kernel that restates a reference decision (cull, tile rect,
+// sort key, support/skip/clamp/early-stop/mesh-stop, z-buffer, texel taps)
+// computes in IEEE fp64 with FMA contraction disabled at compile time
+// (-fmad=false); FMAs appear only where the reference's numpy matmul uses
+// them (dot3 below).  See DESIGN.md "Numerics".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hgs.h"
+
+namespace hgs {
+
+// reference constants: gsmesh/splat/project.py:19-27, splat/tiles.py:16
+constexpr double COV_FLOOR = 0.3;
+constexpr double ALPHA_CLAMP = 0.99;
+constexpr double SIGMA_SKIP = 1.0 / 255.0;
+constexpr double SUPPORT_MAHAL2 = 9.0;
+constexpr double EARLY_STOP_T = 1e-4;
+constexpr double SH_C0 = 0.28209479177387814;
+constexpr double SH_C1 = 0.4886025119029199;
+
+constexpr int NUM_SMS = 148;
+
+// Blend record per Gaussian (fp64, 80 B): the fields the per-pixel walk reads.
+struct __align__(16) BlendRec {
+  double mx, my;      // mean2d
+  double ca, cb, cc;  // conic (xx, xy, yy)
+  double alpha;       // sigmoid(logit)
+  double depth;       // camera z
+  double r, g, b;     // view-evaluated colour, clamped at 0
+};
+static_assert(sizeof(BlendRec) == 80, "BlendRec must be 80 bytes");
+
+// numpy matmul inner-product order on x86-64 OpenBLAS (measured):
+// s = a0*b0; s = fma(a1,b1,s); s = fma(a2,b2,s)
+__device__ __forceinline__ double dot3(double a0, double a1, double a2, double b0, double b1, double b2) {
+  double s = a0 * b0;
+  s = fma(a1, b1, s);
+  s = fma(a2, b2, s);
+  return s;
+}
+
+template <typename T>
+__host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+template <typename T>
+__host__ __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace hgs
+
+#define HGS_CHECK_LAUNCH()                                   \
+  do {                                                       \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) return hgs_set_cuda_error(_e, __FILE__, __LINE__); \
+  } while (0)
+
+int hgs_set_cuda_error(cudaError_t e, const char* file, int line);
+int hgs_set_error(int code, const char* msg);

@@ -1,0 +1,280 @@
+// Device-wide primitives for tile binning: a single-pass chained scan and a
+// stable LSD radix sort (8-bit digits, one kernel per pass), both with
+// decoupled look-back and dynamic partition assignment so that every count
+// can stay on the device (no host round trip between stages).
+//
+// Radix pass: 256 threads x 16 items = 4096 keys per partition.  Ranking is
+// warp-level multisplit (__match_any_sync) with per-warp digit counters in
+// shared memory, which preserves input order inside a partition (stability);
+// partitions are ordered by their dynamically assigned id, and the look-back
+// over predecessor partitions gives each digit's global offset.  Items are
+// staged in shared memory in sorted order and written out digit-run by
+// digit-run, so global stores are coalesced.
+#pragma once
+#include "common.cuh"
+
+namespace hgs {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_IPT = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_IPT;
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_IPT = 16;
+constexpr int RS_TILE = RS_THREADS * RS_IPT;
+constexpr int RADIX = 256;
+
+constexpr uint64_t SCAN_FLAG_AGG = 1ull << 62;
+constexpr uint64_t SCAN_FLAG_INC = 2ull << 62;
+constexpr uint64_t SCAN_VALUE_MASK = (1ull << 62) - 1;
+
+constexpr uint32_t RS_FLAG_AGG = 1u << 30;
+constexpr uint32_t RS_FLAG_INC = 2u << 30;
+constexpr uint32_t RS_VALUE_MASK = (1u << 30) - 1;
+
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim == 256).
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* s_warp /*[8]*/, T& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < 8 ? s_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < 8) s_warp[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  T warp_excl = warp > 0 ? s_warp[warp - 1] : T(0);
+  total = s_warp[7];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
+// Chained-scan partition: every thread owns SCAN_IPT consecutive items.
+// Given per-item values, returns the exclusive prefix of each item and the
+// grand total (valid in the last partition).  status: one u64 per partition.
+template <typename F>
+__device__ __forceinline__ void chained_scan_partition(int part, int64_t n, F value_of, uint64_t* status,
+                                                       uint64_t* item_excl /*[SCAN_IPT]*/, uint64_t& grand_total) {
+  __shared__ uint64_t s_warp[8];
+  __shared__ uint64_t s_prefix;
+  const int64_t base = (int64_t)part * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+  uint64_t vals[SCAN_IPT];
+  uint64_t tsum = 0;
+#pragma unroll
+  for (int j = 0; j < SCAN_IPT; j++) {
+    const int64_t i = base + j;
+    vals[j] = i < n ? value_of(i) : 0;
+    tsum += vals[j];
+  }
+  uint64_t agg;
+  uint64_t texcl = block_exclusive_scan<uint64_t>(tsum, s_warp, agg);
+  if (threadIdx.x == 0) {
+    uint64_t excl = 0;
+    if (part == 0) {
+      st_relaxed(&status[0], SCAN_FLAG_INC | agg);
+    } else {
+      st_relaxed(&status[part], SCAN_FLAG_AGG | agg);
+      int p = part - 1;
+      while (true) {
+        uint64_t s = ld_relaxed(&status[p]);
+        uint64_t flag = s & ~SCAN_VALUE_MASK;
+        if (flag == 0) continue;
+        excl += s & SCAN_VALUE_MASK;
+        if (flag == SCAN_FLAG_INC) break;
+        p--;
+      }
+      st_relaxed(&status[part], SCAN_FLAG_INC | (excl + agg));
+    }
+    s_prefix = excl;
+  }
+  __syncthreads();
+  const uint64_t pre = s_prefix + texcl;
+  uint64_t run = pre;
+#pragma unroll
+  for (int j = 0; j < SCAN_IPT; j++) {
+    item_excl[j] = run;
+    run += vals[j];
+  }
+  grand_total = s_prefix + agg;
+  __syncthreads();
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K k, int shift) {
+  return (uint32_t)((k >> shift) & (K)(RADIX - 1));
+}
+
+// Histograms of `npasses` consecutive 8-bit digits starting at shift0.
+template <typename K>
+__global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ keys, const int64_t* count_ptr,
+                                                         int64_t cap, int shift0, int npasses, uint32_t* hist) {
+  __shared__ uint32_t sh[8][RADIX];
+  for (int i = threadIdx.x; i < 8 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  int64_t n = count_ptr ? *count_ptr : cap;
+  if (n > cap) n = cap;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    K k = keys[i];
+    for (int p = 0; p < npasses; p++) atomicAdd(&sh[p][digit_of<K>(k, shift0 + 8 * p)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npasses * RADIX; i += blockDim.x) {
+    uint32_t c = (&sh[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+template <typename K>
+struct RadixSmem {
+  K keys[RS_TILE];
+  uint32_t vals[RS_TILE];
+};
+
+// One stable LSD pass over the digit at `shift`.
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) radix_pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                                K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                                const int64_t* count_ptr, int64_t cap, int shift,
+                                                                const uint32_t* __restrict__ hist, uint32_t* status,
+                                                                uint32_t* part_ctr, int write_keys) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RadixSmem<K>& sm = *reinterpret_cast<RadixSmem<K>*>(smem_raw);
+  __shared__ uint32_t whist[RS_WARPS][RADIX];
+  __shared__ uint32_t s_digit_base[RADIX];
+  __shared__ uint32_t s_gstart[RADIX];
+  __shared__ uint32_t s_lstart[RADIX];
+  __shared__ uint32_t s_warp[8];
+  __shared__ int s_part;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t n = count_ptr ? *count_ptr : cap;
+  if (n > cap) n = cap;
+  const int nparts = (int)((n + RS_TILE - 1) / RS_TILE);
+  {
+    uint32_t tot;
+    uint32_t e = block_exclusive_scan<uint32_t>(hist[tid], s_warp, tot);
+    s_digit_base[tid] = e;
+  }
+  while (true) {
+    if (tid == 0) s_part = (int)atomicAdd(part_ctr, 1u);
+    for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const int part = s_part;
+    if (part >= nparts) break;
+    const int64_t base = (int64_t)part * RS_TILE;
+    const int tile_n = (int)tmin<int64_t>(RS_TILE, n - base);
+
+    K k[RS_IPT];
+    uint32_t v[RS_IPT];
+    uint32_t rank[RS_IPT];
+#pragma unroll
+    for (int j = 0; j < RS_IPT; j++) {
+      const int li = warp * (RS_IPT * 32) + j * 32 + lane;
+      if (li < tile_n) {
+        k[j] = kin[base + li];
+        v[j] = vin[base + li];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RS_IPT; j++) {
+      const int li = warp * (RS_IPT * 32) + j * 32 + lane;
+      const bool valid = li < tile_n;
+      const unsigned active = __ballot_sync(0xffffffffu, valid);
+      uint32_t d = 0, peers = 0, base_cnt = 0;
+      if (valid) {
+        d = digit_of<K>(k[j], shift);
+        peers = __match_any_sync(active, d);
+        base_cnt = whist[warp][d];
+        rank[j] = base_cnt + __popc(peers & lanemask_lt());
+      }
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1) whist[warp][d] = base_cnt + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps, block count
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; w++) {
+      uint32_t c = whist[w][tid];
+      whist[w][tid] = cnt;
+      cnt += c;
+    }
+    // decoupled look-back for this digit
+    {
+      uint32_t* st = status + (size_t)part * RADIX + tid;
+      uint32_t excl = 0;
+      if (part == 0) {
+        st_relaxed(st, RS_FLAG_INC | cnt);
+      } else {
+        st_relaxed(st, RS_FLAG_AGG | cnt);
+        int p = part - 1;
+        while (true) {
+          uint32_t s = ld_relaxed(status + (size_t)p * RADIX + tid);
+          uint32_t flag = s & ~RS_VALUE_MASK;
+          if (flag == 0) continue;
+          excl += s & RS_VALUE_MASK;
+          if (flag == RS_FLAG_INC) break;
+          p--;
+        }
+        st_relaxed(st, RS_FLAG_INC | (excl + cnt));
+      }
+      s_gstart[tid] = s_digit_base[tid] + excl;
+    }
+    {
+      uint32_t tot;
+      s_lstart[tid] = block_exclusive_scan<uint32_t>(cnt, s_warp, tot);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_IPT; j++) {
+      const int li = warp * (RS_IPT * 32) + j * 32 + lane;
+      if (li < tile_n) {
+        const uint32_t d = digit_of<K>(k[j], shift);
+        const uint32_t pos = s_lstart[d] + whist[warp][d] + rank[j];
+        sm.keys[pos] = k[j];
+        sm.vals[pos] = v[j];
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < tile_n; i += RS_THREADS) {
+      const K key = sm.keys[i];
+      const uint32_t d = digit_of<K>(key, shift);
+      const uint32_t out = s_gstart[d] + (uint32_t)i - s_lstart[d];
+      if (write_keys) kout[out] = key;
+      vout[out] = sm.vals[i];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace hgs

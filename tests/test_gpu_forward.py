@@ -1,0 +1,160 @@
+"""GPU parity of the forward path (libhgs.so) against the reference's golden
+vectors and the CPU oracle.  Bit-exact: kept set, tile counts, tile entry
+order, triangle ids / coverage, last-consumed indices.  Float outputs: the
+device computes in fp64 and stores colour/T/depth images in fp32, so they are
+checked at 1e-6 abs (north_star tolerance is 1e-4)."""
+
+import numpy as np
+import pytest
+import torch
+
+from _util import assert_close, golden_scene, load_golden
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["small_sh0", "small_sh1", "c1"]
+
+
+def dev_scene(gs, cam, mesh):
+    import paper_2506_06988_b200 as hgs
+    g = hgs.GaussianSet.from_any(gs)
+    c = hgs.Camera.from_any(cam)
+    m = hgs.TexturedMesh.from_any(mesh) if mesh is not None else None
+    return g, c, m
+
+
+@pytest.fixture(scope="module", params=CASES)
+def case(request, cuda_device):
+    d = load_golden(request.param)
+    return (request.param, d) + golden_scene(d)
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def test_project_matches_reference(case):
+    import paper_2506_06988_b200 as hgs
+    name, d, gs, cam, mesh = case
+    g, c, _ = dev_scene(gs, cam, mesh)
+    p = hgs.project(g, c)
+    assert np.array_equal(np_(p.kept), d["p_kept"])
+    for k in ("mean2d", "depth", "cov2d", "conic", "alpha", "color", "radius", "t_cam", "color_pre"):
+        assert_close(np_(getattr(p, k)), d["p_" + k], atol=1e-12, rtol=1e-12, what=k)
+
+
+def test_tiles_bit_exact(case):
+    import paper_2506_06988_b200 as hgs
+    name, d, gs, cam, mesh = case
+    g, c, _ = dev_scene(gs, cam, mesh)
+    p = hgs.project(g, c)
+    t = hgs.build_tiles(p, c.width, c.height)
+    assert np.array_equal(np_(t.tile_starts), d["t_starts"]), "tile_starts differ"
+    assert np.array_equal(np_(t.entries), d["t_entries"]), "entry order differs"
+
+
+def test_fragments_bit_exact(case):
+    from paper_2506_06988_b200 import meshraster as mr
+    name, d, gs, cam, mesh = case
+    if mesh is None:
+        pytest.skip("no mesh")
+    g, c, m = dev_scene(gs, cam, mesh)
+    fr = mr.rasterize_fragments(m, c)
+    assert np.array_equal(np_(fr.triangle_id), d["f_tri"]), "triangle ids differ"
+    assert_close(np_(fr.depth), d["f_depth"], atol=0, rtol=1e-15, what="depth")
+    assert_close(np_(fr.uv), d["f_uv"], atol=1e-15, what="uv")
+    if "f_bary" in d:
+        assert_close(np_(fr.bary), d["f_bary"], atol=1e-15, what="bary")
+    col = mr.sample_texture(m.texture, fr.uv, fr.triangle_id)
+    ref = orc.sample_texture(mesh.texture, d["f_uv"], d["f_tri"] >= 0)
+    assert_close(np_(col), ref, atol=1e-6, what="mesh colour (fp32 storage)")
+
+
+def test_forward_matches_reference(case):
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    name, d, gs, cam, mesh = case
+    g, c, m = dev_scene(gs, cam, mesh)
+    layer = mr.mesh_layer(m, c) if m is not None else None
+    out, ctx = hgs.render(g, c, background=d["bg"], mesh=layer)
+    assert np.array_equal(np_(ctx.last_consumed), d["r_last"]), "last-consumed index differs"
+    assert_close(np_(out.color), d["r_color"], atol=1e-6, what="color")
+    assert_close(np_(out.transmittance), d["r_t"], atol=1e-6, what="T")
+    assert_close(np_(out.depth), d["r_depth"], atol=1e-5, rtol=1e-6, what="depth")
+    assert_close(np_(ctx.final_t), d["r_t"], atol=1e-14, what="T fp64 state")
+    if "r0_color" in d:
+        out0, ctx0 = hgs.render(g, c, background=d["bg"], mesh=None)
+        assert np.array_equal(np_(ctx0.last_consumed), d["r0_last"])
+        assert_close(np_(out0.color), d["r0_color"], atol=1e-6, what="color (no mesh)")
+
+
+def test_render_is_deterministic(cuda_device):
+    import paper_2506_06988_b200 as hgs
+    d = load_golden("c1")
+    g, c, _ = dev_scene(*golden_scene(d))
+    a, _ = hgs.render(g, c)
+    b, _ = hgs.render(g, c)
+    assert torch.equal(a.color, b.color) and torch.equal(a.transmittance, b.transmittance)
+
+
+def test_empty_scene_is_background(cuda_device):
+    import paper_2506_06988_b200 as hgs
+    cam = hgs.Camera(60.0, 60.0, 16.0, 12.0, 32, 24, np.eye(4), 0.05, 100.0)
+    out, _ = hgs.render(hgs.GaussianSet.empty(), cam, background=(0.2, 0.4, 0.6))
+    assert np.allclose(np_(out.color), [0.2, 0.4, 0.6], atol=1e-7)
+    assert np.allclose(np_(out.transmittance), 1.0)
+    assert np.isnan(np_(out.depth)).all()
+
+
+def test_edge_cases(cuda_device):
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    d = load_golden("edge")
+    gs = hgs.GaussianSet(np.array([[0.1, 0, 3.0], [-0.1, 0, 3.0], [0, 0.1, 3.0]]), np.tile([1.0, 0, 0, 0], (3, 1)),
+                         np.full((3, 3), -1.0), np.zeros(3), np.zeros((3, 3)))
+    cam = hgs.Camera(60.0, 60.0, 32.0, 32.0, 64, 64, np.eye(4), 0.05, 100.0)
+    p = hgs.project(gs, cam)
+    t = hgs.build_tiles(p, 64, 64)
+    assert np.array_equal(np_(t.tile_starts), d["eq_starts"]) and np.array_equal(np_(t.entries), d["eq_entries"])
+    verts = np.array([[-1.0, -1.0, 2.0], [1.0, -1.0, 2.0], [1.0, 1.0, 2.0], [-1.0, 1.0, 2.0]])
+    tris = np.array([[0, 1, 2], [0, 2, 3]], dtype=np.int32)
+    uvs = np.array([[[0, 0], [1, 0], [1, 1]], [[0, 0], [1, 1], [0, 1]]], dtype=np.float64)
+    m = hgs.TexturedMesh(verts, tris, uvs, np.full((16, 16, 3), 0.25))
+    fr = mr.rasterize_fragments(m, hgs.Camera(32.0, 32.0, 16.0, 16.0, 32, 32, np.eye(4), 0.05, 100.0))
+    assert np.array_equal(np_(fr.triangle_id), d["se_tri"])
+    assert_close(np_(fr.bary), d["se_bary"], atol=0, what="shared-edge bary")
+    m2 = hgs.TexturedMesh(verts * np.array([3.0, 3.0, 1.0]), tris, uvs, np.full((8, 8, 3), 0.6))
+    fr = mr.rasterize_fragments(m2, hgs.Camera(30.0, 30.0, 16.0, 12.0, 32, 24, np.eye(4), 0.05, 100.0))
+    assert np.array_equal(np_(fr.triangle_id), d["fs_tri"])
+    soup = hgs.TexturedMesh(d["soup_v"].astype(np.float64), d["soup_f"])
+    fr = mr.rasterize_fragments(soup, hgs.Camera(43.2, 43.2, 24.0, 24.0, 48, 48, np.eye(4), 0.05, 100.0))
+    assert np.array_equal(np_(fr.triangle_id), d["soup_tri"])
+    assert_close(np_(fr.depth), d["soup_depth"], atol=0, what="soup depth")
+
+
+@pytest.mark.parametrize("cfg", ["c2"])
+def test_c2_matches_oracle(cfg, cuda_device):
+    """100k Gaussians + 20k-tri mesh, 640x480: device vs CPU oracle."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    from paper_2506_06988_b200 import synthetic as syn
+    sc = syn.make_config(cfg, seed=0)
+    cam = sc.cameras[0]
+    g, c, m = dev_scene(sc.gaussians, cam, sc.mesh)
+    p = orc.project(sc.gaussians, cam)
+    t = orc.build_tiles(p, cam.width, cam.height)
+    fr = orc.rasterize_fragments(sc.mesh.vertices, sc.mesh.triangles, sc.mesh.uvs, cam)
+    mc = orc.sample_texture(sc.mesh.texture, fr.uv, fr.valid)
+    color, depth, tt, last = orc.rasterize_forward(p, t, cam.width, cam.height, (0, 0, 0), orc.Mesh(mc, fr.depth, fr.triangle_id))
+    dp = hgs.project(g, c)
+    dt = hgs.build_tiles(dp, c.width, c.height)
+    assert np.array_equal(np_(dt.tile_starts), t.tile_starts)
+    assert np.array_equal(np_(dt.entries), t.entries)
+    dfr = mr.rasterize_fragments(m, c)
+    assert np.array_equal(np_(dfr.triangle_id), fr.triangle_id)
+    layer = mr.mesh_layer(m, c, dfr)
+    out, ctx = hgs.render(g, c, background=(0, 0, 0), mesh=layer)
+    assert np.array_equal(np_(ctx.last_consumed), last)
+    assert_close(np_(out.color), color, atol=1e-6, what="color")
+    assert_close(np_(out.transmittance), tt, atol=1e-6, what="T")
