@@ -157,6 +157,8 @@ typedef struct hgs_adam_group {
 const char* hgs_last_error(void);
 int hgs_abi_version(void);
 int hgs_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+/* number of kernels this library has launched (or enqueued into a graph) */
+int64_t hgs_kernel_launches(void);
 
 /* ---------------- splat forward ---------------- */
 

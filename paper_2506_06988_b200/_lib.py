@@ -90,6 +90,7 @@ SIGNATURES = {
     "hgs_last_error": (ctypes.c_char_p, []),
     "hgs_abi_version": (ctypes.c_int, []),
     "hgs_device_info": (ctypes.c_int, [_P(c_i32), _P(c_i32), _P(c_i32)]),
+    "hgs_kernel_launches": (c_i64, []),
     "hgs_preprocess": (ctypes.c_int, [c_void_p, c_i32, c_i32, _P(HGSGaussians), c_i32, _P(HGSProjected), c_void_p]),
     "hgs_tiles_scratch_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i32]),
     "hgs_build_tiles": (ctypes.c_int, [_P(HGSProjected), c_i64, _P(HGSTiles), c_void_p]),

@@ -4,9 +4,16 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
 namespace {
 thread_local char g_last_error[512] = "";
+std::atomic<long long> g_launches{0};
 }
+
+void hgs_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" int64_t hgs_kernel_launches(void) { return g_launches.load(); }
 
 int hgs_set_error(int code, const char* msg) {
   std::snprintf(g_last_error, sizeof(g_last_error), "%s", msg);

@@ -60,11 +60,15 @@ inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace hgs
 
+// Every kernel launch is followed by HGS_CHECK_LAUNCH(): it surfaces launch
+// errors and counts the launch (hgs_kernel_launches()).
 #define HGS_CHECK_LAUNCH()                                   \
   do {                                                       \
+    hgs_count_launch();                                      \
     cudaError_t _e = cudaGetLastError();                     \
     if (_e != cudaSuccess) return hgs_set_cuda_error(_e, __FILE__, __LINE__); \
   } while (0)
 
 int hgs_set_cuda_error(cudaError_t e, const char* file, int line);
 int hgs_set_error(int code, const char* msg);
+void hgs_count_launch();

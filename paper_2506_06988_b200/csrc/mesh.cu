@@ -292,10 +292,13 @@ extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int
     const int gf = ceil_div(mesh->n_faces, 256);
     raster_small_kernel<0><<<gf, 256, 0, st>>>(vproj, mesh->triangles, mesh->n_faces, width, height, cam, zbuf, idbuf,
                                               big_list, big_count);
+    HGS_CHECK_LAUNCH();
     raster_big_kernel<0><<<2 * NUM_SMS, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf, big_list,
                                                       big_count);
+    HGS_CHECK_LAUNCH();
     raster_small_kernel<1><<<gf, 256, 0, st>>>(vproj, mesh->triangles, mesh->n_faces, width, height, cam, zbuf, idbuf,
                                               big_list, big_count);
+    HGS_CHECK_LAUNCH();
     raster_big_kernel<1><<<2 * NUM_SMS, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf, big_list,
                                                       big_count);
     HGS_CHECK_LAUNCH();

@@ -1,0 +1,178 @@
+"""Preallocated frame engine: the whole hybrid frame (mesh raster + texture
+fetch + preprocess + tile binning + blend) enqueued on one stream with fixed
+buffer addresses, so it can be captured once into a CUDA graph and replayed
+per camera.  The functional API in splat.py / meshraster.py allocates per
+call like the reference; this is the serving / benchmark path and the
+forward half of the training step.
+
+All counts (visible rows M, tile entries K) stay on the device.  The entry
+buffer has a capacity; if a frame overflows it, counters[2] is set, and
+``check()`` (one tiny device->host read) grows the buffers -- callers
+re-render that frame.  ``frame(..., sync_check=True)`` does this
+automatically.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scene import CAMERA_BYTES, Camera, GaussianSet, TexturedMesh, camera_struct
+from .splat import (REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, TileBins, _c_f64_3, _stream_ptr,
+                    MASK_VARIANTS)
+
+
+class HybridRenderer:
+    def __init__(self, gs: GaussianSet, mesh: Optional[TexturedMesh], width: int, height: int,
+                 background=(0.0, 0.0, 0.0), capacity: Optional[int] = None, keep_state: bool = False,
+                 mask=None, collect_stats: bool = False):
+        self.gs = gs
+        self.mesh = mesh
+        self.width, self.height = int(width), int(height)
+        self.dev = gs.device
+        self.bg = np.asarray(background, dtype=np.float64).reshape(3)
+        self.tiles_x = (self.width + TILE_PX - 1) // TILE_PX
+        self.tiles_y = (self.height + TILE_PX - 1) // TILE_PX
+        self.n_tiles = self.tiles_x * self.tiles_y
+        self.keep_state = keep_state
+        self.mask = mask
+        dev = self.dev
+        n = max(len(gs), 1)
+        h, w = self.height, self.width
+        self.cam_dev = torch.zeros(CAMERA_BYTES, dtype=torch.uint8, device=dev)
+        self.cam_host = torch.zeros(CAMERA_BYTES, dtype=torch.uint8).pin_memory()
+        self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
+        self.count = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
+        self.tile_starts = torch.zeros(self.n_tiles + 1, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.counters_host = torch.zeros(4, dtype=torch.int64).pin_memory()
+        self.color = torch.empty(h, w, 3, dtype=torch.float32, device=dev)
+        self.depth = torch.empty(h, w, dtype=torch.float32, device=dev)
+        self.trans = torch.empty(h, w, dtype=torch.float32, device=dev)
+        self.final_t = torch.empty(h, w, dtype=torch.float64, device=dev) if keep_state else None
+        self.last = torch.empty(h, w, dtype=torch.int32, device=dev) if keep_state else None
+        self.mask_out = torch.empty(h, w, dtype=torch.float32, device=dev) if mask is not None else None
+        self.stats = torch.zeros(2, dtype=torch.int64, device=dev) if collect_stats else None
+        if mesh is not None:
+            self.frag_tri = torch.empty(h, w, dtype=torch.int32, device=dev)
+            self.frag_depth = torch.empty(h, w, dtype=torch.float64, device=dev)
+            self.frag_uv = torch.empty(h, w, 2, dtype=torch.float64, device=dev)
+            self.mesh_color = torch.empty(h, w, 3, dtype=torch.float32, device=dev)
+            nbytes = _lib.load().hgs_raster_scratch_bytes(len(mesh.vertices), mesh.n_faces, w, h)
+            self.raster_scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.capacity = 0
+        self._alloc_entries(capacity if capacity is not None else 16 * n)
+        self.graph = None
+
+    # ------------------------------------------------------------------
+    def _alloc_entries(self, capacity: int):
+        capacity = max(int(capacity), 1024)
+        self.capacity = capacity
+        self.entries = torch.empty(capacity, dtype=torch.int32, device=self.dev)
+        nbytes = _lib.load().hgs_tiles_scratch_bytes(len(self.gs), capacity, self.n_tiles)
+        self.tiles_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        self.graph = None
+
+    def set_camera(self, cam) -> None:
+        """H2D of the 200-byte camera struct from pinned memory (async)."""
+        s = camera_struct(cam)
+        raw = np.frombuffer(bytes(s), dtype=np.uint8)
+        self.cam_host.numpy()[:len(raw)] = raw
+        self.cam_dev.copy_(self.cam_host, non_blocking=True)
+
+    def _structs(self):
+        ps = _lib.HGSProjected()
+        ps.rec, ps.count, ps.rect = _lib.ptr(self.rec), _lib.ptr(self.count), _lib.ptr(self.rect)
+        ts = _lib.HGSTiles()
+        ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tiles_x, self.tiles_y, TILE_PX, self.capacity
+        ts.entries, ts.tile_starts, ts.counters = _lib.ptr(self.entries), _lib.ptr(self.tile_starts), _lib.ptr(self.counters)
+        ts.scratch, ts.scratch_bytes = _lib.ptr(self.tiles_scratch), self.tiles_scratch.numel()
+        return ps, ts
+
+    def enqueue(self, rasterize_mesh: bool = True, mesh_layer: Optional[MeshLayer] = None) -> None:
+        """Enqueue one frame for the camera currently in cam_dev."""
+        L = _lib.load()
+        st = _stream_ptr(self.dev)
+        w, h = self.width, self.height
+        ml = _lib.HGSMeshLayer()
+        if self.mesh is not None and mesh_layer is None:
+            if rasterize_mesh:
+                fr = _lib.HGSFragments()
+                fr.triangle_id, fr.depth, fr.uv = _lib.ptr(self.frag_tri), _lib.ptr(self.frag_depth), _lib.ptr(self.frag_uv)
+                _lib.check(L.hgs_rasterize_fragments(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.mesh.struct()),
+                                                     ctypes.byref(fr), _lib.ptr(self.raster_scratch),
+                                                     self.raster_scratch.numel(), st), "rasterize_fragments")
+            tex = self.mesh.texture
+            _lib.check(L.hgs_sample_texture(_lib.ptr(tex), tex.shape[0], tex.shape[1], _lib.ptr(self.frag_uv),
+                                            _lib.ptr(self.frag_tri), w * h, _lib.ptr(self.mesh_color), st),
+                       "sample_texture")
+            ml.color, ml.depth, ml.triangle_id = _lib.ptr(self.mesh_color), _lib.ptr(self.frag_depth), _lib.ptr(self.frag_tri)
+        elif mesh_layer is not None:
+            ml = mesh_layer.struct()
+        ps, ts = self._structs()
+        _lib.check(L.hgs_preprocess(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.gs.struct()), TILE_PX,
+                                    ctypes.byref(ps), st), "preprocess")
+        _lib.check(L.hgs_build_tiles(ctypes.byref(ps), len(self.gs), ctypes.byref(ts), st), "build_tiles")
+        out = _lib.HGSBlendOut()
+        out.color, out.depth, out.transmittance = _lib.ptr(self.color), _lib.ptr(self.depth), _lib.ptr(self.trans)
+        out.final_t, out.last = _lib.ptr(self.final_t), _lib.ptr(self.last)
+        variant, k = 0, 20.0
+        if self.mask is not None:
+            variant, k = MASK_VARIANTS[self.mask[0]], float(self.mask[1])
+            out.mask = _lib.ptr(self.mask_out)
+        out.stats = _lib.ptr(self.stats)
+        _lib.check(L.hgs_blend_forward(ctypes.byref(ps), ctypes.byref(ts), w, h, ctypes.byref(ml), _c_f64_3(self.bg),
+                                       variant, k, ctypes.byref(out), st), "blend_forward")
+
+    def check(self) -> tuple:
+        """(M, K, overflow); grows the entry buffer on overflow."""
+        self.counters_host.copy_(self.counters, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        m, k, ovf = (int(x) for x in self.counters_host[:3])
+        if ovf:
+            self._alloc_entries(int(k * 1.25) + 1024)
+        return m, k, bool(ovf)
+
+    def frame(self, cam, rasterize_mesh: bool = True, sync_check: bool = True):
+        self.set_camera(cam)
+        while True:
+            self.enqueue(rasterize_mesh)
+            if not sync_check:
+                return
+            _, _, ovf = self.check()
+            if not ovf:
+                return
+
+    # CUDA graph of one frame (camera read from cam_dev at replay time) --------
+    def capture(self, rasterize_mesh: bool = True) -> None:
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            self.enqueue(rasterize_mesh)  # warm (lazy attributes, occupancy queries)
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.enqueue(rasterize_mesh)
+        self.graph = g
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    # views for the API / backward ----------------------------------------
+    def projected(self) -> ProjectedGaussians:
+        return ProjectedGaussians(len(self.gs), self.rec, self.count[:len(self.gs)], self.rect, None, self.width,
+                                  self.height)
+
+    def tiles(self) -> TileBins:
+        return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected())
+
+    def layer(self) -> Optional[MeshLayer]:
+        if self.mesh is None:
+            return None
+        return MeshLayer(self.mesh_color, self.frag_depth, self.frag_tri)
