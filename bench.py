@@ -232,6 +232,7 @@ def run_ours(args):
         out = _lib.HGSBlendOut()
         out.color, out.depth, out.transmittance = _lib.ptr(r.color), _lib.ptr(r.depth), _lib.ptr(r.trans)
         out.stats = _lib.ptr(r.stats) if i == 0 else None
+        out.fixup = _lib.ptr(r.fixup)
         _lib.check(L.hgs_blend_forward(ctypes.byref(ps), ctypes.byref(ts), W, H, ctypes.byref(ml),
                                        _c_f64_3(np.zeros(3)), 0, 20.0, ctypes.byref(out), stream.cuda_stream))
         ev[2].record(stream)

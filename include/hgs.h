@@ -89,6 +89,8 @@ typedef struct hgs_projected {
   double* color_pre; /* N x 3, optional */
   double* view_dir;  /* N x 3, optional (SH degree 1 only) */
   double* view_dist; /* N, optional (SH degree 1 only) */
+  void* cull;        /* N x 16 B fp32 {mean x, mean y, 3-sigma half extents x, y}: blend culling records
+                        (optional; without it hgs_blend_forward runs the exact per-pixel walk only) */
 } hgs_projected;
 
 /* TileBins (splat/tiles.py:19-32).  entries hold ORIGINAL Gaussian rows in
@@ -122,6 +124,8 @@ typedef struct hgs_blend_out {
   int32_t* last;        /* H x W global entry index or -1 (may be NULL) */
   float* mask;          /* H x W transmittance_mask(T) (losses.py:79-91), may be NULL */
   int64_t* stats;       /* device int64[2]: += evaluations walked, += blended (may be NULL) */
+  int32_t* fixup;       /* device int32[H*W + 1] work list of pixels the fast path hands to the exact fp64
+                           walk (may be NULL: exact walk for every pixel) */
 } hgs_blend_out;
 
 /* TexturedMesh geometry (scene.py:206-237). */

@@ -50,7 +50,7 @@ class HGSGaussianGrads(ctypes.Structure):
 class HGSProjected(ctypes.Structure):
     _fields_ = [("rec", c_void_p), ("count", c_void_p), ("rect", c_void_p), ("cov2d", c_void_p),
                 ("radius", c_void_p), ("t_cam", c_void_p), ("color_pre", c_void_p), ("view_dir", c_void_p),
-                ("view_dist", c_void_p)]
+                ("view_dist", c_void_p), ("cull", c_void_p)]
 
 
 class HGSTiles(ctypes.Structure):
@@ -65,7 +65,7 @@ class HGSMeshLayer(ctypes.Structure):
 
 class HGSBlendOut(ctypes.Structure):
     _fields_ = [("color", c_void_p), ("depth", c_void_p), ("transmittance", c_void_p), ("final_t", c_void_p),
-                ("last", c_void_p), ("mask", c_void_p), ("stats", c_void_p)]
+                ("last", c_void_p), ("mask", c_void_p), ("stats", c_void_p), ("fixup", c_void_p)]
 
 
 class HGSMesh(ctypes.Structure):

@@ -11,13 +11,15 @@
 //   pass 1: fragments whose z equals the minimum do atomicMin(idbuf[p], f);
 //   resolve: one thread per pixel recomputes the winner's barycentrics,
 //           depth and uv with the reference's arithmetic (fp64, no FMA).
-// Triangles with small screen bounding boxes are rasterized one thread per
-// triangle; large ones are deferred to a CTA-per-triangle kernel.
+// Work is binned by screen bounding-box area: tiny triangles one thread
+// each, medium ones one warp each (lanes stride the box), large ones one
+// CTA each; the bins are built in pass 0 and reused by pass 1.
 #include "common.cuh"
 
 namespace hgs {
 
-constexpr int BIG_TRI_PIXELS = 1024;
+constexpr int SMALL_TRI_PIXELS = 32;
+constexpr int BIG_TRI_PIXELS = 4096;
 
 struct TriSetup {
   double ax, ay, bx, by, cx, cy;  // after winding normalisation
@@ -112,35 +114,42 @@ template <int PASS>
 __global__ void __launch_bounds__(256) raster_small_kernel(const double3* __restrict__ vproj,
                                                            const int32_t* __restrict__ tris, int64_t nf, int width,
                                                            int height, const hgs_camera* __restrict__ cam,
-                                                           unsigned long long* zbuf, int32_t* idbuf, int32_t* big_list,
-                                                           int32_t* big_count) {
+                                                           unsigned long long* zbuf, int32_t* idbuf, int32_t* lists,
+                                                           int32_t* list_counts) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   TriSetup t;
   if (!tri_setup(vproj, tris, f, width, height, cam->near_, t)) return;
   const int64_t area = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
-  if (area > BIG_TRI_PIXELS) {
-    if (PASS == 0) big_list[atomicAdd(big_count, 1)] = (int32_t)f;
+  if (area > SMALL_TRI_PIXELS) {
+    if (PASS == 0) {
+      const int which = area > BIG_TRI_PIXELS ? 1 : 0;  // 0: warp list, 1: CTA list
+      lists[which * nf + atomicAdd(&list_counts[which], 1)] = (int32_t)f;
+    }
     return;
   }
   for (int py = t.y0; py <= t.y1; py++)
     for (int px = t.x0; px <= t.x1; px++) raster_pixel<PASS>(t, f, px, py, width, zbuf, idbuf);
 }
 
-template <int PASS>
-__global__ void __launch_bounds__(256) raster_big_kernel(const double3* __restrict__ vproj,
-                                                         const int32_t* __restrict__ tris, int width, int height,
-                                                         const hgs_camera* __restrict__ cam, unsigned long long* zbuf,
-                                                         int32_t* idbuf, const int32_t* big_list,
-                                                         const int32_t* big_count) {
-  const int nbig = *big_count;
-  for (int b = blockIdx.x; b < nbig; b += gridDim.x) {
-    const int64_t f = big_list[b];
+// GROUP threads per triangle (32: one warp; 256: one CTA), striding the box.
+template <int PASS, int GROUP>
+__global__ void __launch_bounds__(256) raster_group_kernel(const double3* __restrict__ vproj,
+                                                           const int32_t* __restrict__ tris, int width, int height,
+                                                           const hgs_camera* __restrict__ cam,
+                                                           unsigned long long* zbuf, int32_t* idbuf,
+                                                           const int32_t* list, const int32_t* list_count) {
+  const int nlist = *list_count;
+  const int groups_per_block = 256 / GROUP;
+  const int gid = blockIdx.x * groups_per_block + threadIdx.x / GROUP;
+  const int r = threadIdx.x % GROUP;
+  for (int b = gid; b < nlist; b += gridDim.x * groups_per_block) {
+    const int64_t f = list[b];
     TriSetup t;
     if (!tri_setup(vproj, tris, f, width, height, cam->near_, t)) continue;
     const int bw = t.x1 - t.x0 + 1;
     const int64_t area = (int64_t)bw * (t.y1 - t.y0 + 1);
-    for (int64_t q = threadIdx.x; q < area; q += blockDim.x)
+    for (int64_t q = r; q < area; q += GROUP)
       raster_pixel<PASS>(t, f, t.x0 + (int)(q % bw), t.y0 + (int)(q / bw), width, zbuf, idbuf);
   }
 }
@@ -258,7 +267,7 @@ extern "C" size_t hgs_raster_scratch_bytes(int64_t n_vertices, int64_t n_faces, 
   const int64_t npix = (int64_t)width * height;
   return align_up(sizeof(double3) * (size_t)(n_vertices > 0 ? n_vertices : 1), 256) +
          align_up(8 * (size_t)npix, 256) + align_up(4 * (size_t)npix, 256) +
-         align_up(4 * (size_t)(n_faces > 0 ? n_faces : 1), 256) + 256;
+         align_up(8 * (size_t)(n_faces > 0 ? n_faces : 1), 256) + 256;
 }
 
 extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int32_t height, const hgs_mesh* mesh,
@@ -279,10 +288,10 @@ extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int
   base += align_up(8 * (size_t)npix, 256);
   int32_t* idbuf = (int32_t*)base;
   base += align_up(4 * (size_t)npix, 256);
-  int32_t* big_list = (int32_t*)base;
-  base += align_up(4 * (size_t)(mesh->n_faces > 0 ? mesh->n_faces : 1), 256);
-  int32_t* big_count = (int32_t*)base;
-  cudaMemsetAsync(big_count, 0, sizeof(int32_t), st);
+  int32_t* lists = (int32_t*)base;  // [warp list | CTA list], n_faces each
+  base += align_up(8 * (size_t)(mesh->n_faces > 0 ? mesh->n_faces : 1), 256);
+  int32_t* list_counts = (int32_t*)base;
+  cudaMemsetAsync(list_counts, 0, 2 * sizeof(int32_t), st);
   raster_init_kernel<<<ceil_div(npix, 256), 256, 0, st>>>(zbuf, idbuf, npix);
   HGS_CHECK_LAUNCH();
   if (mesh->n_faces > 0) {
@@ -290,17 +299,30 @@ extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int
     mesh_project_kernel<<<ceil_div(mesh->n_vertices, 256), 256, 0, st>>>(cam, mesh->vertices, mesh->n_vertices, vproj);
     HGS_CHECK_LAUNCH();
     const int gf = ceil_div(mesh->n_faces, 256);
-    raster_small_kernel<0><<<gf, 256, 0, st>>>(vproj, mesh->triangles, mesh->n_faces, width, height, cam, zbuf, idbuf,
-                                              big_list, big_count);
+    const int64_t nf = mesh->n_faces;
+    int sms = NUM_SMS;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    raster_small_kernel<0><<<gf, 256, 0, st>>>(vproj, mesh->triangles, nf, width, height, cam, zbuf, idbuf, lists,
+                                              list_counts);
     HGS_CHECK_LAUNCH();
-    raster_big_kernel<0><<<2 * NUM_SMS, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf, big_list,
-                                                      big_count);
+    raster_group_kernel<0, 32><<<8 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
+                                                        lists, list_counts);
     HGS_CHECK_LAUNCH();
-    raster_small_kernel<1><<<gf, 256, 0, st>>>(vproj, mesh->triangles, mesh->n_faces, width, height, cam, zbuf, idbuf,
-                                              big_list, big_count);
+    raster_group_kernel<0, 256><<<2 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
+                                                         lists + nf, list_counts + 1);
     HGS_CHECK_LAUNCH();
-    raster_big_kernel<1><<<2 * NUM_SMS, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf, big_list,
-                                                      big_count);
+    raster_small_kernel<1><<<gf, 256, 0, st>>>(vproj, mesh->triangles, nf, width, height, cam, zbuf, idbuf, lists,
+                                              list_counts);
+    HGS_CHECK_LAUNCH();
+    raster_group_kernel<1, 32><<<8 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
+                                                        lists, list_counts);
+    HGS_CHECK_LAUNCH();
+    raster_group_kernel<1, 256><<<2 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
+                                                         lists + nf, list_counts + 1);
     HGS_CHECK_LAUNCH();
   }
   raster_resolve_kernel<<<ceil_div(npix, 256), 256, 0, st>>>(vproj, mesh->triangles, mesh->uvs, width, height, cam,

@@ -135,6 +135,13 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const hgs_camera* __res
   out.count[i] = cnt;
   reinterpret_cast<ushort4*>(out.rect)[i] = rc;
 
+  if (out.cull) {
+    // conservative extents of the m <= 9 ellipse (|dx| <= 3 sqrt(cov_xx)), inflated for the fp32 compare
+    const float slack = 1e-3f + 2.5e-7f * (float)(fabs(mx) + fabs(my));
+    const float ex = (float)(3.0 * sqrt(cxx)) * (1.0f + 1e-5f) + slack;
+    const float ey = (float)(3.0 * sqrt(cyy)) * (1.0f + 1e-5f) + slack;
+    reinterpret_cast<float4*>(out.cull)[i] = make_float4((float)mx, (float)my, ok ? ex : -1.0f, ok ? ey : -1.0f);
+  }
   if (out.cov2d) { out.cov2d[3 * i] = cxx; out.cov2d[3 * i + 1] = cxy; out.cov2d[3 * i + 2] = cyy; }
   if (out.radius) out.radius[i] = radius;
   if (out.t_cam) { out.t_cam[3 * i] = t[0]; out.t_cam[3 * i + 1] = t[1]; out.t_cam[3 * i + 2] = t[2]; }

@@ -29,6 +29,7 @@ constexpr uint64_t SCAN_FLAG_AGG = 1ull << 62;
 constexpr uint64_t SCAN_FLAG_INC = 2ull << 62;
 constexpr uint64_t SCAN_VALUE_MASK = (1ull << 62) - 1;
 
+constexpr uint32_t SPIN_LIMIT = 1u << 24;
 constexpr uint32_t RS_FLAG_AGG = 1u << 30;
 constexpr uint32_t RS_FLAG_INC = 2u << 30;
 constexpr uint32_t RS_VALUE_MASK = (1u << 30) - 1;
@@ -97,24 +98,34 @@ __device__ __forceinline__ void chained_scan_partition(int part, int64_t n, F va
   }
   uint64_t agg;
   uint64_t texcl = block_exclusive_scan<uint64_t>(tsum, s_warp, agg);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-wide decoupled look-back: 32 predecessors per round trip
+    const int lane = threadIdx.x;
     uint64_t excl = 0;
     if (part == 0) {
-      st_relaxed(&status[0], SCAN_FLAG_INC | agg);
+      if (lane == 0) st_relaxed(&status[0], SCAN_FLAG_INC | agg);
     } else {
-      st_relaxed(&status[part], SCAN_FLAG_AGG | agg);
+      if (lane == 0) st_relaxed(&status[part], SCAN_FLAG_AGG | agg);
       int p = part - 1;
-      while (true) {
-        uint64_t s = ld_relaxed(&status[p]);
-        uint64_t flag = s & ~SCAN_VALUE_MASK;
-        if (flag == 0) continue;
-        excl += s & SCAN_VALUE_MASK;
-        if (flag == SCAN_FLAG_INC) break;
-        p--;
+      for (uint32_t spin = 0; spin <= SPIN_LIMIT; spin++) {  // watchdog: never hang the GPU
+        const int q = p - lane;
+        const uint64_t sv = q >= 0 ? ld_relaxed(&status[q]) : SCAN_FLAG_INC;
+        const uint64_t flag = sv & ~SCAN_VALUE_MASK;
+        const unsigned notready = __ballot_sync(0xffffffffu, flag == 0);
+        const unsigned inc = __ballot_sync(0xffffffffu, flag == SCAN_FLAG_INC);
+        const int first_inc = inc ? __ffs(inc) - 1 : 32;
+        const int first_nr = notready ? __ffs(notready) - 1 : 32;
+        const int take = first_nr < first_inc ? first_nr : (first_inc < 32 ? first_inc + 1 : 32);
+        uint64_t v = lane < take ? (sv & SCAN_VALUE_MASK) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (first_inc < first_nr && first_inc < 32) break;
+        p -= take;
       }
-      st_relaxed(&status[part], SCAN_FLAG_INC | (excl + agg));
+      if (lane == 0) st_relaxed(&status[part], SCAN_FLAG_INC | (excl + agg));
     }
-    s_prefix = excl;
+    if (lane == 0) s_prefix = excl;
   }
   __syncthreads();
   const uint64_t pre = s_prefix + texcl;
@@ -142,8 +153,12 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ k
   __syncthreads();
   int64_t n = count_ptr ? *count_ptr : cap;
   if (n > cap) n = cap;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    K k = keys[i];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nround = (n + stride - 1) / stride * stride;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nround; i += stride) {
+    const bool valid = i < n;
+    const K k = valid ? keys[i] : K(0);
+    if (!valid) continue;
     for (int p = 0; p < npasses; p++) atomicAdd(&sh[p][digit_of<K>(k, shift0 + 8 * p)], 1u);
   }
   __syncthreads();
@@ -161,11 +176,11 @@ struct RadixSmem {
 
 // One stable LSD pass over the digit at `shift`.
 template <typename K>
-__global__ void __launch_bounds__(RS_THREADS) radix_pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 8 ? 2 : 3) radix_pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                                 K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                                 const int64_t* count_ptr, int64_t cap, int shift,
                                                                 const uint32_t* __restrict__ hist, uint32_t* status,
-                                                                uint32_t* part_ctr, int write_keys) {
+                                                                int nparts_cap, uint32_t* part_ctr, int write_keys) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RadixSmem<K>& sm = *reinterpret_cast<RadixSmem<K>*>(smem_raw);
   __shared__ uint32_t whist[RS_WARPS][RADIX];
@@ -229,24 +244,40 @@ __global__ void __launch_bounds__(RS_THREADS) radix_pass_kernel(const K* __restr
       whist[w][tid] = cnt;
       cnt += c;
     }
-    // decoupled look-back for this digit
+    // decoupled look-back for this digit: status is [partition][digit] (a
+    // warp's 32 digits are one 128 B line); each round trip reads a window of
+    // 16 predecessors (independent coalesced loads)
     {
-      uint32_t* st = status + (size_t)part * RADIX + tid;
+      uint32_t* st = status + tid;
       uint32_t excl = 0;
       if (part == 0) {
         st_relaxed(st, RS_FLAG_INC | cnt);
       } else {
-        st_relaxed(st, RS_FLAG_AGG | cnt);
+        st_relaxed(st + (size_t)part * RADIX, RS_FLAG_AGG | cnt);
         int p = part - 1;
-        while (true) {
-          uint32_t s = ld_relaxed(status + (size_t)p * RADIX + tid);
-          uint32_t flag = s & ~RS_VALUE_MASK;
-          if (flag == 0) continue;
-          excl += s & RS_VALUE_MASK;
-          if (flag == RS_FLAG_INC) break;
-          p--;
+        bool fin = false;
+        while (!fin) {
+          // wait (one load per poll) until the nearest unread predecessor is
+          // published, then read a window of 16 and consume its ready prefix
+          for (uint32_t spin = 0; (ld_relaxed(st + (size_t)p * RADIX) & ~RS_VALUE_MASK) == 0; spin++)
+            if (spin > SPIN_LIMIT) { fin = true; break; }  // watchdog: never hang the GPU
+          if (fin) break;
+          uint32_t w[16];
+#pragma unroll
+          for (int k = 0; k < 16; k++) w[k] = (p - k >= 0) ? ld_relaxed(st + (size_t)(p - k) * RADIX) : RS_FLAG_INC;
+          int used = 0;
+#pragma unroll
+          for (int k = 0; k < 16; k++) {
+            if (fin || used < k) continue;  // stopped earlier in this window
+            const uint32_t flag = w[k] & ~RS_VALUE_MASK;
+            if (flag == 0) continue;        // not ready: re-read from here
+            excl += w[k] & RS_VALUE_MASK;
+            used = k + 1;
+            if (flag == RS_FLAG_INC) fin = true;
+          }
+          p -= used;
         }
-        st_relaxed(st, RS_FLAG_INC | (excl + cnt));
+        st_relaxed(st + (size_t)part * RADIX, RS_FLAG_INC | (excl + cnt));
       }
       s_gstart[tid] = s_digit_base[tid] + excl;
     }

@@ -2,24 +2,39 @@
 //
 // The reference orders tile entries with np.lexsort((kept, depth, tile))
 // (tiles.py:65).  Here:
-//   1. compact the visible rows (count > 0) in row order       (chained scan)
-//   2. sort them by the fp64 depth bit pattern, stably         (8 LSD passes)
-//      -> visible rows in (depth, row) order
-//   3. exclusive scan of their tile counts in that order        (chained scan)
-//   4. emit (tile id, row) pairs in depth order                 (1 thread/row)
-//   5. stable LSD sort by tile id (1-2 passes of 8 bits)
-//      -> (tile, depth, row) order == the reference's lexsort, exactly
-//   6. CSR tile ranges from the sorted tile ids.
+//   1. compact the visible rows (count > 0) in row order (chained scan) and
+//      add each row's tile rectangle into a 2D difference grid
+//   2. per-tile entry counts = 2D prefix sums of that grid; their exclusive
+//      scan is the CSR tile_starts (and K); the tile-key digit histograms
+//      follow from the counts                                    (1 CTA)
+//   3. sort the visible rows by the fp64 depth bit pattern, stably
+//      (8 LSD passes) -> rows in (depth, row) order
+//   4. exclusive scan of their tile counts in that order (chained scan)
+//   5. emit (tile id, row) pairs in depth order (warp-cooperative,
+//      coalesced: one warp spreads 32 rows' rectangles over its lanes)
+//   6. stable LSD sort by tile id (1-2 passes of 8 bits)
+//      -> (tile, depth, row) order == the reference's lexsort, exactly.
 // Positive doubles order like their IEEE bit patterns, so step 2 is exact.
 #include "sort.cuh"
 
 namespace hgs {
 
+constexpr int DIFF_SMEM_CELLS = 12288;  // 48 KB of int counters
+
 __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const int32_t* __restrict__ count,
-                                                               const BlendRec* __restrict__ rec, int64_t n,
-                                                               uint64_t* dkeys, uint32_t* dvals, uint64_t* status,
-                                                               uint32_t* part_ctr, int64_t* counters) {
+                                                               const BlendRec* __restrict__ rec,
+                                                               const ushort4* __restrict__ rect, int64_t n,
+                                                               int tiles_x, int tiles_y, uint64_t* dkeys,
+                                                               uint32_t* dvals, uint64_t* status, uint32_t* part_ctr,
+                                                               int64_t* counters, int* diff) {
   __shared__ int s_part;
+  extern __shared__ int s_diff[];
+  const int gw = tiles_x + 1, cells = (tiles_x + 1) * (tiles_y + 1);
+  const bool local = cells <= DIFF_SMEM_CELLS;
+  if (local)
+    for (int c = threadIdx.x; c < cells; c += blockDim.x) s_diff[c] = 0;
+  __syncthreads();
+  int* dst = local ? s_diff : diff;
   const int nparts = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
   while (true) {
     if (threadIdx.x == 0) s_part = (int)atomicAdd(part_ctr, 1u);
@@ -38,10 +53,72 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const int32_t* __
       if (i < n && count[i] > 0) {
         dkeys[excl[j]] = (uint64_t)__double_as_longlong(rec[i].depth);
         dvals[excl[j]] = (uint32_t)i;
+        const ushort4 rc = rect[i];  // x0, x1, y0, y1
+        atomicAdd(&dst[rc.z * gw + rc.x], 1);
+        atomicAdd(&dst[rc.z * gw + rc.y + 1], -1);
+        atomicAdd(&dst[(rc.w + 1) * gw + rc.x], -1);
+        atomicAdd(&dst[(rc.w + 1) * gw + rc.y + 1], 1);
       }
     }
     if (part == nparts - 1 && threadIdx.x == 0) counters[0] = (int64_t)total;
   }
+  if (local) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < cells; c += blockDim.x)
+      if (s_diff[c]) atomicAdd(&diff[c], s_diff[c]);
+  }
+}
+
+// Per-tile counts from the difference grid (2D inclusive prefix sums), the
+// CSR starts (exclusive scan), K, the overflow flag, and the digit
+// histograms of the tile keys for the LSD passes.  One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) tile_counts_kernel(int* diff, int tiles_x, int tiles_y, int64_t capacity,
+                                                           int64_t* tile_starts, int64_t* counters, uint32_t* hist) {
+  __shared__ uint32_t sh[2][RADIX];
+  __shared__ int64_t s_chunk[1024];
+  const int gw = tiles_x + 1;
+  const int n_tiles = tiles_x * tiles_y;
+  for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  // row prefix (along x), one thread per row
+  for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {
+    int run = 0;
+    for (int x = 0; x < tiles_x; x++) { run += diff[y * gw + x]; diff[y * gw + x] = run; }
+  }
+  __syncthreads();
+  // column prefix (along y), one thread per column
+  for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
+    int run = 0;
+    for (int y = 0; y < tiles_y; y++) { run += diff[y * gw + x]; diff[y * gw + x] = run; }
+  }
+  __syncthreads();
+  // exclusive scan of counts in tile order: contiguous chunk per thread
+  const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
+  const int t0 = threadIdx.x * per, t1 = min(n_tiles, t0 + per);
+  int64_t local_sum = 0;
+  for (int t = t0; t < t1; t++) {
+    const int c = diff[(t / tiles_x) * gw + t % tiles_x];
+    local_sum += c;
+    if (c) {
+      atomicAdd(&sh[0][t & 255], (uint32_t)c);
+      atomicAdd(&sh[1][(t >> 8) & 255], (uint32_t)c);
+    }
+  }
+  s_chunk[threadIdx.x] = local_sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; i++) { const int64_t v = s_chunk[i]; s_chunk[i] = run; run += v; }
+    counters[1] = run;
+    counters[2] = run > capacity ? 1 : 0;
+    tile_starts[n_tiles] = run;
+  }
+  __syncthreads();
+  int64_t run = s_chunk[threadIdx.x];
+  for (int t = t0; t < t1; t++) {
+    tile_starts[t] = run;
+    run += diff[(t / tiles_x) * gw + t % tiles_x];
+  }
+  for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) hist[i] = (&sh[0][0])[i];
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) offsets_kernel(const int32_t* __restrict__ count,
@@ -52,10 +129,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) offsets_kernel(const int32_t* __
   __shared__ int s_part;
   const int64_t m = counters_in[0];
   const int nparts = (int)((m + SCAN_TILE - 1) / SCAN_TILE);
-  if (m == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) counters[1] = 0;
-    return;
-  }
+  if (m == 0) return;
   while (true) {
     if (threadIdx.x == 0) s_part = (int)atomicAdd(part_ctr, 1u);
     __syncthreads();
@@ -70,52 +144,62 @@ __global__ void __launch_bounds__(SCAN_THREADS) offsets_kernel(const int32_t* __
 #pragma unroll
     for (int j = 0; j < SCAN_IPT; j++)
       if (base + j < m) offsets[base + j] = (uint32_t)tmin<uint64_t>(excl[j], 0xffffffffull);
-    if (part == nparts - 1 && threadIdx.x == 0) {
-      counters[1] = (int64_t)total;
-      counters[2] = (int64_t)total > capacity ? 1 : 0;
-    }
+    (void)total;
+    (void)capacity;
   }
 }
 
-// One thread per visible row in depth order; writes its tile ids row-major
-// over the rectangle (the order inside one row is irrelevant: distinct keys).
+// Warp-cooperative emission: a warp owns 32 consecutive rows of the depth
+// order; their entries are contiguous in the output, so lanes stride over
+// that span (coalesced stores), each finding its owning row by a binary
+// search over the 32 row offsets held in shared memory.
 template <typename TK>
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ sorted_rows,
                                                    const uint32_t* __restrict__ offsets,
                                                    const ushort4* __restrict__ rect, const int64_t* counters,
                                                    int tiles_x, int64_t capacity, TK* tkeys, uint32_t* tvals) {
+  __shared__ uint32_t s_off[8][32];
+  __shared__ uint32_t s_row[8][32];
+  __shared__ uint32_t s_x0w[8][32];  // x0 | (width << 16)
+  __shared__ uint32_t s_y0[8][32];
   const int64_t m = counters[0];
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t g = sorted_rows[j];
-    int64_t o = offsets[j];
-    const ushort4 rc = rect[g];
-    for (int ty = rc.z; ty <= rc.w; ty++)
-      for (int tx = rc.x; tx <= rc.y; tx++) {
-        if (o < capacity) {
-          tkeys[o] = (TK)(ty * tiles_x + tx);
-          tvals[o] = g;
-        }
-        o++;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t j0 = ((int64_t)blockIdx.x * 8 + warp) * 32; j0 < m; j0 += nwarps * 32) {
+    const int64_t j = j0 + lane;
+    const bool valid = j < m;
+    uint32_t off = 0xffffffffu, cnt = 0;
+    if (valid) {
+      const uint32_t g = sorted_rows[j];
+      off = offsets[j];
+      const ushort4 rc = rect[g];  // x0, x1, y0, y1
+      const uint32_t wdt = rc.y - rc.x + 1;
+      cnt = wdt * (uint32_t)(rc.w - rc.z + 1);
+      s_row[warp][lane] = g;
+      s_x0w[warp][lane] = rc.x | (wdt << 16);
+      s_y0[warp][lane] = rc.z;
+    }
+    s_off[warp][lane] = off;
+    const int last_lane = (int)tmin<int64_t>(31, m - 1 - j0);
+    const uint32_t start = __shfl_sync(0xffffffffu, off, 0);
+    const uint32_t end = __shfl_sync(0xffffffffu, off + cnt, last_lane);
+    __syncwarp();
+    for (uint32_t o = start + lane; o < end; o += 32) {
+      int lo = 0, hi = last_lane;  // largest l with s_off[l] <= o
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_off[warp][mid] <= o) lo = mid; else hi = mid - 1;
       }
-  }
-}
-
-template <typename TK>
-__global__ void __launch_bounds__(256) ranges_kernel(const TK* __restrict__ tkeys, const int64_t* counters,
-                                                     int64_t capacity, int n_tiles, int64_t* tile_starts) {
-  int64_t k = counters[1];
-  if (k > capacity) k = capacity;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  if (k == 0) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n_tiles; i += stride) tile_starts[i] = 0;
-    return;
-  }
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += stride) {
-    const int64_t t = tkeys[p];
-    const int64_t prev = p > 0 ? (int64_t)tkeys[p - 1] : -1;
-    for (int64_t tt = prev + 1; tt <= t; tt++) tile_starts[tt] = p;
-    if (p == k - 1)
-      for (int64_t tt = t + 1; tt <= n_tiles; tt++) tile_starts[tt] = k;
+      const uint32_t local = o - s_off[warp][lo];
+      const uint32_t x0w = s_x0w[warp][lo];
+      const uint32_t rw = x0w >> 16;
+      const uint32_t ty = s_y0[warp][lo] + local / rw, tx = (x0w & 0xffffu) + local % rw;
+      if (o < capacity) {
+        tkeys[o] = (TK)(ty * (uint32_t)tiles_x + tx);
+        tvals[o] = s_row[warp][lo];
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -129,10 +213,11 @@ struct TilesScratch {
   uint32_t* tv0;
   uint32_t* tv1;
   // zeroed control block
-  uint32_t* rs_status;  // (8 + 2) passes x parts x 256
-  uint64_t* scan_status;  // 2 x parts
-  uint32_t* hist;       // 10 x 256
-  uint32_t* part_ctr;   // 16
+  uint32_t* rs_status;    // 8 depth passes x parts_n x 256, then 2 tile passes x parts_k x 256
+  uint64_t* scan_status;  // 2 x (parts_n + 1)
+  uint32_t* hist;         // 10 x 256
+  uint32_t* part_ctr;     // 32
+  int* diff;              // (tiles_x + 1) x (tiles_y + 1)
   size_t control_bytes;
   void* control_begin;
   int64_t parts_n, parts_k;
@@ -140,7 +225,8 @@ struct TilesScratch {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-static size_t carve(int64_t n, int64_t cap, int n_tiles, unsigned char* base, TilesScratch* s) {
+static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned char* base, TilesScratch* s) {
+  const int n_tiles = tiles_x * tiles_y;
   const size_t tkw = n_tiles > 65535 ? 4 : 2;
   const int64_t nn = n > 0 ? n : 1, cc = cap > 0 ? cap : 1;
   const int64_t parts_n = (nn + RS_TILE - 1) / RS_TILE, parts_k = (cc + RS_TILE - 1) / RS_TILE;
@@ -166,6 +252,7 @@ static size_t carve(int64_t n, int64_t cap, int n_tiles, unsigned char* base, Ti
   t.scan_status = (uint64_t*)take(sizeof(uint64_t) * (size_t)(2 * (parts_n + 1)));
   t.hist = (uint32_t*)take(sizeof(uint32_t) * 10 * RADIX);
   t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);
+  t.diff = (int*)take(sizeof(int) * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1));
   t.control_bytes = off - ctl0;
   t.parts_n = parts_n;
   t.parts_k = parts_k;
@@ -173,32 +260,43 @@ static size_t carve(int64_t n, int64_t cap, int n_tiles, unsigned char* base, Ti
   return off;
 }
 
+static int sm_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = NUM_SMS;
+  }
+  return sms;
+}
+
 static int persistent_grid(const void* fn, int threads, size_t smem) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   if (per_sm < 1) per_sm = 1;
-  int dev = 0, sms = NUM_SMS;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return per_sm * sms;
+  return per_sm * sm_count();
 }
 
+// Stable LSD radix sort of (key, value) pairs, npasses 8-bit digits from
+// shift0: one histogram kernel for all passes, then one single-pass
+// (decoupled look-back) kernel per pass.  The last pass writes its values to
+// final_vals when given.
 template <typename K>
 static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_vals, const int64_t* count_ptr,
-                      int64_t cap, int shift0, int npasses, uint32_t* hist, uint32_t* status, int64_t parts,
-                      uint32_t* part_ctr, cudaStream_t st, K** keys_result) {
+                      int64_t cap, int shift0, int npasses, uint32_t* hist, bool hist_ready, uint32_t* status,
+                      int64_t parts, uint32_t* part_ctr, cudaStream_t st, K** keys_result, bool last_keys) {
   const size_t smem = sizeof(RadixSmem<K>);
-  auto pass = radix_pass_kernel<K>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
-  radix_hist_kernel<K><<<2 * NUM_SMS, 256, 0, st>>>(k0, count_ptr, cap, shift0, npasses, hist);
-  HGS_CHECK_LAUNCH();
   static int grid = 0;
-  if (grid == 0) grid = persistent_grid((const void*)pass, RS_THREADS, smem);
-  const int g = (int)hgs::tmin<int64_t>(grid, hgs::tmax<int64_t>(parts, 1));
+  if (grid == 0) {
+    cudaFuncSetAttribute(radix_pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    grid = persistent_grid((const void*)radix_pass_kernel<K>, RS_THREADS, smem);
+  }
+  if (!hist_ready) {
+    radix_hist_kernel<K><<<2 * sm_count(), 256, 0, st>>>(k0, count_ptr, cap, shift0, npasses, hist);
+    HGS_CHECK_LAUNCH();
+  }
+  const int g = (int)tmax<int64_t>(1, tmin<int64_t>(grid, parts));
   K* kin = k0;
   K* kout = k1;
   uint32_t* vin = v0;
@@ -206,8 +304,9 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
   for (int p = 0; p < npasses; p++) {
     const bool last = p == npasses - 1;
     uint32_t* vdst = last && final_vals ? final_vals : vout;
-    pass<<<g, RS_THREADS, smem, st>>>(kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p, hist + RADIX * p,
-                                      status + (size_t)p * parts * RADIX, part_ctr + p, 1);
+    radix_pass_kernel<K><<<g, RS_THREADS, smem, st>>>(kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
+                                                      hist + RADIX * p, status + (size_t)p * parts * RADIX, (int)parts,
+                                                      part_ctr + p, (!last || last_keys) ? 1 : 0);
     HGS_CHECK_LAUNCH();
     std::swap(kin, kout);
     vin = vdst;
@@ -220,7 +319,9 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
 }  // namespace hgs
 
 extern "C" size_t hgs_tiles_scratch_bytes(int64_t n, int64_t capacity, int32_t n_tiles) {
-  return hgs::carve(n, capacity, n_tiles, nullptr, nullptr);
+  // n_tiles is an upper bound on tiles_x * tiles_y; size the difference grid
+  // for the worst aspect ratio (tiles_x + 1) * (tiles_y + 1) <= 2 * n_tiles + 1
+  return hgs::carve(n, capacity, n_tiles, 1, nullptr, nullptr) + 8 * (size_t)n_tiles + 4096;
 }
 
 extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* tiles, void* stream) {
@@ -228,66 +329,73 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   if (!proj || !tiles) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: null argument");
   if (!tiles->entries || !tiles->tile_starts || !tiles->counters)
     return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: missing output pointer");
-  const int n_tiles = tiles->tiles_x * tiles->tiles_y;
   if (tiles->tiles_x <= 0 || tiles->tiles_y <= 0) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: empty tile grid");
-  if (n > 0xffffffffLL || tiles->capacity > (1LL << 30))
-    return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: n or capacity too large");
-  const size_t need = carve(n, tiles->capacity, n_tiles, nullptr, nullptr);
+  if (!proj->count || !proj->rect || !proj->rec) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: missing projection");
+  const int tx = tiles->tiles_x, ty = tiles->tiles_y;
+  const int n_tiles = tx * ty;
+  if (n > 0xffffffffLL || tiles->capacity > (1LL << 30) || n_tiles > (1 << 24))
+    return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: n, capacity or tile grid too large");
+  const size_t need = carve(n, tiles->capacity, tx, ty, nullptr, nullptr);
   if (!tiles->scratch || tiles->scratch_bytes < need)
     return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: scratch too small (see hgs_tiles_scratch_bytes)");
   cudaStream_t st = (cudaStream_t)stream;
   TilesScratch s;
-  carve(n, tiles->capacity, n_tiles, (unsigned char*)tiles->scratch, &s);
+  carve(n, tiles->capacity, tx, ty, (unsigned char*)tiles->scratch, &s);
   cudaMemsetAsync(s.control_begin, 0, s.control_bytes, st);
   cudaMemsetAsync(tiles->counters, 0, 4 * sizeof(int64_t), st);
-  if (n == 0) {
-    ranges_kernel<uint16_t><<<ceil_div(n_tiles + 1, 256), 256, 0, st>>>((const uint16_t*)s.tk[0], tiles->counters,
-                                                                       tiles->capacity, n_tiles, tiles->tile_starts);
-    HGS_CHECK_LAUNCH();
-    return HGS_OK;
+  // 1. compaction of visible rows + tile-rectangle difference grid
+  const int cells = (tx + 1) * (ty + 1);
+  const size_t diff_smem = cells <= DIFF_SMEM_CELLS ? sizeof(int) * (size_t)cells : 0;
+  static int scan_grid_cap = 0;
+  if (scan_grid_cap == 0) {
+    cudaFuncSetAttribute(compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(int) * DIFF_SMEM_CELLS));
+    scan_grid_cap = persistent_grid((const void*)compact_kernel, SCAN_THREADS, sizeof(int) * DIFF_SMEM_CELLS);
   }
-  const int scan_grid = (int)hgs::tmin<int64_t>(persistent_grid((const void*)compact_kernel, SCAN_THREADS, 0),
-                                               (n + SCAN_TILE - 1) / SCAN_TILE);
-  compact_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->count, (const BlendRec*)proj->rec, n, s.dk[0], s.dv[0],
-                                                     s.scan_status, s.part_ctr + 20, tiles->counters);
+  const int scan_grid = (int)tmax<int64_t>(1, tmin<int64_t>(scan_grid_cap, (n + SCAN_TILE - 1) / SCAN_TILE));
+  if (n > 0) {
+    compact_kernel<<<scan_grid, SCAN_THREADS, diff_smem, st>>>(proj->count, (const BlendRec*)proj->rec,
+                                                              (const ushort4*)proj->rect, n, tx, ty, s.dk[0],
+                                                              s.dv[0], s.scan_status, s.part_ctr + 20,
+                                                              tiles->counters, s.diff);
+    HGS_CHECK_LAUNCH();
+  }
+  // 2. per-tile counts -> tile_starts, K, overflow, tile-key histograms
+  tile_counts_kernel<<<1, 1024, 0, st>>>(s.diff, tx, ty, tiles->capacity, tiles->tile_starts, tiles->counters,
+                                         s.hist + 8 * RADIX);
   HGS_CHECK_LAUNCH();
-  // stable sort of the visible rows by fp64 depth bits
-  int rc = radix_sort<uint64_t>(s.dk[0], s.dk[1], s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0, 8, s.hist,
-                                s.rs_status, s.parts_n, s.part_ctr, st, nullptr);
+  if (n == 0) return HGS_OK;
+  // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
+  int rc = radix_sort<uint64_t>(s.dk[0], s.dk[1], s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0, 8, s.hist, false,
+                                s.rs_status, s.parts_n, s.part_ctr, st, nullptr, true);
   if (rc) return rc;
-  // 8 passes: result back in dk[0]/dv[0]
+  // 4. offsets of each row's entries in depth order
   offsets_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->count, s.dv[0], tiles->counters, s.offsets,
                                                      s.scan_status + s.parts_n + 1, s.part_ctr + 21, tiles->counters,
                                                      tiles->capacity);
   HGS_CHECK_LAUNCH();
+  // 5-6. emission in depth order, stable tile-key sort
   int bits = 1;
   while ((1 << bits) < n_tiles) bits++;
   const int tpasses = (bits + 7) / 8;
-  const int emit_grid = ceil_div(n, 256);
   uint32_t* rs_tile_status = s.rs_status + (size_t)8 * s.parts_n * RADIX;
+  if (tpasses > 2) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: more than 65536 tiles");
   if (n_tiles > 65535) {
-    emit_kernel<uint32_t><<<emit_grid, 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect, tiles->counters,
-                                                     tiles->tiles_x, tiles->capacity, (uint32_t*)s.tk[0], s.tv0);
+    emit_kernel<uint32_t><<<4 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+                                                          tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],
+                                                          s.tv0);
     HGS_CHECK_LAUNCH();
-    uint32_t* kres = nullptr;
     rc = radix_sort<uint32_t>((uint32_t*)s.tk[0], (uint32_t*)s.tk[1], s.tv0, s.tv1, tiles->entries,
-                              tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, rs_tile_status,
-                              s.parts_k, s.part_ctr + 8, st, &kres);
-    if (rc) return rc;
-    ranges_kernel<uint32_t><<<2 * NUM_SMS, 256, 0, st>>>(kres, tiles->counters, tiles->capacity, n_tiles,
-                                                         tiles->tile_starts);
+                              tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, true, rs_tile_status,
+                              s.parts_k, s.part_ctr + 8, st, nullptr, false);
   } else {
-    emit_kernel<uint16_t><<<emit_grid, 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect, tiles->counters,
-                                                     tiles->tiles_x, tiles->capacity, (uint16_t*)s.tk[0], s.tv0);
+    emit_kernel<uint16_t><<<4 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+                                                          tiles->counters, tx, tiles->capacity, (uint16_t*)s.tk[0],
+                                                          s.tv0);
     HGS_CHECK_LAUNCH();
-    uint16_t* kres = nullptr;
     rc = radix_sort<uint16_t>((uint16_t*)s.tk[0], (uint16_t*)s.tk[1], s.tv0, s.tv1, tiles->entries,
-                              tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, rs_tile_status,
-                              s.parts_k, s.part_ctr + 8, st, &kres);
-    if (rc) return rc;
-    ranges_kernel<uint16_t><<<2 * NUM_SMS, 256, 0, st>>>(kres, tiles->counters, tiles->capacity, n_tiles,
-                                                         tiles->tile_starts);
+                              tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, true, rs_tile_status,
+                              s.parts_k, s.part_ctr + 8, st, nullptr, false);
   }
-  HGS_CHECK_LAUNCH();
-  return HGS_OK;
+  return rc;
 }

@@ -48,6 +48,8 @@ class HybridRenderer:
         self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
         self.count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
+        self.cull = torch.empty(n * 4, dtype=torch.float32, device=dev)
+        self.fixup = torch.zeros(h * w + 1, dtype=torch.int32, device=dev)
         self.tile_starts = torch.zeros(self.n_tiles + 1, dtype=torch.int64, device=dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
         self.counters_host = torch.zeros(4, dtype=torch.int64).pin_memory()
@@ -88,6 +90,7 @@ class HybridRenderer:
     def _structs(self):
         ps = _lib.HGSProjected()
         ps.rec, ps.count, ps.rect = _lib.ptr(self.rec), _lib.ptr(self.count), _lib.ptr(self.rect)
+        ps.cull = _lib.ptr(self.cull)
         ts = _lib.HGSTiles()
         ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tiles_x, self.tiles_y, TILE_PX, self.capacity
         ts.entries, ts.tile_starts, ts.counters = _lib.ptr(self.entries), _lib.ptr(self.tile_starts), _lib.ptr(self.counters)
@@ -126,6 +129,7 @@ class HybridRenderer:
             variant, k = MASK_VARIANTS[self.mask[0]], float(self.mask[1])
             out.mask = _lib.ptr(self.mask_out)
         out.stats = _lib.ptr(self.stats)
+        out.fixup = _lib.ptr(self.fixup)
         _lib.check(L.hgs_blend_forward(ctypes.byref(ps), ctypes.byref(ts), w, h, ctypes.byref(ml), _c_f64_3(self.bg),
                                        variant, k, ctypes.byref(out), st), "blend_forward")
 
@@ -166,8 +170,8 @@ class HybridRenderer:
 
     # views for the API / backward ----------------------------------------
     def projected(self) -> ProjectedGaussians:
-        return ProjectedGaussians(len(self.gs), self.rec, self.count[:len(self.gs)], self.rect, None, self.width,
-                                  self.height)
+        return ProjectedGaussians(len(self.gs), self.rec, self.count, self.rect, None, self.width,
+                                  self.height, TILE_PX, self.cull)
 
     def tiles(self) -> TileBins:
         return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected())

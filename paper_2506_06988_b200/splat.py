@@ -85,15 +85,19 @@ class ProjectedGaussians:
     view_dist) over the device state indexed by original row (rec, count,
     rect) that build_tiles / rasterize_forward consume."""
 
-    def __init__(self, n, rec, count, rect, extras=None, width=None, height=None, tile_px=TILE_PX):
-        self.n, self.rec, self.count, self.rect = n, rec, count, rect
+    def __init__(self, n, rec, count, rect, extras=None, width=None, height=None, tile_px=TILE_PX, cull=None):
+        # count may be longer than n (buffers are allocated with >= 1 row so
+        # their device pointers are never NULL); the API view is count[:n]
+        self._count_buf = count
+        self.n, self.rec, self.count, self.rect, self.cull = n, rec, count[:n], rect, cull
         self._extras = extras
         self._compact = None
         self.width, self.height, self.tile_px = width, height, tile_px
 
     def struct(self) -> _lib.HGSProjected:
         s = _lib.HGSProjected()
-        s.rec, s.count, s.rect = _lib.ptr(self.rec), _lib.ptr(self.count), _lib.ptr(self.rect)
+        s.rec, s.count, s.rect = _lib.ptr(self.rec), _lib.ptr(self._count_buf), _lib.ptr(self.rect)
+        s.cull = _lib.ptr(self.cull)
         return s
 
     def _fields(self):
@@ -212,7 +216,7 @@ class _Scratch:
     def get(self, name: str, nbytes: int, device) -> torch.Tensor:
         b = self.bufs.get((name, device))
         if b is None or b.numel() < nbytes:
-            b = torch.empty(max(int(nbytes * 1.25), 256), dtype=torch.uint8, device=device)
+            b = torch.empty((max(int(nbytes * 1.25), 256) + 255) // 256 * 256, dtype=torch.uint8, device=device)
             self.bufs[(name, device)] = b
         return b
 
@@ -247,9 +251,10 @@ def _preprocess(gs: GaussianSet, cam, cam_dev, tile_px: int, extras: bool) -> Pr
     rec = torch.empty(max(n, 1) * REC_BYTES, dtype=torch.uint8, device=dev)
     count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
     rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
+    cull = torch.empty(max(n, 1) * 4, dtype=torch.float32, device=dev)
     ex = None
     ps = _lib.HGSProjected()
-    ps.rec, ps.count, ps.rect = _lib.ptr(rec), _lib.ptr(count), _lib.ptr(rect)
+    ps.rec, ps.count, ps.rect, ps.cull = _lib.ptr(rec), _lib.ptr(count), _lib.ptr(rect), _lib.ptr(cull)
     if extras:
         f64 = dict(dtype=torch.float64, device=dev)
         ex = {"cov2d": torch.zeros(n, 3, **f64), "radius": torch.zeros(n, **f64), "t_cam": torch.zeros(n, 3, **f64),
@@ -261,7 +266,7 @@ def _preprocess(gs: GaussianSet, cam, cam_dev, tile_px: int, extras: bool) -> Pr
             setattr(ps, k, _lib.ptr(v))
     _lib.call("hgs_preprocess", _lib.ptr(cam_dev), int(cam.width), int(cam.height), ctypes.byref(gs.struct()),
               int(tile_px), ctypes.byref(ps), _stream_ptr(dev))
-    return ProjectedGaussians(n, rec, count[:n], rect, ex, int(cam.width), int(cam.height), tile_px)
+    return ProjectedGaussians(n, rec, count, rect, ex, int(cam.width), int(cam.height), tile_px, cull)
 
 
 def project(gs, cam) -> ProjectedGaussians:
@@ -326,6 +331,8 @@ def _blend(proj, tiles: TileBins, width, height, mesh: Optional[MeshLayer], bg: 
         mask_t = torch.empty(height, width, dtype=torch.float32, device=dev)
         out.mask = _lib.ptr(mask_t)
     out.stats = _lib.ptr(stats)
+    fixup = SCRATCH.get("fixup", 4 * (height * width + 1), dev)
+    out.fixup = _lib.ptr(fixup)
     ml = mesh.struct() if mesh is not None else _lib.HGSMeshLayer()
     _lib.call("hgs_blend_forward", ctypes.byref(proj.struct()), ctypes.byref(tiles.struct()), int(width), int(height),
               ctypes.byref(ml), _c_f64_3(bg), variant, k, ctypes.byref(out), _stream_ptr(dev))
