@@ -75,8 +75,9 @@ typedef struct hgs_gaussian_grads {
 } hgs_gaussian_grads;
 
 /* Per-Gaussian projection state, indexed by ORIGINAL row (uncompacted).
-   rec: N x 80 B fp64 blend records {mean2d x,y; conic xx,xy,yy; alpha;
-   depth; colour r,g,b}.  count[i] = tile count (tiles.py:45-50), 0 iff the
+   rec: N x 80 B fp64 blend records {mean2d x,y; conic xx, 2*xy, yy; alpha;
+   depth; colour r,g,b} (the xy term is stored doubled, an exact scaling:
+   kernels.py:44 multiplies it by 2.0 first).  count[i] = tile count (tiles.py:45-50), 0 iff the
    row is culled by project (project.py:80-83,118-119).  The optional fields
    (NULL to skip) are ProjectedGaussians extras (project.py:38-50). */
 typedef struct hgs_projected {
@@ -89,7 +90,7 @@ typedef struct hgs_projected {
   double* color_pre; /* N x 3, optional */
   double* view_dir;  /* N x 3, optional (SH degree 1 only) */
   double* view_dist; /* N, optional (SH degree 1 only) */
-  void* cull;        /* N x 16 B fp32 {mean x, mean y, 3-sigma half extents x, y}: blend culling records
+  void* cull;        /* N x 32 B fp32 {mean x, mean y, 3-sigma half extents x, y; conic xx, xy, yy, 0}: blend culling records
                         (optional; without it hgs_blend_forward runs the exact per-pixel walk only) */
 } hgs_projected;
 

@@ -2,23 +2,26 @@
 // forward_kernel (splat/kernels.py:12-74), with the transmittance-mask
 // epilogue (train/losses.py:79-91).
 //
-// Fast path (blend_fast_kernel): one CTA per 16x16 tile, one thread per
-// pixel, warps own 8x4 sub-tiles.  The tile's depth-sorted entry list is
-// walked in batches of 256: every thread gathers one 80 B fp64 record + a
-// 16 B fp32 cull record into shared memory; each warp then compacts the
-// batch to the entries whose 3-sigma box touches its 8x4 sub-tile (ballot,
-// order preserving), and each pixel runs the reference's front-to-back loop
-// over that list only.  Per pixel-entry pair: an fp32 support prefilter with
-// a rigorous error bound rejects the clearly-outside pairs; the rest take the
-// exact fp64 support test (reference operation order), an exp() evaluated on
-// the SFU from an fp64-reduced argument (rel. err ~3e-7), and fp64
-// accumulation.  The two thresholds the approximate exp can flip (sigma <
-// 1/255 and T(1-sigma) < 1e-4) are guarded: if a decision lies within the
-// tracked error band the pixel is flagged and blend_exact_kernel recomputes
-// it with fp64 exp() -- so every skip/stop decision equals the reference's.
-// The mesh-depth stop is an exact fp64 compare.  Culled entries cannot
-// change the result: they have no support in the sub-tile, and the depth
-// stop is monotone along the depth-sorted list.
+// Fast path (blend_fast_kernel): one CTA per 16x16 tile, warp-specialised:
+// 8 consumer warps each own an 8x4 sub-tile (one pixel per lane), 1
+// producer warp streams the tile's depth-sorted entry list through a
+// 4-stage shared-memory ring (128 entries x 96 B per stage: the 80 B fp64
+// blend record + a 16 B fp32 cull box) with cp.async, completion tracked
+// by mbarriers (full: producer -> consumers, empty: consumers -> producer).
+// Consumers never meet at a CTA barrier: each compacts every stage to the
+// entries whose 3-sigma box touches its sub-tile (ballot, order
+// preserving) and runs the reference's front-to-back loop over that list.
+// Once every consumer's pixels are done the producer stops streaming.
+//
+// Per pixel-entry pair: exact fp64 support test (reference operation
+// order), exp() on the SFU (rel. err <= 6e-7), fp64 accumulation.  The two
+// thresholds the approximate exp can flip (sigma < 1/255 and
+// T(1-sigma) < 1e-4) are guarded: if a decision lies within the tracked
+// error band the pixel is flagged and blend_exact_kernel recomputes it with
+// fp64 exp() -- so every skip/stop decision equals the reference's.  The
+// mesh-depth stop is an exact fp64 compare.  Culled entries cannot change
+// the result: they have no support in the sub-tile, and the depth stop is
+// monotone along the depth-sorted list.
 #include "common.cuh"
 
 namespace hgs {
@@ -27,12 +30,92 @@ constexpr int BLEND_TILE = 16;
 constexpr int BLEND_THREADS = BLEND_TILE * BLEND_TILE;
 constexpr double LOG2E = 1.4426950408889634;
 
-struct BlendSmem {
-  double mx[BLEND_THREADS], my[BLEND_THREADS], ca[BLEND_THREADS], cb2[BLEND_THREADS], cc[BLEND_THREADS];
-  double alpha[BLEND_THREADS], depth[BLEND_THREADS], r[BLEND_THREADS], g[BLEND_THREADS], b[BLEND_THREADS];
-  float4 box[BLEND_THREADS];  // fp32 mean x, mean y + conservative 3-sigma half extents
-  unsigned char list[BLEND_THREADS / 32][BLEND_THREADS];
+constexpr int BATCH = 128;
+constexpr int NSTAGE = 4;
+constexpr int CONSUMERS = 8;
+constexpr int FAST_THREADS = (CONSUMERS + 1) * 32;
+
+struct __align__(16) StageEntry {
+  double2 a;  // mean x, mean y
+  double2 b;  // conic xx, 2*xy
+  double2 c;  // conic yy, alpha
+  double2 d;  // depth, r
+  double2 e;  // g, b
+  float4 box; // fp32 mean x, y, 3-sigma half extents x, y (z < 0: empty slot)
+  float4 con; // fp32 conic xx, xy, yy (ellipse cull)
 };
+static_assert(sizeof(StageEntry) == 112, "stage entry is 112 B");
+
+struct FastSmem {
+  StageEntry ent[NSTAGE][BATCH];
+  unsigned long long full[NSTAGE];
+  unsigned long long empty[NSTAGE];
+  unsigned char list[CONSUMERS][BATCH];
+  int done_warps;
+  int end_batch;
+  unsigned long long stats[2];
+};
+
+__device__ const float4 g_empty_box = {0.0f, 0.0f, -1.0f, -1.0f};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// One lane polls (the loop is visible to the compiler, so the warp
+// reconverges at the __syncwarp that publishes the acquired state).
+__device__ __forceinline__ void warp_wait(unsigned long long* bar, unsigned parity, int lane) {
+  if (lane == 0)
+    while (!mbar_try_wait(bar, parity)) {
+    }
+  __syncwarp();
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Conservative test: does the support ellipse {m <= 9} reach any point of
+// the box [x0,x1] x [y0,y1] (centre outside the box)?  The minimum of the
+// convex quadratic m over the box lies on an edge; each edge minimum is a
+// clamped 1D vertex.  fp32 with a generous margin (sure misses only).
+__device__ __forceinline__ float edge_min(float a, float b, float c, float u, float v0, float v1) {
+  // m(u, v) = a u^2 + 2 b u v + c v^2 with u fixed, v in [v0, v1]
+  const float v = fminf(fmaxf(-b * u / c, v0), v1);
+  return a * u * u + 2.0f * b * u * v + c * v * v;
+}
+__device__ __forceinline__ bool ellipse_meets_box(float4 con, float mx, float my, float x0, float x1, float y0,
+                                                  float y1) {
+  const float a = con.x, b = con.y, c = con.z;
+  const float dx0 = x0 - mx, dx1 = x1 - mx, dy0 = y0 - my, dy1 = y1 - my;
+  float mn = edge_min(a, b, c, dx0, dy0, dy1);
+  mn = fminf(mn, edge_min(a, b, c, dx1, dy0, dy1));
+  mn = fminf(mn, edge_min(c, b, a, dy0, dx0, dx1));
+  mn = fminf(mn, edge_min(c, b, a, dy1, dx0, dx1));
+  return mn <= 9.05f;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 __device__ __forceinline__ double mask_value(double t, double k, int variant) {
   switch (variant) {
@@ -52,19 +135,6 @@ __device__ __forceinline__ double fast_exp_neg_half(double m) {
   float e;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(t));
   return (double)e;
-}
-
-__device__ __forceinline__ void load_entry(BlendSmem& sm, int slot, const BlendRec* __restrict__ rec,
-                                           const float4* __restrict__ cull, uint32_t g) {
-  const double2* p = reinterpret_cast<const double2*>(rec + g);
-  const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3), e = __ldg(p + 4);
-  const float4 cr = __ldg(cull + g);
-  sm.mx[slot] = a.x; sm.my[slot] = a.y;
-  sm.ca[slot] = b.x; sm.cb2[slot] = 2.0 * b.y;  // (2.0 * conic_xy) is exact
-  sm.cc[slot] = c.x; sm.alpha[slot] = c.y;
-  sm.depth[slot] = d.x; sm.r[slot] = d.y;
-  sm.g[slot] = e.x; sm.b[slot] = e.y;
-  sm.box[slot] = cr;
 }
 
 __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_mesh_layer& mesh, bool mesh_here,
@@ -94,99 +164,177 @@ __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_
   if (out.mask) out.mask[p] = (float)mask_value(T, mask_k, mask_variant);
 }
 
-__global__ void __launch_bounds__(BLEND_THREADS, 3) blend_fast_kernel(
+template <bool STATS>
+__global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
     const BlendRec* __restrict__ rec, const float4* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup) {
-  __shared__ BlendSmem sm;
-  __shared__ unsigned long long s_stats[2];
+  extern __shared__ __align__(128) unsigned char fast_smem_raw[];
+  FastSmem& sm = *reinterpret_cast<FastSmem*>(fast_smem_raw);
   const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // warp -> 8x4 sub-tile (2 across, 4 down); lane -> pixel inside it
-  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
+  const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
+  const int nbatches = (int)((e - s + BATCH - 1) / BATCH);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSTAGE; i++) {
+      mbar_init(&sm.full[i], 32);
+      mbar_init(&sm.empty[i], CONSUMERS);
+    }
+    sm.done_warps = 0;
+    sm.end_batch = 0x7fffffff;
+    sm.stats[0] = sm.stats[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+
+  if (warp == CONSUMERS) {
+    // ------------------------------------------------------------ producer
+    for (int b = 0; b < nbatches; b++) {
+      const int slot = b % NSTAGE;
+      if (b >= NSTAGE) warp_wait(&sm.empty[slot], ((b / NSTAGE) - 1) & 1, lane);
+      if (*(volatile int*)&sm.done_warps == CONSUMERS) {
+        if (lane == 0) *(volatile int*)&sm.end_batch = b;
+        __syncwarp();
+        mbar_arrive(&sm.full[slot]);  // 32 plain arrivals complete the phase
+        break;
+      }
+      const int64_t base = s + (int64_t)b * BATCH;
+      for (int i = lane; i < BATCH; i += 32) {
+        StageEntry* dst = &sm.ent[slot][i];
+        const int64_t k = base + i;
+        if (k < e) {
+          const uint32_t g = __ldg(entries + k);
+          const char* src = reinterpret_cast<const char*>(rec + g);
+          cp_async16(&dst->a, src);
+          cp_async16(&dst->b, src + 16);
+          cp_async16(&dst->c, src + 32);
+          cp_async16(&dst->d, src + 48);
+          cp_async16(&dst->e, src + 64);
+          cp_async16(&dst->box, cull + 2 * (size_t)g);
+          cp_async16(&dst->con, cull + 2 * (size_t)g + 1);
+        } else {
+          cp_async16(&dst->box, &g_empty_box);
+        }
+      }
+      cp_async_arrive_noinc(&sm.full[slot]);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
   const int px = tx * BLEND_TILE + sx0 + (lane & 7);
   const int py = ty * BLEND_TILE + sy0 + (lane >> 3);
   const bool inside = px < width && py < height;
   const int64_t p = (int64_t)py * width + px;
-  const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
   const double fx = px + 0.5, fy = py + 0.5;
-  // pixel-centre box of this warp's sub-tile
   const float wx0 = tx * BLEND_TILE + sx0 + 0.5f, wx1 = wx0 + 7.0f;
   const float wy0 = ty * BLEND_TILE + sy0 + 0.5f, wy1 = wy0 + 3.0f;
-  const bool has_mesh = mesh.color != nullptr;
-  const bool mesh_here = has_mesh && inside && mesh.triangle_id[p] >= 0;
+  const bool mesh_here = mesh.color != nullptr && inside && mesh.triangle_id[p] >= 0;
   const double limit = mesh_here ? mesh.depth[p] : __longlong_as_double(0x7ff0000000000000LL);
   bool done = !inside;
   bool flagged = false;
-  double T = 1.0, r = 0.0, g = 0.0, b = 0.0, dacc = 0.0;
+  bool warp_done = false;
+  double T = 1.0, dacc = 0.0;
+  float r = 0.0f, g = 0.0f, bl = 0.0f;  // colour sums (fp32: no decision depends on them)
   float errT = 0.0f;  // bound on the relative error of T from the SFU exp
-  int64_t last = -1;
-  unsigned long long walked = 0, blended = 0;
-  if (threadIdx.x < 2) s_stats[threadIdx.x] = 0;
+  int last = -1;      // entry index relative to s
+  unsigned walked = 0, blended = 0;
 
-  for (int64_t base = s; base < e; base += BLEND_THREADS) {
-    if (__syncthreads_count(!done) == 0) break;
-    const int64_t idx = base + threadIdx.x;
-    if (idx < e) load_entry(sm, threadIdx.x, rec, cull, entries[idx]);
-    __syncthreads();
-    const int nb = (int)tmin<int64_t>(BLEND_THREADS, e - base);
-    // per-warp, order-preserving compaction of the entries touching the sub-tile
-    int nl = 0;
-    if (__any_sync(0xffffffffu, !done)) {
-      for (int k = 0; k < nb; k += 32) {
-        const int j = k + lane;
-        bool hit = false;
-        if (j < nb) {
-          const float4 q = sm.box[j];
-          const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
-          hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
-        }
+  for (int b = 0; b < nbatches; b++) {
+    const int slot = b % NSTAGE;
+    warp_wait(&sm.full[slot], (b / NSTAGE) & 1, lane);
+    if (b >= *(volatile int*)&sm.end_batch) break;
+    if (!warp_done) {
+      // order-preserving compaction of the stage to entries touching the sub-tile
+      int nl = 0;
+#pragma unroll
+      for (int k = 0; k < BATCH; k += 32) {
+        const float4 q = sm.ent[slot][k + lane].box;
+        const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
+        bool hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
+        if (hit && (q.x != cx || q.y != cy)) hit = ellipse_meets_box(sm.ent[slot][k + lane].con, q.x, q.y, wx0, wx1,
+                                                                  wy0, wy1);
         const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)j;
+        if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)(k + lane);
         nl += __popc(m);
+      }
+      __syncwarp();
+      if (__any_sync(0xffffffffu, !done)) {  // warp-uniform: the loop below votes
+        const int bbase = b * BATCH;
+        // Two entries per step: the independent part (support test, exp) of
+        // both is evaluated together for ILP, then the reference's
+        // sequential T/colour recurrence consumes them in order.  Uniform
+        // trip count + a vote per step keeps the warp converged.
+        for (int li = 0; li < nl; li += 2) {
+          const bool has1 = li + 1 < nl;
+          const int j0 = sm.list[warp][li];
+          const int j1 = has1 ? sm.list[warp][li + 1] : j0;
+          const StageEntry& E0 = sm.ent[slot][j0];
+          const StageEntry& E1 = sm.ent[slot][j1];
+          const double2 D0 = E0.d, D1 = E1.d;  // depth, r
+          const double2 A0 = E0.a, A1 = E1.a, B0 = E0.b, B1 = E1.b, C0 = E0.c, C1 = E1.c;
+          const double dx0 = fx - A0.x, dy0 = fy - A0.y, dx1 = fx - A1.x, dy1 = fy - A1.y;
+          // exact fp64 support test in the reference's operation order
+          const double m0 = B0.x * dx0 * dx0 + B0.y * dx0 * dy0 + C0.x * dy0 * dy0;
+          const double m1 = B1.x * dx1 * dx1 + B1.y * dx1 * dy1 + C1.x * dy1 * dy1;
+          const bool in0 = !(m0 > SUPPORT_MAHAL2 || m0 < 0.0);
+          const bool in1 = has1 && !(m1 > SUPPORT_MAHAL2 || m1 < 0.0);
+          double sig0 = C0.y * fast_exp_neg_half(in0 ? m0 : 0.0);
+          double sig1 = C1.y * fast_exp_neg_half(in1 ? m1 : 0.0);
+          if (sig0 > ALPHA_CLAMP) sig0 = ALPHA_CLAMP;
+          if (sig1 > ALPHA_CLAMP) sig1 = ALPHA_CLAMP;
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            const bool in = u == 0 ? in0 : in1;
+            const double sig = u == 0 ? sig0 : sig1;
+            const double2 D = u == 0 ? D0 : D1;
+            const StageEntry& E = u == 0 ? E0 : E1;
+            const int j = u == 0 ? j0 : j1;
+            if (done || (u == 1 && !has1)) continue;
+            if (STATS) walked++;
+            if (D.x >= limit) { done = true; continue; }  // list is depth sorted; mesh is opaque
+            if (!in) continue;
+            const float sgf = (float)sig;
+            // guard: the 1/255 skip decision is ambiguous within the exp error band
+            if (fabsf(sgf - (float)SIGMA_SKIP) <= 1.5f * FAST_EXP_REL_ERR * (float)SIGMA_SKIP) flagged = true;
+            if (sig < SIGMA_SKIP) continue;
+            const double test_t = T * (1.0 - sig);
+            errT += 1.1f * FAST_EXP_REL_ERR * sgf * rcp_approx(1.0f - sgf);
+            // guard: the early-stop decision is ambiguous within the tracked T error band
+            if (fabsf((float)test_t - (float)EARLY_STOP_T) <= (errT + 1e-6f) * (float)EARLY_STOP_T) flagged = true;
+            if (test_t < EARLY_STOP_T) { done = true; continue; }
+            const double w = sig * T;
+            const float wf = (float)w;
+            const double2 Ec = E.e;
+            r = fmaf((float)D.y, wf, r);
+            g = fmaf((float)Ec.x, wf, g);
+            bl = fmaf((float)Ec.y, wf, bl);
+            dacc = fma(D.x, w, dacc);
+            T = test_t;
+            last = b * BATCH + j;
+            if (STATS) blended++;
+          }
+          if (__all_sync(0xffffffffu, done)) break;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) {
+        warp_done = true;
+        if (lane == 0) atomicAdd(&sm.done_warps, 1);
       }
     }
     __syncwarp();
-    if (!done) {
-      for (int li = 0; li < nl; li++) {
-        const int j = sm.list[warp][li];
-        walked++;
-        if (sm.depth[j] >= limit) { done = true; break; }  // list is depth sorted; mesh is opaque
-        // exact fp64 support test in the reference's operation order
-        const double dx = fx - sm.mx[j], dy = fy - sm.my[j];
-        const double m = sm.ca[j] * dx * dx + sm.cb2[j] * dx * dy + sm.cc[j] * dy * dy;
-        if (m > SUPPORT_MAHAL2 || m < 0.0) continue;
-        double sig = sm.alpha[j] * fast_exp_neg_half(m);
-        if (sig > ALPHA_CLAMP) sig = ALPHA_CLAMP;
-        const float sgf = (float)sig;
-        // guard: the 1/255 skip decision is ambiguous within the exp error band
-        if (fabsf(sgf - (float)SIGMA_SKIP) <= 1.5f * FAST_EXP_REL_ERR * (float)SIGMA_SKIP) flagged = true;
-        if (sig < SIGMA_SKIP) continue;
-        const double test_t = T * (1.0 - sig);
-        errT += 1.1f * FAST_EXP_REL_ERR * __fdividef(sgf, 1.0f - sgf);
-        // guard: the early-stop decision is ambiguous within the tracked T error band
-        if (fabsf((float)test_t - (float)EARLY_STOP_T) <= (errT + 1e-6f) * (float)EARLY_STOP_T) flagged = true;
-        if (test_t < EARLY_STOP_T) { done = true; break; }
-        const double w = sig * T;
-        r = fma(sm.r[j], w, r);
-        g = fma(sm.g[j], w, g);
-        b = fma(sm.b[j], w, b);
-        dacc = fma(sm.depth[j], w, dacc);
-        T = test_t;
-        last = base + j;
-        blended++;
-      }
-    }
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
   }
-  if (out.stats) {
-    __syncthreads();
-    atomicAdd(&s_stats[0], walked);
-    atomicAdd(&s_stats[1], blended);
-    __syncthreads();
+  if (STATS) {
+    atomicAdd(&sm.stats[0], (unsigned long long)walked);
+    atomicAdd(&sm.stats[1], (unsigned long long)blended);
+    // consumers only: the producer may already have left
+    asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS * 32));
     if (threadIdx.x == 0) {
-      atomicAdd((unsigned long long*)&out.stats[0], s_stats[0]);
-      atomicAdd((unsigned long long*)&out.stats[1], s_stats[1]);
+      atomicAdd((unsigned long long*)&out.stats[0], sm.stats[0]);
+      atomicAdd((unsigned long long*)&out.stats[1], sm.stats[1]);
     }
   }
   if (!inside) return;
@@ -195,7 +343,8 @@ __global__ void __launch_bounds__(BLEND_THREADS, 3) blend_fast_kernel(
     fixup[1 + slot] = (int32_t)p;
     return;
   }
-  write_pixel(out, mesh, mesh_here, p, T, r, g, b, dacc, last, bg0, bg1, bg2, mask_variant, mask_k);
+  write_pixel(out, mesh, mesh_here, p, T, r, g, bl, dacc, last >= 0 ? s + last : -1, bg0, bg1, bg2, mask_variant,
+              mask_k);
 }
 
 // Exact reference walk (fp64 exp()).  With fixup != NULL: one warp per
@@ -232,7 +381,7 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
         dep = q.depth;
         stop = q.depth >= limit;
         const double dx = fx - q.mx, dy = fy - q.my;
-        const double m = q.ca * dx * dx + (2.0 * q.cb) * dx * dy + q.cc * dy * dy;
+        const double m = q.ca * dx * dx + q.cb2 * dx * dy + q.cc * dy * dy;
         if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
           sig = q.alpha * exp(-0.5 * m);
           if (sig > ALPHA_CLAMP) sig = ALPHA_CLAMP;
@@ -291,16 +440,27 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
   const int64_t npix = (int64_t)width * height;
   if (out->fixup && proj->cull) {
     cudaMemsetAsync(out->fixup, 0, sizeof(int32_t), st);
-    blend_fast_kernel<<<n_tiles, BLEND_THREADS, 0, st>>>((const BlendRec*)proj->rec, (const float4*)proj->cull,
-                                                         tiles->entries, tiles->tile_starts, tiles->tiles_x, width,
-                                                         height, ml, bg_host3[0], bg_host3[1], bg_host3[2],
-                                                         mask_variant, mask_k, *out, out->fixup);
+    const size_t smem = sizeof(FastSmem);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(blend_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(blend_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    if (out->stats)
+      blend_fast_kernel<true><<<n_tiles, FAST_THREADS, smem, st>>>(
+          (const BlendRec*)proj->rec, (const float4*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
+          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
+    else
+      blend_fast_kernel<false><<<n_tiles, FAST_THREADS, smem, st>>>(
+          (const BlendRec*)proj->rec, (const float4*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
+          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
     HGS_CHECK_LAUNCH();
     // persistent fix-up over the (device-side) list of flagged pixels
     blend_exact_kernel<<<2 * NUM_SMS, 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,
-                                                            tiles->tile_starts, tiles->tiles_x, width, height, ml,
-                                                            bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
-                                                            mask_k, *out, out->fixup);
+                                                    tiles->tile_starts, tiles->tiles_x, width, height, ml,
+                                                    bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
+                                                    mask_k, *out, out->fixup);
     HGS_CHECK_LAUNCH();
   } else {
     blend_exact_kernel<<<ceil_div(npix * 32, 256), 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,

@@ -27,7 +27,7 @@ constexpr int NUM_SMS = 148;
 // Blend record per Gaussian (fp64, 80 B): the fields the per-pixel walk reads.
 struct __align__(16) BlendRec {
   double mx, my;      // mean2d
-  double ca, cb, cc;  // conic (xx, xy, yy)
+  double ca, cb2, cc;  // conic xx, 2 * conic xy (exact scaling), conic yy
   double alpha;       // sigmoid(logit)
   double depth;       // camera z
   double r, g, b;     // view-evaluated colour, clamped at 0

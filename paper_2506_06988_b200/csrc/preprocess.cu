@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const hgs_camera* __res
 
   BlendRec rec;
   rec.mx = mx; rec.my = my;
-  rec.ca = cyy * inv_det; rec.cb = -cxy * inv_det; rec.cc = cxx * inv_det;
+  rec.ca = cyy * inv_det; rec.cb2 = 2.0 * (-cxy * inv_det); rec.cc = cxx * inv_det;
   rec.alpha = alpha; rec.depth = depth;
   rec.r = fmax(pre[0], 0.0); rec.g = fmax(pre[1], 0.0); rec.b = fmax(pre[2], 0.0);
   reinterpret_cast<BlendRec*>(out.rec)[i] = rec;
@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const hgs_camera* __res
     const float slack = 1e-3f + 2.5e-7f * (float)(fabs(mx) + fabs(my));
     const float ex = (float)(3.0 * sqrt(cxx)) * (1.0f + 1e-5f) + slack;
     const float ey = (float)(3.0 * sqrt(cyy)) * (1.0f + 1e-5f) + slack;
-    reinterpret_cast<float4*>(out.cull)[i] = make_float4((float)mx, (float)my, ok ? ex : -1.0f, ok ? ey : -1.0f);
+    float4* cr = reinterpret_cast<float4*>(out.cull) + 2 * i;
+    cr[0] = make_float4((float)mx, (float)my, ok ? ex : -1.0f, ok ? ey : -1.0f);
+    cr[1] = make_float4((float)(cyy * inv_det), (float)(-cxy * inv_det), (float)(cxx * inv_det), 0.0f);
   }
   if (out.cov2d) { out.cov2d[3 * i] = cxx; out.cov2d[3 * i + 1] = cxy; out.cov2d[3 * i + 2] = cyy; }
   if (out.radius) out.radius[i] = radius;

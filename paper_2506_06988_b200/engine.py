@@ -48,7 +48,7 @@ class HybridRenderer:
         self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
         self.count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
-        self.cull = torch.empty(n * 4, dtype=torch.float32, device=dev)
+        self.cull = torch.empty(n * 8, dtype=torch.float32, device=dev)
         self.fixup = torch.zeros(h * w + 1, dtype=torch.int32, device=dev)
         self.tile_starts = torch.zeros(self.n_tiles + 1, dtype=torch.int64, device=dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev)

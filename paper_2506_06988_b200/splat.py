@@ -105,7 +105,9 @@ class ProjectedGaussians:
             alive = self.count > 0
             kept = torch.nonzero(alive).reshape(-1)
             rec = self.rec.view(torch.float64)[:self.n * 10].view(self.n, 10)[kept]
-            f = {"kept": kept, "mean2d": rec[:, 0:2].contiguous(), "conic": rec[:, 2:5].contiguous(),
+            conic = rec[:, 2:5].clone()
+            conic[:, 1] *= 0.5  # the record stores 2 * conic_xy (exact)
+            f = {"kept": kept, "mean2d": rec[:, 0:2].contiguous(), "conic": conic,
                  "alpha": rec[:, 5].contiguous(), "depth": rec[:, 6].contiguous(), "color": rec[:, 7:10].contiguous()}
             ex = self._extras or {}
             for k in ("cov2d", "radius", "t_cam", "color_pre", "view_dir", "view_dist"):
@@ -251,7 +253,7 @@ def _preprocess(gs: GaussianSet, cam, cam_dev, tile_px: int, extras: bool) -> Pr
     rec = torch.empty(max(n, 1) * REC_BYTES, dtype=torch.uint8, device=dev)
     count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
     rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
-    cull = torch.empty(max(n, 1) * 4, dtype=torch.float32, device=dev)
+    cull = torch.empty(max(n, 1) * 8, dtype=torch.float32, device=dev)
     ex = None
     ps = _lib.HGSProjected()
     ps.rec, ps.count, ps.rect, ps.cull = _lib.ptr(rec), _lib.ptr(count), _lib.ptr(rect), _lib.ptr(cull)
