@@ -119,6 +119,36 @@ def cpu_frames(scene, max_seconds=15.0, max_frames=5, threads=0):
     return frames / dt, frames, dt, orc.max_threads() if threads <= 0 else threads
 
 
+def train_cpu_estimate(n_gauss=1_000_000, seconds_cap=40.0):
+    """Oracle (CPU port) time of one c4 view's training work (render + loss +
+    backward + texture backward) on the host cores; the 64-view step time is
+    that x 64 (stated as an extrapolation)."""
+    from oracle import oracle as orc
+    from paper_2506_06988_b200 import synthetic as syn
+    sc = syn.make_config("c4", seed=0, n_views=1)
+    cam = sc.cameras[0]
+    m = sc.mesh
+    cores = len(os.sched_getaffinity(0))
+
+    class Cfg:
+        dssim_weight, zero_dssim_after_densify, densify_until_iter, warmup_iters = 0.2, False, 15000, 3000
+        texture_weight, mask_sharpness, mask_variant = 0.1, 20.0, "sigmoid"
+
+    t0 = time.perf_counter()
+    fr = orc.rasterize_fragments(m.vertices, m.triangles, m.uvs, cam, nthreads=cores)
+    t1 = time.perf_counter()
+    mc = orc.sample_texture(m.texture, fr.uv, fr.valid, nthreads=cores)
+    color, depth, tt, ctx = orc.render(sc.gaussians, cam, (0, 0, 0), orc.Mesh(mc, fr.depth, fr.triangle_id),
+                                       nthreads=cores)
+    target = np.clip(mc + 0.05, 0, 1)
+    bd, gih, gim, gt = orc.composite_loss(target, color, mc, fr.valid, tt, 3001, Cfg, nthreads=cores)
+    g = orc.backward(ctx, gih, gt, nthreads=cores)
+    orc.texture_backward(fr, g.mesh_color + gim, m.texture.shape[:2])
+    t2 = time.perf_counter()
+    per_view = (t2 - t1)  # fragments are cached per camera in the reference loop (loop.py:172-175)
+    return per_view, cores
+
+
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -279,10 +309,75 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": fps_cpu, "unit": UNIT, "cores": th, "kind": "port",
                                 "sample": f"{frames} full {args.config} frames in {dt:.1f} s (oracle/gsmesh_oracle.c, "
                                           f"OpenMP, {th} threads)"}
+    if not args.no_train:
+        line["train"] = run_train(args, rank, world, local, dev)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            per_view, cores = train_cpu_estimate()
+            step_s = per_view * args.train_views
+            line["train"]["cpu_baseline"] = {
+                "value": 1.0 / step_s, "unit": "iters/s", "cores": cores, "kind": "port",
+                "sample": f"1 c4 view (render + loss + backward + texture backward) in {per_view:.2f} s on the host "
+                          f"(oracle/gsmesh_oracle.c, OpenMP); x{args.train_views} views per step (extrapolated)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_train(args, rank, world, local, dev):
+    """c4: one optimisation step = args.train_views views (texture window
+    active), view-sharded over ranks, one NCCL all-reduce, fused Adam."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import _lib
+    from paper_2506_06988_b200 import synthetic as syn
+    from paper_2506_06988_b200.config import TrainConfig
+    from paper_2506_06988_b200.train import HybridTrainer, shard_views
+
+    nv = args.train_views
+    sc = syn.make_config("c4", seed=0, n_views=nv)
+    gs = hgs.GaussianSet.from_any(sc.gaussians)
+    mesh = hgs.TexturedMesh.from_any(sc.mesh)
+    cams = [hgs.Camera.from_any(c) for c in sc.cameras]
+    cfg = TrainConfig()
+    it = cfg.warmup_iters + 1  # texture-loss window active
+    H, W = cams[0].height, cams[0].width
+    mine = shard_views(nv, rank, world)
+    # targets: the textured mesh seen by each view, perturbed (synthetic data)
+    placeholder = [torch.zeros(H, W, 3, device=dev) for _ in cams]
+    tr = HybridTrainer(gs, mesh, cams, placeholder, cfg, rank=rank, world=world)
+    g = torch.Generator(device=dev).manual_seed(1234)
+    for v in range(nv):
+        tr.images[v] = (tr.mesh_layer(v).color + 0.05 * torch.rand(H, W, 3, device=dev, generator=g)).clamp_(0, 1)
+    views = list(range(nv))
+    for _ in range(max(3, args.train_warmup)):
+        tr.step(it, views)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = _lib.load().hgs_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.train_steps):
+        loss = tr.step(it, views)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = _lib.load().hgs_kernel_launches() - l0
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"metric": "joint GS+mesh optimisation steps/s (c4)", "value": args.train_steps / (ms * 1e-3),
+            "unit": "iters/s", "ms_per_step": ms / args.train_steps, "steps": args.train_steps,
+            "warmup": max(3, args.train_warmup), "scaling": "strong", "views_per_step": nv,
+            "views_per_rank": len(mine), "gaussians": len(gs), "triangles": mesh.n_faces,
+            "texture": list(mesh.texture.shape), "resolution": [W, H], "dtype": "f64 decisions / f32 params",
+            "loss_total": float(loss[4]), "gpu_launches": int(launches),
+            "note": "step = per-view render + composite loss (L1, D-SSIM, texture) + backward + texture backward, "
+                    "all_reduce(SUM) of one flat grad bucket (N>1), fused Adam (Gaussians + texture)"}
 
 
 def main():
@@ -295,6 +390,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-seconds", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-views", type=int, default=64)
+    ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--train-warmup", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
