@@ -128,7 +128,9 @@ __device__ __forceinline__ double mask_value(double t, double k, int variant) {
 
 // exp(-m/2) for m in [0, 9] on the SFU: 2^(m * -0.5 log2 e) with the
 // exponent rounded to fp32 (abs. err <= 2^-21 -> rel. 3.3e-7) and ex2.approx
-// (rel. err <= 2^-22): |rel. err| <= 6e-7 (FAST_EXP_REL_ERR).
+// (rel. err <= 2^-22): |rel. err| <= 6e-7 (FAST_EXP_REL_ERR).  (A hi/lo
+// split of the exponent halves the error and the fix-up flags but costs
+// ~10 % of the blend kernel -- measured, not worth it.)
 constexpr float FAST_EXP_REL_ERR = 6e-7f;
 __device__ __forceinline__ double fast_exp_neg_half(double m) {
   const float t = (float)(m * (-0.5 * LOG2E));
@@ -283,6 +285,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
           const bool in1 = has1 && !(m1 > SUPPORT_MAHAL2 || m1 < 0.0);
           double sig0 = C0.y * fast_exp_neg_half(in0 ? m0 : 0.0);
           double sig1 = C1.y * fast_exp_neg_half(in1 ? m1 : 0.0);
+          // the 1/255 skip is a per-entry decision: near it, recompute exp in
+          // fp64 right here (exact decision, no pixel flag needed)
+          if (fabs(sig0 - SIGMA_SKIP) <= 2.0 * (double)FAST_EXP_REL_ERR * SIGMA_SKIP) sig0 = C0.y * exp(-0.5 * m0);
+          if (fabs(sig1 - SIGMA_SKIP) <= 2.0 * (double)FAST_EXP_REL_ERR * SIGMA_SKIP) sig1 = C1.y * exp(-0.5 * m1);
           if (sig0 > ALPHA_CLAMP) sig0 = ALPHA_CLAMP;
           if (sig1 > ALPHA_CLAMP) sig1 = ALPHA_CLAMP;
 #pragma unroll
@@ -297,8 +303,6 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
             if (D.x >= limit) { done = true; continue; }  // list is depth sorted; mesh is opaque
             if (!in) continue;
             const float sgf = (float)sig;
-            // guard: the 1/255 skip decision is ambiguous within the exp error band
-            if (fabsf(sgf - (float)SIGMA_SKIP) <= 1.5f * FAST_EXP_REL_ERR * (float)SIGMA_SKIP) flagged = true;
             if (sig < SIGMA_SKIP) continue;
             const double test_t = T * (1.0 - sig);
             errT += 1.1f * FAST_EXP_REL_ERR * sgf * rcp_approx(1.0f - sgf);
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
     }
   }
   if (!inside) return;
-  if (flagged) {
+  if (flagged) {  // hand the pixel to the exact walk (work list: count, pixel ids)
     const int slot = atomicAdd(&fixup[0], 1);
     fixup[1 + slot] = (int32_t)p;
     return;
@@ -372,12 +376,17 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
     double T = 1.0, r = 0.0, g = 0.0, b = 0.0, dacc = 0.0;
     int64_t last = -1;
     bool done = false;
+    // software-pipelined: the next chunk's record gather is in flight while
+    // the current chunk is evaluated and consumed
+    BlendRec nxt;
+    if (s + lane < e) nxt = rec[entries[s + lane]];
     for (int64_t base = s; base < e && !done; base += 32) {
       const int64_t k = base + lane;
+      const BlendRec q = nxt;
+      if (base + 32 + lane < e) nxt = rec[entries[base + 32 + lane]];
       bool stop = false, use = false;
       double sig = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, dep = 0.0;
       if (k < e) {
-        const BlendRec q = rec[entries[k]];
         dep = q.depth;
         stop = q.depth >= limit;
         const double dx = fx - q.mx, dy = fy - q.my;
@@ -456,7 +465,7 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
           (const BlendRec*)proj->rec, (const float4*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
           width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
     HGS_CHECK_LAUNCH();
-    // persistent fix-up over the (device-side) list of flagged pixels
+    // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)
     blend_exact_kernel<<<2 * NUM_SMS, 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,
                                                     tiles->tile_starts, tiles->tiles_x, width, height, ml,
                                                     bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
