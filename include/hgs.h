@@ -35,6 +35,7 @@ extern "C" {
 #define HGS_ERR_CUDA 2
 
 #define HGS_ABI_VERSION 1
+#define HGS_TILE_DIFF_COPIES 16
 
 /* Pinhole camera, Camera (scene.py:144-203).  Derived fields are computed by
    the host exactly as the reference computes them:
@@ -92,6 +93,10 @@ typedef struct hgs_projected {
   double* view_dist; /* N, optional (SH degree 1 only) */
   void* cull;        /* N x 32 B fp32 {mean x, mean y, 3-sigma half extents x, y; conic xx, xy, yy, 0}: blend culling records
                         (optional; without it hgs_blend_forward runs the exact per-pixel walk only) */
+  uint64_t* sort_keys; /* N: fp64 depth bit pattern of visible rows, ~0 for culled rows (required by
+                          hgs_build_tiles) */
+  int32_t* tile_diff;  /* HGS_TILE_DIFF_COPIES x (tiles_x + 1) x (tiles_y + 1) 2D difference grids of the rows'
+                          tile rectangles (required by hgs_build_tiles; hgs_preprocess zeroes and fills it) */
 } hgs_projected;
 
 /* TileBins (splat/tiles.py:19-32).  entries hold ORIGINAL Gaussian rows in
@@ -175,7 +180,8 @@ int hgs_preprocess(const hgs_camera* cam, int32_t width, int32_t height, const h
 
 /* build_tiles (splat/tiles.py:35-69): visible-row compaction, fp64 depth
    radix sort, tile-entry emission in depth order, stable tile radix sort,
-   CSR ranges.  All counts stay on the device (tiles->counters). */
+   CSR ranges.  All counts stay on the device (tiles->counters).  proj must
+   come from hgs_preprocess with sort_keys and tile_diff set. */
 size_t hgs_tiles_scratch_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
 int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* tiles, void* stream);
 

@@ -50,7 +50,7 @@ class HGSGaussianGrads(ctypes.Structure):
 class HGSProjected(ctypes.Structure):
     _fields_ = [("rec", c_void_p), ("count", c_void_p), ("rect", c_void_p), ("cov2d", c_void_p),
                 ("radius", c_void_p), ("t_cam", c_void_p), ("color_pre", c_void_p), ("view_dir", c_void_p),
-                ("view_dist", c_void_p), ("cull", c_void_p)]
+                ("view_dist", c_void_p), ("cull", c_void_p), ("sort_keys", c_void_p), ("tile_diff", c_void_p)]
 
 
 class HGSTiles(ctypes.Structure):

@@ -22,18 +22,19 @@
 namespace hgs {
 
 constexpr int BW_THREADS = 256;
+constexpr int BW_BATCH = 256;
 constexpr double BW_LOG2E = 1.4426950408889634;
 
 struct BwSmem {
-  double2 a[BW_THREADS];  // mean x, y
-  double2 b[BW_THREADS];  // conic xx, 2*xy
-  double2 c[BW_THREADS];  // conic yy, alpha
-  double2 d[BW_THREADS];  // depth, r
-  double2 e[BW_THREADS];  // g, b
-  float4 box[BW_THREADS];
-  float4 con[BW_THREADS];
-  uint32_t gid[BW_THREADS];
-  unsigned char list[BW_THREADS / 32][BW_THREADS];
+  double2 a[BW_BATCH];  // mean x, y
+  double2 b[BW_BATCH];  // conic xx, 2*xy
+  double2 c[BW_BATCH];  // conic yy, alpha
+  double2 d[BW_BATCH];  // depth, r
+  double2 e[BW_BATCH];  // g, b
+  float4 box[BW_BATCH];
+  float4 con[BW_BATCH];
+  uint32_t gid[BW_BATCH];
+  unsigned char list[BW_THREADS / 32][BW_BATCH];
   int max_last;
 };
 
@@ -92,6 +93,112 @@ __device__ __forceinline__ int scatter16_index(int lane) {
   return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
 }
 
+// Per-pixel reverse-walk state.
+struct BwPix {
+  int64_t last;
+  double gr, gg, gb, gtp, t_fin, t_after, acc_r, acc_g, acc_b, fx, fy;
+  bool inside, mesh_here;
+};
+
+__device__ __forceinline__ void bw_pixel_init(BwPix& q, int px, int py, int width, int height, int64_t s,
+                                              const hgs_mesh_layer& mesh, double bg0, double bg1, double bg2,
+                                              const double* __restrict__ final_t, const int32_t* __restrict__ last_idx,
+                                              const float* __restrict__ grad_color, const float* __restrict__ grad_t,
+                                              float* __restrict__ mesh_grad, int accumulate_mesh) {
+  q.inside = px < width && py < height;
+  q.fx = px + 0.5;
+  q.fy = py + 0.5;
+  q.last = -1;
+  q.gr = q.gg = q.gb = q.gtp = 0.0;
+  q.t_fin = 1.0;
+  q.mesh_here = false;
+  const int64_t p = (int64_t)py * width + px;
+  if (q.inside) {
+    q.last = last_idx[p];
+    q.gr = grad_color[3 * p];
+    q.gg = grad_color[3 * p + 1];
+    q.gb = grad_color[3 * p + 2];
+    q.gtp = grad_t ? (double)grad_t[p] : 0.0;
+    q.t_fin = final_t[p];
+    q.mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
+    if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
+      const double f = q.mesh_here ? q.t_fin : 0.0;
+      float* mg = mesh_grad + 3 * p;
+      if (accumulate_mesh) {
+        mg[0] += (float)(q.gr * f); mg[1] += (float)(q.gg * f); mg[2] += (float)(q.gb * f);
+      } else {
+        mg[0] = (float)(q.gr * f); mg[1] = (float)(q.gg * f); mg[2] = (float)(q.gb * f);
+      }
+    }
+  }
+  q.t_after = q.t_fin;  // suffix colour starts at T_final * (mesh or background) (kernels.py:111-119)
+  if (q.mesh_here) {
+    q.acc_r = q.t_after * (double)mesh.color[3 * p];
+    q.acc_g = q.t_after * (double)mesh.color[3 * p + 1];
+    q.acc_b = q.t_after * (double)mesh.color[3 * p + 2];
+  } else {
+    q.acc_r = q.t_after * bg0;
+    q.acc_g = q.t_after * bg1;
+    q.acc_b = q.t_after * bg2;
+  }
+  if (q.last >= 0) q.last -= s;  // relative to the tile start
+}
+
+// One reverse step of kernels.py:120-160 for entry slot i (relative index
+// rel); adds this pixel's 9-vector into v.
+__device__ __forceinline__ bool bw_pixel_step(BwPix& q, const BwSmem& sm, int i, int rel, float v[16]) {
+  if (q.last < 0 || rel > q.last) return false;
+  const double2 A = sm.a[i], B = sm.b[i], C = sm.c[i];
+  const double dx = q.fx - A.x, dy = q.fy - A.y;
+  const double m = B.x * dx * dx + B.y * dx * dy + C.x * dy * dy;
+  if (m > SUPPORT_MAHAL2 || m < 0.0) return false;
+  // SFU exp, exact fp64 recompute near the skip/clamp thresholds
+  float ef;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ef) : "f"((float)(m * (-0.5 * BW_LOG2E))));
+  double gauss = (double)ef;
+  double sig = C.y * gauss;
+  if (fabs(sig - SIGMA_SKIP) <= 2e-6 * SIGMA_SKIP || fabs(sig - ALPHA_CLAMP) <= 2e-6) {
+    gauss = exp(-0.5 * m);
+    sig = C.y * gauss;
+  }
+  const bool clamped = sig > ALPHA_CLAMP;
+  if (clamped) sig = ALPHA_CLAMP;
+  if (sig < SIGMA_SKIP) return false;
+  const double2 D = sm.d[i], E = sm.e[i];
+  const double cr = D.y, cg = E.x, cb = E.y;
+  const double one_minus = 1.0 - sig;
+  const double inv = 1.0 / one_minus;  // one division for the five of kernels.py:135,142-146
+  const double t_before = q.t_after * inv;
+  const double w = sig * t_before;
+  const float wf = (float)w;
+  v[6] += (float)q.gr * wf;
+  v[7] += (float)q.gg * wf;
+  v[8] += (float)q.gb * wf;
+  double s_i = (q.gr * (cr * t_before - q.acc_r * inv) + q.gg * (cg * t_before - q.acc_g * inv)) +
+               q.gb * (cb * t_before - q.acc_b * inv);
+  if (q.gtp != 0.0) s_i += q.gtp * (-q.t_fin * inv);
+  if (!clamped) {
+    // no decision depends on these: fp32 from here on
+    const float dxf = (float)dx, dyf = (float)dy, cbh = 0.5f * (float)B.y;  // conic xy
+    const float qd_x = (float)B.x * dxf + cbh * dyf;
+    const float qd_y = cbh * dxf + (float)C.x * dyf;
+    const float common = (float)(s_i * sig);
+    const float hc = 0.5f * common;
+    v[0] += common * qd_x;
+    v[1] += common * qd_y;
+    v[2] += hc * qd_x * qd_x;
+    v[3] += hc * qd_x * qd_y;
+    v[4] += hc * qd_y * qd_y;
+    v[5] += (float)(s_i * gauss);
+  }
+  q.acc_r += cr * w;
+  q.acc_g += cg * w;
+  q.acc_b += cb * w;
+  q.t_after = t_before;
+  return true;
+}
+
+// 256 threads = 8 warps, each warp an 8x4 sub-tile, one pixel per lane.
 __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
     const BlendRec* __restrict__ rec, const float4* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
@@ -105,56 +212,23 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
   const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
   const int px = tx * 16 + sx0 + (lane & 7);
   const int py = ty * 16 + sy0 + (lane >> 3);
-  const bool inside = px < width && py < height;
-  const int64_t p = (int64_t)py * width + px;
   const int64_t s = tile_starts[tile];
   const float wx0 = tx * 16 + sx0 + 0.5f, wx1 = wx0 + 7.0f;
   const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + 3.0f;
-  const double fx = px + 0.5, fy = py + 0.5;
-  int64_t last = -1;
-  double gr = 0.0, gg = 0.0, gb = 0.0, gtp = 0.0, t_fin = 1.0;
-  bool mesh_here = false;
-  if (inside) {
-    last = last_idx[p];
-    gr = grad_color[3 * p];
-    gg = grad_color[3 * p + 1];
-    gb = grad_color[3 * p + 2];
-    gtp = grad_t ? (double)grad_t[p] : 0.0;
-    t_fin = final_t[p];
-    mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
-    if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
-      const double f = mesh_here ? t_fin : 0.0;
-      float* mg = mesh_grad + 3 * p;
-      if (accumulate_mesh) {
-        mg[0] += (float)(gr * f); mg[1] += (float)(gg * f); mg[2] += (float)(gb * f);
-      } else {
-        mg[0] = (float)(gr * f); mg[1] = (float)(gg * f); mg[2] = (float)(gb * f);
-      }
-    }
-  }
-  double t_after = t_fin;
-  double acc_r, acc_g, acc_b;
-  if (mesh_here) {
-    acc_r = t_after * (double)mesh.color[3 * p];
-    acc_g = t_after * (double)mesh.color[3 * p + 1];
-    acc_b = t_after * (double)mesh.color[3 * p + 2];
-  } else {
-    acc_r = t_after * bg0;
-    acc_g = t_after * bg1;
-    acc_b = t_after * bg2;
-  }
+  BwPix q0;
+  bw_pixel_init(q0, px, py, width, height, s, mesh, bg0, bg1, bg2, final_t, last_idx, grad_color, grad_t, mesh_grad,
+                accumulate_mesh);
   if (threadIdx.x == 0) sm.max_last = -1;
   __syncthreads();
-  if (last >= 0) atomicMax(&sm.max_last, (int)(last - s));
+  if (q0.last >= 0) atomicMax(&sm.max_last, (int)q0.last);
   __syncthreads();
   const int top = sm.max_last;  // relative index of the newest entry any pixel used
   const int vidx = scatter16_index(lane);
-  for (int hi = top; hi >= 0; hi -= BW_THREADS) {
-    const int lo = hi - BW_THREADS + 1 > 0 ? hi - BW_THREADS + 1 : 0;
+  for (int hi = top; hi >= 0; hi -= BW_BATCH) {
+    const int lo = hi - BW_BATCH + 1 > 0 ? hi - BW_BATCH + 1 : 0;
     const int nb = hi - lo + 1;
     __syncthreads();
-    if (threadIdx.x < nb) {  // slot i holds entry lo + i
-      const int i = threadIdx.x;
+    for (int i = threadIdx.x; i < nb; i += BW_THREADS) {  // slot i holds entry lo + i
       const uint32_t g = entries[s + lo + i];
       const double2* rp = reinterpret_cast<const double2*>(rec + g);
       sm.a[i] = __ldg(rp);
@@ -173,10 +247,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
       const int i = nb - 1 - (k + lane);
       bool hit = false;
       if (i >= 0) {
-        const float4 q = sm.box[i];
-        const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
-        hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
-        if (hit && (q.x != cx || q.y != cy)) hit = bw_ellipse_meets_box(sm.con[i], q.x, q.y, wx0, wx1, wy0, wy1);
+        const float4 b = sm.box[i];
+        const float cx = fminf(fmaxf(b.x, wx0), wx1), cy = fminf(fmaxf(b.y, wy0), wy1);
+        hit = fabsf(b.x - cx) <= b.z && fabsf(b.y - cy) <= b.w;
+        if (hit && (b.x != cx || b.y != cy)) hit = bw_ellipse_meets_box(sm.con[i], b.x, b.y, wx0, wx1, wy0, wy1);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)i;
@@ -188,56 +262,8 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
       float v[16];
 #pragma unroll
       for (int c = 0; c < 16; c++) v[c] = 0.0f;
-      bool contrib = false;
-      if (last >= 0 && lo + i <= (int)(last - s)) {
-        const double2 A = sm.a[i], B = sm.b[i], C = sm.c[i];
-        const double dx = fx - A.x, dy = fy - A.y;
-        const double m = B.x * dx * dx + B.y * dx * dy + C.x * dy * dy;
-        if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
-          // SFU exp, exact fp64 recompute near the skip/clamp thresholds
-          float ef;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ef) : "f"((float)(m * (-0.5 * BW_LOG2E))));
-          double gauss = (double)ef;
-          double sig = C.y * gauss;
-          if (fabs(sig - SIGMA_SKIP) <= 2e-6 * SIGMA_SKIP || fabs(sig - ALPHA_CLAMP) <= 2e-6) {
-            gauss = exp(-0.5 * m);
-            sig = C.y * gauss;
-          }
-          const bool clamped = sig > ALPHA_CLAMP;
-          if (clamped) sig = ALPHA_CLAMP;
-          if (!(sig < SIGMA_SKIP)) {
-            const double2 D = sm.d[i], E = sm.e[i];
-            const double cr = D.y, cg = E.x, cb = E.y;
-            const double one_minus = 1.0 - sig;
-            const double t_before = t_after / one_minus;
-            const double w = sig * t_before;
-            v[6] = (float)(gr * w);
-            v[7] = (float)(gg * w);
-            v[8] = (float)(gb * w);
-            double s_i = (gr * (cr * t_before - acc_r / one_minus) + gg * (cg * t_before - acc_g / one_minus)) +
-                         gb * (cb * t_before - acc_b / one_minus);
-            if (gtp != 0.0) s_i += gtp * (-t_fin / one_minus);
-            if (!clamped) {
-              const double cbh = 0.5 * B.y;  // conic xy
-              const double qd_x = B.x * dx + cbh * dy;
-              const double qd_y = cbh * dx + C.x * dy;
-              const double common = s_i * sig;
-              v[0] = (float)(common * qd_x);
-              v[1] = (float)(common * qd_y);
-              v[2] = (float)(0.5 * common * qd_x * qd_x);
-              v[3] = (float)(0.5 * common * qd_x * qd_y);
-              v[4] = (float)(0.5 * common * qd_y * qd_y);
-              v[5] = (float)(s_i * gauss);
-            }
-            acc_r += cr * w;
-            acc_g += cg * w;
-            acc_b += cb * w;
-            t_after = t_before;
-            contrib = true;
-          }
-        }
-      }
-      if (__any_sync(0xffffffffu, contrib)) {
+      const bool c0 = bw_pixel_step(q0, sm, i, lo + i, v);
+      if (__any_sync(0xffffffffu, c0)) {
         const float tot = warp_reduce_scatter16(v, lane);
         if ((lane & 1) == 0 && vidx < 9 && tot != 0.0f) atomicAdd(&screen[9 * (size_t)sm.gid[i] + vidx], (double)tot);
       }

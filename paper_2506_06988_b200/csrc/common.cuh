@@ -23,6 +23,8 @@ constexpr double SH_C0 = 0.28209479177387814;
 constexpr double SH_C1 = 0.4886025119029199;
 
 constexpr int NUM_SMS = 148;
+// privatised copies of the tile-rectangle difference grid (hgs_projected.tile_diff)
+constexpr int TILE_DIFF_COPIES = HGS_TILE_DIFF_COPIES;
 
 // Blend record per Gaussian (fp64, 80 B): the fields the per-pixel walk reads.
 struct __align__(16) BlendRec {

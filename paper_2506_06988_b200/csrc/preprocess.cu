@@ -36,7 +36,7 @@ __device__ __forceinline__ void quat_to_rot(double q0, double q1, double q2, dou
   Rq[8] = 1.0 - 2.0 * (x * x + y * y);
 }
 
-__global__ void __launch_bounds__(256) preprocess_kernel(const hgs_camera* __restrict__ cam_ptr, hgs_gaussians gs,
+__global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __restrict__ cam_ptr, hgs_gaussians gs,
                                                          int tile_px, int tiles_x, int tiles_y, hgs_projected out) {
   __shared__ CamConst cs;
   if (threadIdx.x == 0) load_cam(cam_ptr, cs);
@@ -134,6 +134,16 @@ __global__ void __launch_bounds__(256) preprocess_kernel(const hgs_camera* __res
   }
   out.count[i] = cnt;
   reinterpret_cast<ushort4*>(out.rect)[i] = rc;
+  if (out.sort_keys) out.sort_keys[i] = ok ? (uint64_t)__double_as_longlong(depth) : ~0ull;
+  if (out.tile_diff && ok) {  // rectangle into the 2D difference grid (tiles.py:45-50 counts per tile)
+    // TILE_DIFF_COPIES privatised copies spread the atomics over more L2 addresses
+    const int gw = tiles_x + 1;
+    int* grid = out.tile_diff + (size_t)(blockIdx.x % TILE_DIFF_COPIES) * (size_t)gw * (size_t)(tiles_y + 1);
+    atomicAdd(&grid[rc.z * gw + rc.x], 1);
+    atomicAdd(&grid[rc.z * gw + rc.y + 1], -1);
+    atomicAdd(&grid[(rc.w + 1) * gw + rc.x], -1);
+    atomicAdd(&grid[(rc.w + 1) * gw + rc.y + 1], 1);
+  }
 
   if (out.cull) {
     // conservative extents of the m <= 9 ellipse (|dx| <= 3 sqrt(cov_xx)), inflated for the fp32 compare
@@ -160,12 +170,22 @@ extern "C" int hgs_preprocess(const hgs_camera* cam, int32_t width, int32_t heig
   if (gs->n < 0) return hgs_set_error(HGS_ERR_INVALID, "hgs_preprocess: negative n");
   if (tile_px <= 0 || width <= 0 || height <= 0)
     return hgs_set_error(HGS_ERR_INVALID, "hgs_preprocess: tile_px/width/height must be positive");
-  if (gs->n == 0) return HGS_OK;
+  const int tx0 = (width + tile_px - 1) / tile_px, ty0 = (height + tile_px - 1) / tile_px;
+  if (gs->n == 0) {
+    if (out->tile_diff)
+      cudaMemsetAsync(out->tile_diff, 0, sizeof(int32_t) * hgs::TILE_DIFF_COPIES * (size_t)(tx0 + 1) * (size_t)(ty0 + 1),
+                      (cudaStream_t)stream);
+    return HGS_OK;
+  }
   if (!gs->centers || !gs->rotations || !gs->log_scales || !gs->logits || !gs->colors_dc || !out->rec ||
       !out->count || !out->rect)
     return hgs_set_error(HGS_ERR_INVALID, "hgs_preprocess: missing parameter/output pointer");
   const int tiles_x = (width + tile_px - 1) / tile_px, tiles_y = (height + tile_px - 1) / tile_px;
   if (tiles_x > 65535 || tiles_y > 65535) return hgs_set_error(HGS_ERR_INVALID, "hgs_preprocess: tile grid too large");
+  if (out->tile_diff)
+    cudaMemsetAsync(out->tile_diff, 0,
+                    sizeof(int32_t) * hgs::TILE_DIFF_COPIES * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1),
+                    (cudaStream_t)stream);
   hgs::preprocess_kernel<<<hgs::ceil_div(gs->n, 256), 256, 0, (cudaStream_t)stream>>>(cam, *gs, tile_px, tiles_x,
                                                                                        tiles_y, *out);
   HGS_CHECK_LAUNCH();

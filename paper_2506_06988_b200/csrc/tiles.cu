@@ -19,22 +19,12 @@
 
 namespace hgs {
 
-constexpr int DIFF_SMEM_CELLS = 12288;  // 48 KB of int counters
-
-__global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const int32_t* __restrict__ count,
-                                                               const BlendRec* __restrict__ rec,
-                                                               const ushort4* __restrict__ rect, int64_t n,
-                                                               int tiles_x, int tiles_y, uint64_t* dkeys,
-                                                               uint32_t* dvals, uint64_t* status, uint32_t* part_ctr,
-                                                               int64_t* counters, int* diff) {
+// Order-preserving compaction of the visible rows' sort keys (chained scan).
+// Each thread owns 16 consecutive keys, loaded as 8 x 16 B vectors.
+__global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                                               uint64_t* dkeys, uint32_t* dvals, uint64_t* status,
+                                                               uint32_t* part_ctr, int64_t* counters) {
   __shared__ int s_part;
-  extern __shared__ int s_diff[];
-  const int gw = tiles_x + 1, cells = (tiles_x + 1) * (tiles_y + 1);
-  const bool local = cells <= DIFF_SMEM_CELLS;
-  if (local)
-    for (int c = threadIdx.x; c < cells; c += blockDim.x) s_diff[c] = 0;
-  __syncthreads();
-  int* dst = local ? s_diff : diff;
   const int nparts = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
   while (true) {
     if (threadIdx.x == 0) s_part = (int)atomicAdd(part_ctr, 1u);
@@ -42,81 +32,105 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const int32_t* __
     const int part = s_part;
     __syncthreads();
     if (part >= nparts) break;
+    const int64_t base = (int64_t)part * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+    uint64_t k[SCAN_IPT];
+    if (base + SCAN_IPT <= n) {
+#pragma unroll
+      for (int j = 0; j < SCAN_IPT; j += 2) {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + j));
+        k[j] = v.x;
+        k[j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < SCAN_IPT; j++) k[j] = base + j < n ? keys[base + j] : ~0ull;
+    }
     uint64_t excl[SCAN_IPT];
     uint64_t total;
-    chained_scan_partition(part, n, [&](int64_t i) -> uint64_t { return count[i] > 0 ? 1ull : 0ull; }, status,
-                           excl, total);
-    const int64_t base = (int64_t)part * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+    chained_scan_partition(part, n, [&](int64_t i) -> uint64_t { return k[i - base] != ~0ull ? 1ull : 0ull; },
+                           status, excl, total);
 #pragma unroll
     for (int j = 0; j < SCAN_IPT; j++) {
-      const int64_t i = base + j;
-      if (i < n && count[i] > 0) {
-        dkeys[excl[j]] = (uint64_t)__double_as_longlong(rec[i].depth);
-        dvals[excl[j]] = (uint32_t)i;
-        const ushort4 rc = rect[i];  // x0, x1, y0, y1
-        atomicAdd(&dst[rc.z * gw + rc.x], 1);
-        atomicAdd(&dst[rc.z * gw + rc.y + 1], -1);
-        atomicAdd(&dst[(rc.w + 1) * gw + rc.x], -1);
-        atomicAdd(&dst[(rc.w + 1) * gw + rc.y + 1], 1);
+      if (k[j] != ~0ull) {
+        dkeys[excl[j]] = k[j];
+        dvals[excl[j]] = (uint32_t)(base + j);
       }
     }
     if (part == nparts - 1 && threadIdx.x == 0) counters[0] = (int64_t)total;
   }
-  if (local) {
-    __syncthreads();
-    for (int c = threadIdx.x; c < cells; c += blockDim.x)
-      if (s_diff[c]) atomicAdd(&diff[c], s_diff[c]);
-  }
 }
 
-// Per-tile counts from the difference grid (2D inclusive prefix sums), the
-// CSR starts (exclusive scan), K, the overflow flag, and the digit
-// histograms of the tile keys for the LSD passes.  One CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) tile_counts_kernel(int* diff, int tiles_x, int tiles_y, int64_t capacity,
-                                                           int64_t* tile_starts, int64_t* counters, uint32_t* hist) {
+// Per-tile counts from the difference grid (2D inclusive prefix sums, in
+// shared memory), the CSR starts (exclusive scan), K, the overflow flag, and
+// the digit histograms of the tile keys for the LSD passes.  One CTA.
+__global__ void __launch_bounds__(1024) tile_counts_kernel(const int* __restrict__ diff, int tiles_x, int tiles_y,
+                                                           int64_t capacity, int64_t* tile_starts, int64_t* counters,
+                                                           uint32_t* hist) {
+  extern __shared__ int g[];  // (tiles_x + 1) x (tiles_y + 1)
   __shared__ uint32_t sh[2][RADIX];
   __shared__ int64_t s_chunk[1024];
   const int gw = tiles_x + 1;
+  const int cells = gw * (tiles_y + 1);
   const int n_tiles = tiles_x * tiles_y;
   for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
-  // row prefix (along x), one thread per row
-  for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {
-    int run = 0;
-    for (int x = 0; x < tiles_x; x++) { run += diff[y * gw + x]; diff[y * gw + x] = run; }
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+    int v = 0;
+#pragma unroll
+    for (int k = 0; k < TILE_DIFF_COPIES; k++) v += diff[(size_t)k * cells + c];
+    g[c] = v;
   }
   __syncthreads();
-  // column prefix (along y), one thread per column
-  for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {
+  for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along x
     int run = 0;
-    for (int y = 0; y < tiles_y; y++) { run += diff[y * gw + x]; diff[y * gw + x] = run; }
+    for (int x = 0; x < tiles_x; x++) { run += g[y * gw + x]; g[y * gw + x] = run; }
   }
   __syncthreads();
-  // exclusive scan of counts in tile order: contiguous chunk per thread
+  for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along y
+    int run = 0;
+    for (int y = 0; y < tiles_y; y++) { run += g[y * gw + x]; g[y * gw + x] = run; }
+  }
+  __syncthreads();
   const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per, t1 = min(n_tiles, t0 + per);
   int64_t local_sum = 0;
   for (int t = t0; t < t1; t++) {
-    const int c = diff[(t / tiles_x) * gw + t % tiles_x];
+    const int c = g[(t / tiles_x) * gw + t % tiles_x];
     local_sum += c;
     if (c) {
       atomicAdd(&sh[0][t & 255], (uint32_t)c);
       atomicAdd(&sh[1][(t >> 8) & 255], (uint32_t)c);
     }
   }
-  s_chunk[threadIdx.x] = local_sum;
+  // block-wide exclusive scan of the chunk sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = local_sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_chunk[warp] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t run = 0;
-    for (int i = 0; i < (int)blockDim.x; i++) { const int64_t v = s_chunk[i]; s_chunk[i] = run; run += v; }
-    counters[1] = run;
-    counters[2] = run > capacity ? 1 : 0;
-    tile_starts[n_tiles] = run;
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? s_chunk[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s_chunk[lane] = w;  // inclusive over warps
   }
   __syncthreads();
-  int64_t run = s_chunk[threadIdx.x];
+  int64_t run = (warp > 0 ? s_chunk[warp - 1] : 0) + x - local_sum;
+  if (threadIdx.x == blockDim.x - 1) {
+    const int64_t total = s_chunk[(blockDim.x >> 5) - 1];
+    counters[1] = total;
+    counters[2] = total > capacity ? 1 : 0;
+    tile_starts[n_tiles] = total;
+  }
   for (int t = t0; t < t1; t++) {
     tile_starts[t] = run;
-    run += diff[(t / tiles_x) * gw + t % tiles_x];
+    run += g[(t / tiles_x) * gw + t % tiles_x];
   }
   for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) hist[i] = (&sh[0][0])[i];
 }
@@ -151,24 +165,50 @@ __global__ void __launch_bounds__(SCAN_THREADS) offsets_kernel(const int32_t* __
 
 // Warp-cooperative emission: a warp owns 32 consecutive rows of the depth
 // order; their entries are contiguous in the output, so lanes stride over
-// that span (coalesced stores), each finding its owning row by a binary
-// search over the 32 row offsets held in shared memory.
+// that span (coalesced stores), each lane advancing its owning row through
+// the 32 row offsets staged in shared memory.  Rows with more than
+// EMIT_BIG entries (near-camera Gaussians, which the depth order groups
+// together) are deferred to emit_big_kernel, one CTA per row, so they cannot
+// serialise a warp.
+constexpr uint32_t EMIT_BIG = 256;
+
+__device__ __forceinline__ void emit_entry(uint32_t o, uint32_t local, uint32_t x0, uint32_t y0, uint32_t rw,
+                                           uint32_t g, int tiles_x, uint16_t* tkeys, uint32_t* tvals) {
+  // local / rw with a float reciprocal (exact after one correction: local < 2^24, rw < 2^16)
+  uint32_t q = (uint32_t)((float)local * __frcp_rn((float)rw));
+  int32_t rr = (int32_t)(local - q * rw);
+  if (rr < 0) { q--; rr += rw; } else if (rr >= (int32_t)rw) { q++; rr -= rw; }
+  tkeys[o] = (uint16_t)((y0 + q) * (uint32_t)tiles_x + x0 + (uint32_t)rr);
+  tvals[o] = g;
+}
+__device__ __forceinline__ void emit_entry(uint32_t o, uint32_t local, uint32_t x0, uint32_t y0, uint32_t rw,
+                                           uint32_t g, int tiles_x, uint32_t* tkeys, uint32_t* tvals) {
+  uint32_t q = (uint32_t)((float)local * __frcp_rn((float)rw));
+  int32_t rr = (int32_t)(local - q * rw);
+  if (rr < 0) { q--; rr += rw; } else if (rr >= (int32_t)rw) { q++; rr -= rw; }
+  tkeys[o] = (y0 + q) * (uint32_t)tiles_x + x0 + (uint32_t)rr;
+  tvals[o] = g;
+}
+
 template <typename TK>
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ sorted_rows,
                                                    const uint32_t* __restrict__ offsets,
                                                    const ushort4* __restrict__ rect, const int64_t* counters,
-                                                   int tiles_x, int64_t capacity, TK* tkeys, uint32_t* tvals) {
+                                                   int tiles_x, int64_t capacity, TK* tkeys, uint32_t* tvals,
+                                                   uint32_t* big_rows, uint32_t* big_count) {
   __shared__ uint32_t s_off[8][32];
+  __shared__ uint32_t s_end[8][32];
   __shared__ uint32_t s_row[8][32];
   __shared__ uint32_t s_x0w[8][32];  // x0 | (width << 16)
   __shared__ uint32_t s_y0[8][32];
   const int64_t m = counters[0];
+  if (counters[1] > capacity) return;  // overflow: flagged in counters[2], nothing valid to emit
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
   for (int64_t j0 = ((int64_t)blockIdx.x * 8 + warp) * 32; j0 < m; j0 += nwarps * 32) {
     const int64_t j = j0 + lane;
     const bool valid = j < m;
-    uint32_t off = 0xffffffffu, cnt = 0;
+    uint32_t off = 0, cnt = 0;
     if (valid) {
       const uint32_t g = sorted_rows[j];
       off = offsets[j];
@@ -178,28 +218,50 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
       s_row[warp][lane] = g;
       s_x0w[warp][lane] = rc.x | (wdt << 16);
       s_y0[warp][lane] = rc.z;
+      if (cnt > EMIT_BIG) {
+        big_rows[atomicAdd(big_count, 1u)] = (uint32_t)j;
+        cnt = 0;  // emitted by emit_big_kernel
+      }
     }
-    s_off[warp][lane] = off;
+    s_off[warp][lane] = valid ? off : 0xffffffffu;
+    s_end[warp][lane] = off + cnt;
     const int last_lane = (int)tmin<int64_t>(31, m - 1 - j0);
     const uint32_t start = __shfl_sync(0xffffffffu, off, 0);
-    const uint32_t end = __shfl_sync(0xffffffffu, off + cnt, last_lane);
+    const uint32_t end = __shfl_sync(0xffffffffu, off + (valid ? cnt : 0), last_lane);
     __syncwarp();
+    int r = 0;  // owning row: non-decreasing along this lane's positions
     for (uint32_t o = start + lane; o < end; o += 32) {
-      int lo = 0, hi = last_lane;  // largest l with s_off[l] <= o
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_off[warp][mid] <= o) lo = mid; else hi = mid - 1;
+      while (r < last_lane && (s_end[warp][r] <= o)) r++;
+      if (o < s_off[warp][r]) {  // inside a deferred big row: jump past it, keeping o = start + lane (mod 32)
+        o += (s_off[warp][r] - o - 1) / 32 * 32;
+        continue;
       }
-      const uint32_t local = o - s_off[warp][lo];
-      const uint32_t x0w = s_x0w[warp][lo];
-      const uint32_t rw = x0w >> 16;
-      const uint32_t ty = s_y0[warp][lo] + local / rw, tx = (x0w & 0xffffu) + local % rw;
-      if (o < capacity) {
-        tkeys[o] = (TK)(ty * (uint32_t)tiles_x + tx);
-        tvals[o] = s_row[warp][lo];
-      }
+      const uint32_t x0w = s_x0w[warp][r];
+      emit_entry(o, o - s_off[warp][r], x0w & 0xffffu, s_y0[warp][r], x0w >> 16, s_row[warp][r], tiles_x, tkeys,
+                 tvals);
     }
     __syncwarp();
+  }
+}
+
+template <typename TK>
+__global__ void __launch_bounds__(256) emit_big_kernel(const uint32_t* __restrict__ sorted_rows,
+                                                       const uint32_t* __restrict__ offsets,
+                                                       const ushort4* __restrict__ rect, const int64_t* counters,
+                                                       int tiles_x, int64_t capacity, TK* tkeys, uint32_t* tvals,
+                                                       const uint32_t* __restrict__ big_rows,
+                                                       const uint32_t* __restrict__ big_count) {
+  if (counters[1] > capacity) return;
+  const uint32_t nbig = *big_count;
+  for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+    const uint32_t j = big_rows[b];
+    const uint32_t g = sorted_rows[j];
+    const uint32_t off = offsets[j];
+    const ushort4 rc = rect[g];
+    const uint32_t rw = rc.y - rc.x + 1;
+    const uint32_t cnt = rw * (uint32_t)(rc.w - rc.z + 1);
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x)
+      emit_entry(off + t, t, rc.x, rc.z, rw, g, tiles_x, tkeys, tvals);
   }
 }
 
@@ -209,6 +271,7 @@ struct TilesScratch {
   uint64_t* dk[2];
   uint32_t* dv[2];
   uint32_t* offsets;
+  uint32_t* big_rows;
   void* tk[2];
   uint32_t* tv0;
   uint32_t* tv1;
@@ -242,6 +305,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.dv[0] = (uint32_t*)take(4 * nn);
   t.dv[1] = (uint32_t*)take(4 * nn);
   t.offsets = (uint32_t*)take(4 * nn);
+  t.big_rows = (uint32_t*)take(4 * nn);
   t.tk[0] = take(tkw * cc);
   t.tk[1] = take(tkw * cc);
   t.tv0 = (uint32_t*)take(4 * cc);
@@ -330,7 +394,8 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   if (!tiles->entries || !tiles->tile_starts || !tiles->counters)
     return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: missing output pointer");
   if (tiles->tiles_x <= 0 || tiles->tiles_y <= 0) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: empty tile grid");
-  if (!proj->count || !proj->rect || !proj->rec) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: missing projection");
+  if (!proj->count || !proj->rect || !proj->rec || !proj->sort_keys || !proj->tile_diff)
+    return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: projection needs count, rect, rec, sort_keys, tile_diff");
   const int tx = tiles->tiles_x, ty = tiles->tiles_y;
   const int n_tiles = tx * ty;
   if (n > 0xffffffffLL || tiles->capacity > (1LL << 30) || n_tiles > (1 << 24))
@@ -343,26 +408,25 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   carve(n, tiles->capacity, tx, ty, (unsigned char*)tiles->scratch, &s);
   cudaMemsetAsync(s.control_begin, 0, s.control_bytes, st);
   cudaMemsetAsync(tiles->counters, 0, 4 * sizeof(int64_t), st);
-  // 1. compaction of visible rows + tile-rectangle difference grid
-  const int cells = (tx + 1) * (ty + 1);
-  const size_t diff_smem = cells <= DIFF_SMEM_CELLS ? sizeof(int) * (size_t)cells : 0;
+  // 1. order-preserving compaction of the visible rows' depth keys
   static int scan_grid_cap = 0;
-  if (scan_grid_cap == 0) {
-    cudaFuncSetAttribute(compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(int) * DIFF_SMEM_CELLS));
-    scan_grid_cap = persistent_grid((const void*)compact_kernel, SCAN_THREADS, sizeof(int) * DIFF_SMEM_CELLS);
-  }
+  if (scan_grid_cap == 0) scan_grid_cap = persistent_grid((const void*)compact_kernel, SCAN_THREADS, 0);
   const int scan_grid = (int)tmax<int64_t>(1, tmin<int64_t>(scan_grid_cap, (n + SCAN_TILE - 1) / SCAN_TILE));
   if (n > 0) {
-    compact_kernel<<<scan_grid, SCAN_THREADS, diff_smem, st>>>(proj->count, (const BlendRec*)proj->rec,
-                                                              (const ushort4*)proj->rect, n, tx, ty, s.dk[0],
-                                                              s.dv[0], s.scan_status, s.part_ctr + 20,
-                                                              tiles->counters, s.diff);
+    compact_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->sort_keys, n, s.dk[0], s.dv[0], s.scan_status,
+                                                       s.part_ctr + 20, tiles->counters);
     HGS_CHECK_LAUNCH();
   }
   // 2. per-tile counts -> tile_starts, K, overflow, tile-key histograms
-  tile_counts_kernel<<<1, 1024, 0, st>>>(s.diff, tx, ty, tiles->capacity, tiles->tile_starts, tiles->counters,
-                                         s.hist + 8 * RADIX);
+  const size_t grid_smem = sizeof(int) * (size_t)(tx + 1) * (size_t)(ty + 1);
+  if (grid_smem > 200 * 1024) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large");
+  static bool tc_attr = false;
+  if (!tc_attr) {
+    cudaFuncSetAttribute(tile_counts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    tc_attr = true;
+  }
+  tile_counts_kernel<<<1, 1024, grid_smem, st>>>(proj->tile_diff, tx, ty, tiles->capacity, tiles->tile_starts,
+                                                 tiles->counters, s.hist + 8 * RADIX);
   HGS_CHECK_LAUNCH();
   if (n == 0) return HGS_OK;
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
@@ -383,7 +447,11 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   if (n_tiles > 65535) {
     emit_kernel<uint32_t><<<4 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
                                                           tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],
-                                                          s.tv0);
+                                                          s.tv0, s.big_rows, s.part_ctr + 22);
+    HGS_CHECK_LAUNCH();
+    emit_big_kernel<uint32_t><<<2 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+                                                              tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],
+                                                              s.tv0, s.big_rows, s.part_ctr + 22);
     HGS_CHECK_LAUNCH();
     rc = radix_sort<uint32_t>((uint32_t*)s.tk[0], (uint32_t*)s.tk[1], s.tv0, s.tv1, tiles->entries,
                               tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, true, rs_tile_status,
@@ -391,7 +459,11 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   } else {
     emit_kernel<uint16_t><<<4 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
                                                           tiles->counters, tx, tiles->capacity, (uint16_t*)s.tk[0],
-                                                          s.tv0);
+                                                          s.tv0, s.big_rows, s.part_ctr + 22);
+    HGS_CHECK_LAUNCH();
+    emit_big_kernel<uint16_t><<<2 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+                                                              tiles->counters, tx, tiles->capacity, (uint16_t*)s.tk[0],
+                                                              s.tv0, s.big_rows, s.part_ctr + 22);
     HGS_CHECK_LAUNCH();
     rc = radix_sort<uint16_t>((uint16_t*)s.tk[0], (uint16_t*)s.tk[1], s.tv0, s.tv1, tiles->entries,
                               tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, true, rs_tile_status,

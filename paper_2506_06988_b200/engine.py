@@ -49,6 +49,8 @@ class HybridRenderer:
         self.count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
         self.cull = torch.empty(n * 8, dtype=torch.float32, device=dev)
+        self.sort_keys = torch.empty(n, dtype=torch.int64, device=dev)
+        self.tile_diff = torch.empty(16 * (self.tiles_x + 1) * (self.tiles_y + 1), dtype=torch.int32, device=dev)
         self.fixup = torch.zeros(h * w + 1, dtype=torch.int32, device=dev)
         self.tile_starts = torch.zeros(self.n_tiles + 1, dtype=torch.int64, device=dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -91,6 +93,7 @@ class HybridRenderer:
         ps = _lib.HGSProjected()
         ps.rec, ps.count, ps.rect = _lib.ptr(self.rec), _lib.ptr(self.count), _lib.ptr(self.rect)
         ps.cull = _lib.ptr(self.cull)
+        ps.sort_keys, ps.tile_diff = _lib.ptr(self.sort_keys), _lib.ptr(self.tile_diff)
         ts = _lib.HGSTiles()
         ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tiles_x, self.tiles_y, TILE_PX, self.capacity
         ts.entries, ts.tile_starts, ts.counters = _lib.ptr(self.entries), _lib.ptr(self.tile_starts), _lib.ptr(self.counters)
@@ -171,7 +174,7 @@ class HybridRenderer:
     # views for the API / backward ----------------------------------------
     def projected(self) -> ProjectedGaussians:
         return ProjectedGaussians(len(self.gs), self.rec, self.count, self.rect, None, self.width,
-                                  self.height, TILE_PX, self.cull)
+                                  self.height, TILE_PX, self.cull, self.sort_keys, self.tile_diff)
 
     def tiles(self) -> TileBins:
         return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected())

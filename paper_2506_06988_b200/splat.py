@@ -85,7 +85,9 @@ class ProjectedGaussians:
     view_dist) over the device state indexed by original row (rec, count,
     rect) that build_tiles / rasterize_forward consume."""
 
-    def __init__(self, n, rec, count, rect, extras=None, width=None, height=None, tile_px=TILE_PX, cull=None):
+    def __init__(self, n, rec, count, rect, extras=None, width=None, height=None, tile_px=TILE_PX, cull=None,
+                 sort_keys=None, tile_diff=None):
+        self.sort_keys, self.tile_diff = sort_keys, tile_diff
         # count may be longer than n (buffers are allocated with >= 1 row so
         # their device pointers are never NULL); the API view is count[:n]
         self._count_buf = count
@@ -98,6 +100,7 @@ class ProjectedGaussians:
         s = _lib.HGSProjected()
         s.rec, s.count, s.rect = _lib.ptr(self.rec), _lib.ptr(self._count_buf), _lib.ptr(self.rect)
         s.cull = _lib.ptr(self.cull)
+        s.sort_keys, s.tile_diff = _lib.ptr(self.sort_keys), _lib.ptr(self.tile_diff)
         return s
 
     def _fields(self):
@@ -254,9 +257,14 @@ def _preprocess(gs: GaussianSet, cam, cam_dev, tile_px: int, extras: bool) -> Pr
     count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
     rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
     cull = torch.empty(max(n, 1) * 8, dtype=torch.float32, device=dev)
+    sort_keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    tx = (int(cam.width) + tile_px - 1) // tile_px
+    ty = (int(cam.height) + tile_px - 1) // tile_px
+    tile_diff = torch.empty(16 * (tx + 1) * (ty + 1), dtype=torch.int32, device=dev)
     ex = None
     ps = _lib.HGSProjected()
     ps.rec, ps.count, ps.rect, ps.cull = _lib.ptr(rec), _lib.ptr(count), _lib.ptr(rect), _lib.ptr(cull)
+    ps.sort_keys, ps.tile_diff = _lib.ptr(sort_keys), _lib.ptr(tile_diff)
     if extras:
         f64 = dict(dtype=torch.float64, device=dev)
         ex = {"cov2d": torch.zeros(n, 3, **f64), "radius": torch.zeros(n, **f64), "t_cam": torch.zeros(n, 3, **f64),
@@ -268,7 +276,8 @@ def _preprocess(gs: GaussianSet, cam, cam_dev, tile_px: int, extras: bool) -> Pr
             setattr(ps, k, _lib.ptr(v))
     _lib.call("hgs_preprocess", _lib.ptr(cam_dev), int(cam.width), int(cam.height), ctypes.byref(gs.struct()),
               int(tile_px), ctypes.byref(ps), _stream_ptr(dev))
-    return ProjectedGaussians(n, rec, count, rect, ex, int(cam.width), int(cam.height), tile_px, cull)
+    return ProjectedGaussians(n, rec, count, rect, ex, int(cam.width), int(cam.height), tile_px, cull, sort_keys,
+                              tile_diff)
 
 
 def project(gs, cam) -> ProjectedGaussians:

@@ -85,7 +85,12 @@ class HybridTrainer:
         self.count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
         self.rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
         self.cull = torch.empty(max(n, 1) * 8, dtype=torch.float32, device=dev)
+        self.sort_keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         self.screen = torch.zeros(max(n, 1) * 9, dtype=torch.float64, device=dev)
+        c0 = self.cameras[0]
+        self.tx = (int(c0.width) + TILE_PX - 1) // TILE_PX
+        self.ty = (int(c0.height) + TILE_PX - 1) // TILE_PX
+        self.tile_diff = torch.empty(16 * (self.tx + 1) * (self.ty + 1), dtype=torch.int32, device=dev)
         self.capacity = 0
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
         self.overflow = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -119,10 +124,11 @@ class HybridTrainer:
         ps = _lib.HGSProjected()
         ps.rec, ps.count, ps.rect, ps.cull = (_lib.ptr(self.rec), _lib.ptr(self.count), _lib.ptr(self.rect),
                                               _lib.ptr(self.cull))
+        ps.sort_keys, ps.tile_diff = _lib.ptr(self.sort_keys), _lib.ptr(self.tile_diff)
         _lib.call("hgs_preprocess", _lib.ptr(self.cam_dev[v]), int(cam.width), int(cam.height),
                   ctypes.byref(self.gs.struct()), TILE_PX, ctypes.byref(ps), _stream_ptr(self.dev))
         return ProjectedGaussians(len(self.gs), self.rec, self.count, self.rect, None, int(cam.width),
-                                  int(cam.height), TILE_PX, self.cull)
+                                  int(cam.height), TILE_PX, self.cull, self.sort_keys, self.tile_diff)
 
     def _tiles(self, proj) -> TileBins:
         ts = _lib.HGSTiles()
