@@ -30,6 +30,7 @@ constexpr uint64_t SCAN_FLAG_INC = 2ull << 62;
 constexpr uint64_t SCAN_VALUE_MASK = (1ull << 62) - 1;
 
 constexpr uint32_t SPIN_LIMIT = 1u << 24;
+constexpr int LB_WINDOW = 16;  // predecessors read per look-back round trip
 constexpr uint32_t RS_FLAG_AGG = 1u << 30;
 constexpr uint32_t RS_FLAG_INC = 2u << 30;
 constexpr uint32_t RS_VALUE_MASK = (1u << 30) - 1;
@@ -168,21 +169,22 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ k
   }
 }
 
-template <typename K>
+template <typename K, int IPT = RS_IPT>
 struct RadixSmem {
-  K keys[RS_TILE];
-  uint32_t vals[RS_TILE];
+  K keys[RS_THREADS * IPT];
+  uint32_t vals[RS_THREADS * IPT];
 };
 
 // One stable LSD pass over the digit at `shift`.
-template <typename K>
-__global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 8 ? 2 : 3) radix_pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+template <typename K, int IPT>
+__global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2 : 3)) radix_pass_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                                 K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                                 const int64_t* count_ptr, int64_t cap, int shift,
                                                                 const uint32_t* __restrict__ hist, uint32_t* status,
                                                                 int nparts_cap, uint32_t* part_ctr, int write_keys) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  RadixSmem<K>& sm = *reinterpret_cast<RadixSmem<K>*>(smem_raw);
+  RadixSmem<K, IPT>& sm = *reinterpret_cast<RadixSmem<K, IPT>*>(smem_raw);
+  constexpr int TILE = RS_THREADS * IPT;
   __shared__ uint32_t whist[RS_WARPS][RADIX];
   __shared__ uint32_t s_digit_base[RADIX];
   __shared__ uint32_t s_gstart[RADIX];
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 8 ? 2 : 3) radix_pass
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t n = count_ptr ? *count_ptr : cap;
   if (n > cap) n = cap;
-  const int nparts = (int)((n + RS_TILE - 1) / RS_TILE);
+  const int nparts = (int)((n + TILE - 1) / TILE);
   {
     uint32_t tot;
     uint32_t e = block_exclusive_scan<uint32_t>(hist[tid], s_warp, tot);
@@ -205,23 +207,23 @@ __global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 8 ? 2 : 3) radix_pass
     __syncthreads();
     const int part = s_part;
     if (part >= nparts) break;
-    const int64_t base = (int64_t)part * RS_TILE;
-    const int tile_n = (int)tmin<int64_t>(RS_TILE, n - base);
+    const int64_t base = (int64_t)part * TILE;
+    const int tile_n = (int)tmin<int64_t>(TILE, n - base);
 
-    K k[RS_IPT];
-    uint32_t v[RS_IPT];
-    uint32_t rank[RS_IPT];
+    K k[IPT];
+    uint32_t v[IPT];
+    uint32_t rank[IPT];
 #pragma unroll
-    for (int j = 0; j < RS_IPT; j++) {
-      const int li = warp * (RS_IPT * 32) + j * 32 + lane;
+    for (int j = 0; j < IPT; j++) {
+      const int li = warp * (IPT * 32) + j * 32 + lane;
       if (li < tile_n) {
         k[j] = kin[base + li];
         v[j] = vin[base + li];
       }
     }
 #pragma unroll
-    for (int j = 0; j < RS_IPT; j++) {
-      const int li = warp * (RS_IPT * 32) + j * 32 + lane;
+    for (int j = 0; j < IPT; j++) {
+      const int li = warp * (IPT * 32) + j * 32 + lane;
       const bool valid = li < tile_n;
       const unsigned active = __ballot_sync(0xffffffffu, valid);
       uint32_t d = 0, peers = 0, base_cnt = 0;
@@ -258,16 +260,17 @@ __global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 8 ? 2 : 3) radix_pass
         bool fin = false;
         while (!fin) {
           // wait (one load per poll) until the nearest unread predecessor is
-          // published, then read a window of 16 and consume its ready prefix
+          // published, then read a window of LB_WINDOW and consume its ready prefix
           for (uint32_t spin = 0; (ld_relaxed(st + (size_t)p * RADIX) & ~RS_VALUE_MASK) == 0; spin++)
             if (spin > SPIN_LIMIT) { fin = true; break; }  // watchdog: never hang the GPU
           if (fin) break;
-          uint32_t w[16];
+          uint32_t w[LB_WINDOW];
 #pragma unroll
-          for (int k = 0; k < 16; k++) w[k] = (p - k >= 0) ? ld_relaxed(st + (size_t)(p - k) * RADIX) : RS_FLAG_INC;
+          for (int k = 0; k < LB_WINDOW; k++)
+            w[k] = (p - k >= 0) ? ld_relaxed(st + (size_t)(p - k) * RADIX) : RS_FLAG_INC;
           int used = 0;
 #pragma unroll
-          for (int k = 0; k < 16; k++) {
+          for (int k = 0; k < LB_WINDOW; k++) {
             if (fin || used < k) continue;  // stopped earlier in this window
             const uint32_t flag = w[k] & ~RS_VALUE_MASK;
             if (flag == 0) continue;        // not ready: re-read from here
@@ -287,8 +290,8 @@ __global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 8 ? 2 : 3) radix_pass
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < RS_IPT; j++) {
-      const int li = warp * (RS_IPT * 32) + j * 32 + lane;
+    for (int j = 0; j < IPT; j++) {
+      const int li = warp * (IPT * 32) + j * 32 + lane;
       if (li < tile_n) {
         const uint32_t d = digit_of<K>(k[j], shift);
         const uint32_t pos = s_lstart[d] + whist[warp][d] + rank[j];

@@ -23,8 +23,10 @@ namespace hgs {
 // Each thread owns 16 consecutive keys, loaded as 8 x 16 B vectors.
 __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* __restrict__ keys, int64_t n,
                                                                uint64_t* dkeys, uint32_t* dvals, uint64_t* status,
-                                                               uint32_t* part_ctr, int64_t* counters) {
+                                                               uint32_t* part_ctr, int64_t* counters,
+                                                               unsigned long long* minmax) {
   __shared__ int s_part;
+  unsigned long long nmin = 0, kmax = 0;  // max of ~key (== ~min key) and max key over visible rows
   const int nparts = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
   while (true) {
     if (threadIdx.x == 0) s_part = (int)atomicAdd(part_ctr, 1u);
@@ -54,9 +56,81 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
       if (k[j] != ~0ull) {
         dkeys[excl[j]] = k[j];
         dvals[excl[j]] = (uint32_t)(base + j);
+        nmin = max(nmin, (unsigned long long)~k[j]);
+        kmax = max(kmax, (unsigned long long)k[j]);
       }
     }
     if (part == nparts - 1 && threadIdx.x == 0) counters[0] = (int64_t)total;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nmin = max(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if ((threadIdx.x & 31) == 0 && kmax) {
+    atomicMax(&minmax[0], nmin);
+    atomicMax(&minmax[1], kmax);
+  }
+}
+
+// Depth keys -> 32 bits, order preserving: (bits - min) >> shift, where
+// shift drops the low bits the visible range does not need.  Equal 32-bit
+// keys from distinct fp64 depths are re-ordered exactly by depth_fixup_kernel.
+__device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
+  const unsigned long long lo = ~minmax[0], hi = minmax[1];
+  const unsigned long long range = hi > lo ? hi - lo : 0;
+  const int bits = range ? 64 - __clzll((long long)range) : 0;
+  return bits > 32 ? bits - 32 : 0;
+}
+
+__global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __restrict__ keys, const int64_t* counters,
+                                                          const unsigned long long* __restrict__ minmax,
+                                                          uint32_t* __restrict__ k32) {
+  const int64_t m = counters[0];
+  const unsigned long long lo = ~minmax[0];
+  const int sh = depth_shift(minmax);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    k32[j] = (uint32_t)((keys[j] - lo) >> sh);
+}
+
+// After the stable 32-bit sort, rows with equal truncated keys are in row
+// order; the reference order is (fp64 depth, row): re-sort each such run by
+// the full 64-bit depth key (runs are rare and short; long runs of exactly
+// equal depths are already ordered and only verified).
+__global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ rows,
+                                                          const BlendRec* __restrict__ rec, const int64_t* counters,
+                                                          const unsigned long long* __restrict__ minmax) {
+  const int64_t m = counters[0];
+  if (depth_shift(minmax) == 0) return;  // keys were exact
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t kj = k32[j];
+    if (j > 0 && k32[j - 1] == kj) continue;        // not a run start
+    if (j + 1 >= m || k32[j + 1] != kj) continue;   // singleton
+    int64_t e = j + 1;
+    while (e < m && k32[e] == kj) e++;
+    auto key64 = [&](uint32_t row) { return (unsigned long long)__double_as_longlong(rec[row].depth); };
+    bool sorted = true;
+    for (int64_t t = j + 1; t < e && sorted; t++) {
+      const unsigned long long a = key64(rows[t - 1]), b = key64(rows[t]);
+      sorted = a < b || (a == b && rows[t - 1] < rows[t]);
+    }
+    if (sorted) continue;
+    // Shell sort by (key64, row): correct for any run length
+    const int64_t len = e - j;
+    for (int64_t gap = len / 2; gap > 0; gap /= 2)
+      for (int64_t t = j + gap; t < e; t++) {
+        const uint32_t r = rows[t];
+        const unsigned long long kr = key64(r);
+        int64_t u = t;
+        while (u >= j + gap) {
+          const uint32_t ru = rows[u - gap];
+          const unsigned long long ku = key64(ru);
+          if (ku < kr || (ku == kr && ru < r)) break;
+          rows[u] = ru;
+          u -= gap;
+        }
+        rows[u] = r;
+      }
   }
 }
 
@@ -315,7 +389,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 2 * parts_k));
   t.scan_status = (uint64_t*)take(sizeof(uint64_t) * (size_t)(2 * (parts_n + 1)));
   t.hist = (uint32_t*)take(sizeof(uint32_t) * 10 * RADIX);
-  t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);
+  t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);  // [24..27]: depth key min/max (u64 x 2)
   t.diff = (int*)take(sizeof(int) * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1));
   t.control_bytes = off - ctl0;
   t.parts_n = parts_n;
@@ -346,16 +420,18 @@ static int persistent_grid(const void* fn, int threads, size_t smem) {
 // shift0: one histogram kernel for all passes, then one single-pass
 // (decoupled look-back) kernel per pass.  The last pass writes its values to
 // final_vals when given.
-template <typename K>
+template <typename K, int IPT = RS_IPT>
 static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_vals, const int64_t* count_ptr,
                       int64_t cap, int shift0, int npasses, uint32_t* hist, bool hist_ready, uint32_t* status,
                       int64_t parts, uint32_t* part_ctr, cudaStream_t st, K** keys_result, bool last_keys) {
-  const size_t smem = sizeof(RadixSmem<K>);
+  const size_t smem = sizeof(RadixSmem<K, IPT>);
   static int grid = 0;
   if (grid == 0) {
-    cudaFuncSetAttribute(radix_pass_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    grid = persistent_grid((const void*)radix_pass_kernel<K>, RS_THREADS, smem);
+    cudaFuncSetAttribute(radix_pass_kernel<K, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    grid = persistent_grid((const void*)radix_pass_kernel<K, IPT>, RS_THREADS, smem);
   }
+  const int64_t tile = (int64_t)RS_THREADS * IPT;
+  parts = (cap + tile - 1) / tile;  // partitions of this pass width (status sized for RS_TILE partitions)
   if (!hist_ready) {
     radix_hist_kernel<K><<<2 * sm_count(), 256, 0, st>>>(k0, count_ptr, cap, shift0, npasses, hist);
     HGS_CHECK_LAUNCH();
@@ -368,7 +444,7 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
   for (int p = 0; p < npasses; p++) {
     const bool last = p == npasses - 1;
     uint32_t* vdst = last && final_vals ? final_vals : vout;
-    radix_pass_kernel<K><<<g, RS_THREADS, smem, st>>>(kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
+    radix_pass_kernel<K, IPT><<<g, RS_THREADS, smem, st>>>(kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
                                                       hist + RADIX * p, status + (size_t)p * parts * RADIX, (int)parts,
                                                       part_ctr + p, (!last || last_keys) ? 1 : 0);
     HGS_CHECK_LAUNCH();
@@ -414,7 +490,8 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   const int scan_grid = (int)tmax<int64_t>(1, tmin<int64_t>(scan_grid_cap, (n + SCAN_TILE - 1) / SCAN_TILE));
   if (n > 0) {
     compact_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->sort_keys, n, s.dk[0], s.dv[0], s.scan_status,
-                                                       s.part_ctr + 20, tiles->counters);
+                                                       s.part_ctr + 20, tiles->counters,
+                                                       reinterpret_cast<unsigned long long*>(s.part_ctr + 24));
     HGS_CHECK_LAUNCH();
   }
   // 2. per-tile counts -> tile_starts, K, overflow, tile-key histograms
@@ -430,9 +507,19 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   HGS_CHECK_LAUNCH();
   if (n == 0) return HGS_OK;
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
-  int rc = radix_sort<uint64_t>(s.dk[0], s.dk[1], s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0, 8, s.hist, false,
-                                s.rs_status, s.parts_n, s.part_ctr, st, nullptr, true);
+  // 32-bit order-preserving remap of the depth keys, 4 passes, exact fix-up of truncation ties
+  uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
+  uint32_t* k32b = k32a + (n > 0 ? n : 1);
+  unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
+  depth_remap_kernel<<<4 * sm_count(), 256, 0, st>>>(s.dk[0], tiles->counters, minmax, k32a);
+  HGS_CHECK_LAUNCH();
+  uint32_t* k32res = nullptr;
+  int rc = radix_sort<uint32_t, 8>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0, 4, s.hist, false,
+                                s.rs_status, s.parts_n, s.part_ctr, st, &k32res, true);
   if (rc) return rc;
+  depth_fixup_kernel<<<4 * sm_count(), 256, 0, st>>>(k32res, s.dv[0], (const BlendRec*)proj->rec, tiles->counters,
+                                                     minmax);
+  HGS_CHECK_LAUNCH();
   // 4. offsets of each row's entries in depth order
   offsets_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->count, s.dv[0], tiles->counters, s.offsets,
                                                      s.scan_status + s.parts_n + 1, s.part_ctr + 21, tiles->counters,

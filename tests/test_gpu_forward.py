@@ -158,3 +158,31 @@ def test_c2_matches_oracle(cfg, cuda_device):
     assert np.array_equal(np_(ctx.last_consumed), last)
     assert_close(np_(out.color), color, atol=1e-6, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-6, what="T")
+
+
+def test_depth_order_exact_under_key_truncation(cuda_device):
+    """The depth sort runs on 32-bit truncated keys; runs of distinct fp64
+    depths that share a truncated key must still come out in exact
+    (depth, row) order.  Cluster many Gaussians within a few ulps of one
+    depth while other Gaussians stretch the depth range."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import synthetic as syn
+    rng = np.random.default_rng(11)
+    n = 3000
+    cam = syn.look_at((0.0, 0.0, 0.0), (0.0, 0.0, 1.0), width=64, height=64)
+    z = np.where(np.arange(n) % 3 == 0, rng.uniform(0.5, 60.0, n), 4.0)
+    xy = rng.uniform(-0.8, 0.8, (n, 2)) * z[:, None] * 0.5
+    pc = np.column_stack([xy, z])
+    # tiny fp32-representable perturbations of the clustered depths
+    pc[np.arange(n) % 3 != 0, 2] += rng.integers(-40, 40, (n - (n + 2) // 3)) * 2.0 ** -21
+    R, t = cam.rotation, cam.translation
+    gs = syn.HostGaussians(syn.q32((pc - t) @ R), syn.q32(rng.normal(size=(n, 4))),
+                           syn.q32(rng.uniform(-4.0, -2.5, (n, 3))), syn.q32(rng.uniform(-2, 1, n)),
+                           syn.q32(rng.uniform(-1, 1, (n, 3))))
+    p = orc.project(gs, cam)
+    t_ref = orc.build_tiles(p, 64, 64)
+    g, c, _ = dev_scene(gs, cam, None)
+    dp = hgs.project(g, c)
+    dt = hgs.build_tiles(dp, 64, 64)
+    assert np.array_equal(np_(dt.tile_starts), t_ref.tile_starts)
+    assert np.array_equal(np_(dt.entries), t_ref.entries)
