@@ -36,6 +36,8 @@ extern "C" {
 
 #define HGS_ABI_VERSION 1
 #define HGS_TILE_DIFF_COPIES 16
+/* fp32 words per row of hgs_projected.cull */
+#define HGS_CULL_FLOATS 12
 
 /* Pinhole camera, Camera (scene.py:144-203).  Derived fields are computed by
    the host exactly as the reference computes them:
@@ -91,8 +93,10 @@ typedef struct hgs_projected {
   double* color_pre; /* N x 3, optional */
   double* view_dir;  /* N x 3, optional (SH degree 1 only) */
   double* view_dist; /* N, optional (SH degree 1 only) */
-  void* cull;        /* N x 32 B fp32 {mean x, mean y, 3-sigma half extents x, y; conic xx, xy, yy, 0}: blend culling records
-                        (optional; without it hgs_blend_forward runs the exact per-pixel walk only) */
+  void* cull;        /* N x 48 B fp32 (HGS_CULL_FLOATS) {mean x, mean y, 3-sigma half extents x, y;
+                        conic xx, xy, yy, depth; alpha (negated: ill-conditioned conic, always evaluated
+                        exactly), r, g, b}: blend culling + fast-path records (optional; without it
+                        hgs_blend_forward runs the exact per-pixel walk only) */
   uint64_t* sort_keys; /* N: fp64 depth bit pattern of visible rows, ~0 for culled rows (required by
                           hgs_build_tiles) */
   int32_t* tile_diff;  /* HGS_TILE_DIFF_COPIES x (tiles_x + 1) x (tiles_y + 1) 2D difference grids of the rows'

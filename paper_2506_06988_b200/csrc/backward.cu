@@ -28,8 +28,8 @@ constexpr double BW_LOG2E = 1.4426950408889634;
 struct BwSmem {
   double2 a[BW_BATCH];  // mean x, y
   double2 b[BW_BATCH];  // conic xx, 2*xy
-  double2 c[BW_BATCH];  // conic yy, alpha
-  double2 d[BW_BATCH];  // depth, r
+  double2 c[BW_BATCH];  // conic yy, depth
+  double2 d[BW_BATCH];  // alpha, r
   double2 e[BW_BATCH];  // g, b
   float4 box[BW_BATCH];
   float4 con[BW_BATCH];
@@ -156,10 +156,11 @@ __device__ __forceinline__ bool bw_pixel_step(BwPix& q, const BwSmem& sm, int i,
   float ef;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ef) : "f"((float)(m * (-0.5 * BW_LOG2E))));
   double gauss = (double)ef;
-  double sig = C.y * gauss;
+  const double alpha = sm.d[i].x;
+  double sig = alpha * gauss;
   if (fabs(sig - SIGMA_SKIP) <= 2e-6 * SIGMA_SKIP || fabs(sig - ALPHA_CLAMP) <= 2e-6) {
     gauss = exp(-0.5 * m);
-    sig = C.y * gauss;
+    sig = alpha * gauss;
   }
   const bool clamped = sig > ALPHA_CLAMP;
   if (clamped) sig = ALPHA_CLAMP;
@@ -236,8 +237,8 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
       sm.c[i] = __ldg(rp + 2);
       sm.d[i] = __ldg(rp + 3);
       sm.e[i] = __ldg(rp + 4);
-      sm.box[i] = __ldg(cull + 2 * (size_t)g);
-      sm.con[i] = __ldg(cull + 2 * (size_t)g + 1);
+      sm.box[i] = __ldg(cull + 3 * (size_t)g);
+      sm.con[i] = __ldg(cull + 3 * (size_t)g + 1);
       sm.gid[i] = g;
     }
     __syncthreads();

@@ -5,23 +5,30 @@
 // Fast path (blend_fast_kernel): one CTA per 16x16 tile, warp-specialised:
 // 8 consumer warps each own an 8x4 sub-tile (one pixel per lane), 1
 // producer warp streams the tile's depth-sorted entry list through a
-// 4-stage shared-memory ring (128 entries x 96 B per stage: the 80 B fp64
-// blend record + a 16 B fp32 cull box) with cp.async, completion tracked
-// by mbarriers (full: producer -> consumers, empty: consumers -> producer).
-// Consumers never meet at a CTA barrier: each compacts every stage to the
-// entries whose 3-sigma box touches its sub-tile (ballot, order
-// preserving) and runs the reference's front-to-back loop over that list.
-// Once every consumer's pixels are done the producer stops streaming.
+// 4-stage shared-memory ring (128 entries x 112 B per stage: 64 B of the
+// fp64 blend record + the 48 B fp32 CullRec) with cp.async, completion
+// tracked by mbarriers (full: producer -> consumers, empty: consumers ->
+// producer).  Consumers never meet at a CTA barrier: each compacts every
+// stage to the entries whose support ellipse touches its sub-tile (ballot,
+// order preserving) and runs the reference's front-to-back loop over that
+// list.  Once every consumer's pixels are done the producer stops.
 //
-// Per pixel-entry pair: exact fp64 support test (reference operation
-// order), exp() on the SFU (rel. err <= 6e-7), fp64 accumulation.  The two
-// thresholds the approximate exp can flip (sigma < 1/255 and
-// T(1-sigma) < 1e-4) are guarded: if a decision lies within the tracked
-// error band the pixel is flagged and blend_exact_kernel recomputes it with
-// fp64 exp() -- so every skip/stop decision equals the reference's.  The
-// mesh-depth stop is an exact fp64 compare.  Culled entries cannot change
-// the result: they have no support in the sub-tile, and the depth stop is
-// monotone along the depth-sorted list.
+// Numerics of the fast path (every decision equals the reference's):
+//  * the conic form m is evaluated in fp64 with FMAs and scaled to the exp2
+//    argument u = m log2(e)/2 in fp64; u is narrowed to fp32 with integer
+//    ops (no F2F).  The support test m > 9 / m < 0 is decided on u with a
+//    2^-20 relative guard band; inside the band (or for a conic flagged
+//    ill-conditioned by preprocess) the entry is re-evaluated exactly in the
+//    reference's operation order with fp64 exp() -- per entry, in place.
+//  * sigma = alpha * 2^-u in fp32 on the SFU: |rel. err| <= EPS_SIG.  Near
+//    the 1/255 skip threshold the same exact re-evaluation decides.
+//  * T, the blend weights and the colour/depth sums are fp32.  An absolute
+//    bound eT on |T - T_reference| is carried along; when an early-stop test
+//    T(1-sigma) < 1e-4 falls within it the pixel is flagged and
+//    blend_exact_kernel replays it in fp64 -- so every stop decision is the
+//    reference's too.  The mesh-depth stop is an exact fp64 compare.
+//  * Culled entries cannot change the result: they have no support in the
+//    sub-tile, and the depth stop is monotone along the depth-sorted list.
 #include "common.cuh"
 
 namespace hgs {
@@ -36,13 +43,11 @@ constexpr int CONSUMERS = 8;
 constexpr int FAST_THREADS = (CONSUMERS + 1) * 32;
 
 struct __align__(16) StageEntry {
-  double2 a;  // mean x, mean y
-  double2 b;  // conic xx, 2*xy
-  double2 c;  // conic yy, alpha
-  double2 d;  // depth, r
-  double2 e;  // g, b
-  float4 box; // fp32 mean x, y, 3-sigma half extents x, y (z < 0: empty slot)
-  float4 con; // fp32 conic xx, xy, yy (ellipse cull)
+  double2 a;  // mean x, mean y               (BlendRec bytes 0..15)
+  double2 b;  // conic xx, 2*xy               (16..31)
+  double2 c;  // conic yy, depth              (32..47)
+  double2 d;  // alpha, r (r unused here)     (48..63)
+  CullRec f;  // fp32 box, conic + depth, alpha + colour
 };
 static_assert(sizeof(StageEntry) == 112, "stage entry is 112 B");
 
@@ -66,14 +71,17 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait suspends the polling lane in hardware (until the phase completes
+// or the hint expires) instead of spinning through issue slots
+constexpr unsigned MBAR_SUSPEND_NS = 20000;
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(MBAR_SUSPEND_NS)
       : "memory");
   return ok != 0;
 }
@@ -126,22 +134,41 @@ __device__ __forceinline__ double mask_value(double t, double k, int variant) {
   }
 }
 
-// exp(-m/2) for m in [0, 9] on the SFU: 2^(m * -0.5 log2 e) with the
-// exponent rounded to fp32 (abs. err <= 2^-21 -> rel. 3.3e-7) and ex2.approx
-// (rel. err <= 2^-22): |rel. err| <= 6e-7 (FAST_EXP_REL_ERR).  (A hi/lo
-// split of the exponent halves the error and the fix-up flags but costs
-// ~10 % of the blend kernel -- measured, not worth it.)
-constexpr float FAST_EXP_REL_ERR = 6e-7f;
-__device__ __forceinline__ double fast_exp_neg_half(double m) {
-  const float t = (float)(m * (-0.5 * LOG2E));
+// ---- fast-path numerics -------------------------------------------------
+// exp2 argument u = m * log2(e)/2 (fp64), narrowed to fp32 round-to-nearest.
+constexpr double U_SCALE = 0.5 * LOG2E;
+constexpr float U9 = (float)(9.0 * 0.5 * LOG2E);
+constexpr float U9_LO = U9 * (1.0f - 9.5367431640625e-7f);  // 2^-20 guard band around m = 9
+constexpr float U9_BAND_INV = 1.0f / (U9 * 9.5367431640625e-7f);
+// |sigma_fast / sigma_reference - 1| <= EPS_SIG: ex2.approx (2^-22) +
+// argument (ln2 * 6.5 * 2^-24) + alpha narrowing and product (2 * 2^-24)
+constexpr float EPS_SIG = 6.5e-7f;
+constexpr float SKIP_F = (float)SIGMA_SKIP;
+constexpr float SKIP_BAND_INV = 1.0f / (2.0f * EPS_SIG * SKIP_F);
+constexpr float CLAMP_F = (float)ALPHA_CLAMP;
+constexpr float STOP_F = (float)EARLY_STOP_T;
+// T - 2 eT above this: the early-stop test is neither taken nor ambiguous
+constexpr float STOP_NEAR = (float)(EARLY_STOP_T * 1.001);
+
+// Distance of an entry's fast-path decisions from their thresholds, in
+// units of the guard bands; <= 1 means "decide exactly".  A negative alpha
+// (ill-conditioned conic, preprocess) forces the exact evaluation.  (The
+// conic form of a well-conditioned conic is never negative, so m < 0 needs
+// no separate test; alpha >= 1/255 > 1 band-unit is never a false flag.)
+__device__ __forceinline__ float amb_key(float uu, float sgf, float a32) {
+  const float k1 = fabsf(fmaf(uu, U9_BAND_INV, -U9 * U9_BAND_INV));
+  const float k2 = fabsf(fmaf(sgf, SKIP_BAND_INV, -SKIP_F * SKIP_BAND_INV));
+  return fminf(fminf(k1, k2), a32 * 1e4f);
+}
+__device__ __forceinline__ float ex2_neg(float u) {
   float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(t));
-  return (double)e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-u));
+  return e;
 }
 
 __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_mesh_layer& mesh, bool mesh_here,
                                             int64_t p, double T, double r, double g, double b, double dacc,
-                                            int64_t last, double bg0, double bg1, double bg2, int mask_variant,
+                                            double acc, int64_t last, double bg0, double bg1, double bg2, int mask_variant,
                                             double mask_k) {
   double oc0, oc1, oc2, od;
   if (mesh_here) {
@@ -153,7 +180,6 @@ __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_
     oc0 = r + T * bg0;
     oc1 = g + T * bg1;
     oc2 = b + T * bg2;
-    const double acc = 1.0 - T;
     od = acc > 1e-12 ? dacc / acc : __longlong_as_double(0x7ff8000000000000LL);
   }
   out.color[3 * p] = (float)oc0;
@@ -166,9 +192,118 @@ __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_
   if (out.mask) out.mask[p] = (float)mask_value(T, mask_k, mask_variant);
 }
 
+// Exact re-evaluation of one entry in the reference's operation order
+// (kernels.py:42-51): support test, fp64 exp, clamp, skip.  Returns sigma
+// (narrowed), or -1 when the entry is not blended.
+__device__ __noinline__ float exact_entry(const StageEntry& E, double fx, double fy) {
+  const double dx = fx - E.a.x, dy = fy - E.a.y;
+  const double m = E.b.x * dx * dx + E.b.y * dx * dy + E.c.x * dy * dy;
+  if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0f;
+  double sg = E.d.x * exp(-0.5 * m);
+  if (sg > ALPHA_CLAMP) sg = ALPHA_CLAMP;
+  return sg < SIGMA_SKIP ? -1.0f : (float)sg;
+}
+
+// Exact walk of one pixel by one warp (fp64 exp()): lanes evaluate 32
+// consecutive entries in parallel -- support test, exp, clamp, skip and
+// the mesh-depth stop exactly as kernels.py:38-51 -- then the chunk's
+// transmittance recurrence T <- T (1 - sigma) is evaluated as a shuffle
+// prefix product.  That rounds differently from the reference's serial
+// product (|rel. diff| < 1e-13 over any walk), so the early-stop decision
+// is trusted only outside a 1e-12 band around 1e-4; a chunk with a value
+// inside it is replayed serially in the reference's order.  Colour/depth
+// sums are per-lane partials reduced once at the end.  Software-pipelined:
+// the next chunk's record gather is in flight during the current one.
+// Result is warp-uniform.
+struct ExactPixel {
+  double T, r, g, b, dacc;
+  int64_t last;
+};
+__device__ __noinline__ ExactPixel exact_walk(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
+                                              int64_t s, int64_t e, double fx, double fy, double limit, int lane) {
+  double T = 1.0, pr = 0.0, pg = 0.0, pb = 0.0, pd = 0.0;
+  int64_t last = -1;
+  bool done = false;
+  BlendRec nxt;
+  if (s + lane < e) nxt = rec[entries[s + lane]];
+  for (int64_t base = s; base < e && !done; base += 32) {
+    const int64_t k = base + lane;
+    const BlendRec c = nxt;
+    if (base + 32 + lane < e) nxt = rec[entries[base + 32 + lane]];
+    bool stop = false, use = false;
+    double sig = 0.0;
+    if (k < e) {
+      stop = c.depth >= limit;
+      const double dx = fx - c.mx, dy = fy - c.my;
+      const double m = c.ca * dx * dx + c.cb2 * dx * dy + c.cc * dy * dy;
+      if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
+        sig = c.alpha * exp(-0.5 * m);
+        if (sig > ALPHA_CLAMP) sig = ALPHA_CLAMP;
+        use = !(sig < SIGMA_SKIP);
+      }
+    }
+    const unsigned stop_mask = __ballot_sync(0xffffffffu, stop);
+    const int first_stop = stop_mask ? __ffs(stop_mask) - 1 : 32;
+    if (lane >= first_stop) use = false;
+    if (first_stop < 32) done = true;
+    // inclusive prefix product of the (1 - sigma) factors
+    double P = use ? 1.0 - sig : 1.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, P, d);
+      if (lane >= d) P *= t;
+    }
+    double Pex = __shfl_up_sync(0xffffffffu, P, 1);
+    if (lane == 0) Pex = 1.0;
+    const double t_after = T * P;
+    const bool near = use && fabs(t_after - EARLY_STOP_T) <= 1e-12 * EARLY_STOP_T;
+    double w = 0.0;
+    if (!__any_sync(0xffffffffu, near)) {
+      const unsigned smask = __ballot_sync(0xffffffffu, use && t_after < EARLY_STOP_T);
+      const int kstop = smask ? __ffs(smask) - 1 : 32;
+      const bool valid = use && lane < kstop;
+      if (valid) w = sig * (T * Pex);
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      if (vmask) {
+        const int lv = 31 - __clz(vmask);
+        T = __shfl_sync(0xffffffffu, t_after, lv);
+        last = base + lv;
+      }
+      if (kstop < 32) done = true;
+    } else {
+      // serial replay of this chunk in the reference's order
+      unsigned use_mask = __ballot_sync(0xffffffffu, use);
+      while (use_mask) {
+        const int i = __ffs(use_mask) - 1;
+        use_mask &= use_mask - 1;
+        const double sg = __shfl_sync(0xffffffffu, sig, i);
+        const double test_t = T * (1.0 - sg);
+        if (test_t < EARLY_STOP_T) { done = true; break; }
+        if (lane == i) w = sg * T;
+        T = test_t;
+        last = base + i;
+      }
+    }
+    if (w != 0.0) {  // (lanes past the list end hold no record)
+      pr += c.r * w;
+      pg += c.g * w;
+      pb += c.b * w;
+      pd += c.depth * w;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    pr += __shfl_xor_sync(0xffffffffu, pr, d);
+    pg += __shfl_xor_sync(0xffffffffu, pg, d);
+    pb += __shfl_xor_sync(0xffffffffu, pb, d);
+    pd += __shfl_xor_sync(0xffffffffu, pd, d);
+  }
+  return ExactPixel{T, pr, pg, pb, pd, last};
+}
+
 template <bool STATS>
 __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
-    const BlendRec* __restrict__ rec, const float4* __restrict__ cull, const uint32_t* __restrict__ entries,
+    const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup) {
   extern __shared__ __align__(128) unsigned char fast_smem_raw[];
@@ -208,15 +343,16 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
         if (k < e) {
           const uint32_t g = __ldg(entries + k);
           const char* src = reinterpret_cast<const char*>(rec + g);
+          const char* cs = reinterpret_cast<const char*>(cull + g);
           cp_async16(&dst->a, src);
           cp_async16(&dst->b, src + 16);
           cp_async16(&dst->c, src + 32);
           cp_async16(&dst->d, src + 48);
-          cp_async16(&dst->e, src + 64);
-          cp_async16(&dst->box, cull + 2 * (size_t)g);
-          cp_async16(&dst->con, cull + 2 * (size_t)g + 1);
+          cp_async16(&dst->f.box, cs);
+          cp_async16(&dst->f.con, cs + 16);
+          cp_async16(&dst->f.col, cs + 32);
         } else {
-          cp_async16(&dst->box, &g_empty_box);
+          cp_async16(&dst->f.box, &g_empty_box);
         }
       }
       cp_async_arrive_noinc(&sm.full[slot]);
@@ -238,9 +374,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
   bool done = !inside;
   bool flagged = false;
   bool warp_done = false;
-  double T = 1.0, dacc = 0.0;
-  float r = 0.0f, g = 0.0f, bl = 0.0f;  // colour sums (fp32: no decision depends on them)
-  float errT = 0.0f;  // bound on the relative error of T from the SFU exp
+  float T = 1.0f;     // transmittance
+  float eT = 0.0f;    // bound on |T - T_reference| (valid while not done)
+  float acc = 0.0f;   // sum of blend weights (= 1 - T_reference up to rounding)
+  float r = 0.0f, g = 0.0f, bl = 0.0f, dacc = 0.0f;
   int last = -1;      // entry index relative to s
   unsigned walked = 0, blended = 0;
 
@@ -253,72 +390,126 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
       int nl = 0;
 #pragma unroll
       for (int k = 0; k < BATCH; k += 32) {
-        const float4 q = sm.ent[slot][k + lane].box;
+        const float4 q = sm.ent[slot][k + lane].f.box;
         const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
         bool hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
-        if (hit && (q.x != cx || q.y != cy)) hit = ellipse_meets_box(sm.ent[slot][k + lane].con, q.x, q.y, wx0, wx1,
-                                                                  wy0, wy1);
+        if (hit && (q.x != cx || q.y != cy))
+          hit = ellipse_meets_box(sm.ent[slot][k + lane].f.con, q.x, q.y, wx0, wx1, wy0, wy1);
         const unsigned m = __ballot_sync(0xffffffffu, hit);
         if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)(k + lane);
         nl += __popc(m);
       }
       __syncwarp();
       if (__any_sync(0xffffffffu, !done)) {  // warp-uniform: the loop below votes
-        const int bbase = b * BATCH;
-        // Two entries per step: the independent part (support test, exp) of
-        // both is evaluated together for ILP, then the reference's
-        // sequential T/colour recurrence consumes them in order.  Uniform
-        // trip count + a vote per step keeps the warp converged.
+        // Two entries per step: the independent part (conic form, exp2,
+        // decisions) of both is evaluated together for ILP, then the
+        // reference's sequential T/colour recurrence consumes them in order
+        // with selects.  Uniform trip count + a vote per step keeps the warp
+        // converged.
         for (int li = 0; li < nl; li += 2) {
           const bool has1 = li + 1 < nl;
-          const int j0 = sm.list[warp][li];
-          const int j1 = has1 ? sm.list[warp][li + 1] : j0;
-          const StageEntry& E0 = sm.ent[slot][j0];
-          const StageEntry& E1 = sm.ent[slot][j1];
-          const double2 D0 = E0.d, D1 = E1.d;  // depth, r
-          const double2 A0 = E0.a, A1 = E1.a, B0 = E0.b, B1 = E1.b, C0 = E0.c, C1 = E1.c;
-          const double dx0 = fx - A0.x, dy0 = fy - A0.y, dx1 = fx - A1.x, dy1 = fy - A1.y;
-          // exact fp64 support test in the reference's operation order
-          const double m0 = B0.x * dx0 * dx0 + B0.y * dx0 * dy0 + C0.x * dy0 * dy0;
-          const double m1 = B1.x * dx1 * dx1 + B1.y * dx1 * dy1 + C1.x * dy1 * dy1;
-          const bool in0 = !(m0 > SUPPORT_MAHAL2 || m0 < 0.0);
-          const bool in1 = has1 && !(m1 > SUPPORT_MAHAL2 || m1 < 0.0);
-          double sig0 = C0.y * fast_exp_neg_half(in0 ? m0 : 0.0);
-          double sig1 = C1.y * fast_exp_neg_half(in1 ? m1 : 0.0);
-          // the 1/255 skip is a per-entry decision: near it, recompute exp in
-          // fp64 right here (exact decision, no pixel flag needed)
-          if (fabs(sig0 - SIGMA_SKIP) <= 2.0 * (double)FAST_EXP_REL_ERR * SIGMA_SKIP) sig0 = C0.y * exp(-0.5 * m0);
-          if (fabs(sig1 - SIGMA_SKIP) <= 2.0 * (double)FAST_EXP_REL_ERR * SIGMA_SKIP) sig1 = C1.y * exp(-0.5 * m1);
-          if (sig0 > ALPHA_CLAMP) sig0 = ALPHA_CLAMP;
-          if (sig1 > ALPHA_CLAMP) sig1 = ALPHA_CLAMP;
+          int jj[2];
+          jj[0] = sm.list[warp][li];
+          jj[1] = has1 ? sm.list[warp][li + 1] : jj[0];
+          float sg[2];
+          bool ok[2], dstop[2];
+          float key = 2.0f;
 #pragma unroll
           for (int u = 0; u < 2; u++) {
-            const bool in = u == 0 ? in0 : in1;
-            const double sig = u == 0 ? sig0 : sig1;
-            const double2 D = u == 0 ? D0 : D1;
-            const StageEntry& E = u == 0 ? E0 : E1;
-            const int j = u == 0 ? j0 : j1;
-            if (done || (u == 1 && !has1)) continue;
-            if (STATS) walked++;
-            if (D.x >= limit) { done = true; continue; }  // list is depth sorted; mesh is opaque
-            if (!in) continue;
-            const float sgf = (float)sig;
-            if (sig < SIGMA_SKIP) continue;
-            const double test_t = T * (1.0 - sig);
-            errT += 1.1f * FAST_EXP_REL_ERR * sgf * rcp_approx(1.0f - sgf);
-            // guard: the early-stop decision is ambiguous within the tracked T error band
-            if (fabsf((float)test_t - (float)EARLY_STOP_T) <= (errT + 1e-6f) * (float)EARLY_STOP_T) flagged = true;
-            if (test_t < EARLY_STOP_T) { done = true; continue; }
-            const double w = sig * T;
-            const float wf = (float)w;
-            const double2 Ec = E.e;
-            r = fmaf((float)D.y, wf, r);
-            g = fmaf((float)Ec.x, wf, g);
-            bl = fmaf((float)Ec.y, wf, bl);
-            dacc = fma(D.x, w, dacc);
-            T = test_t;
-            last = b * BATCH + j;
-            if (STATS) blended++;
+            const StageEntry& E = sm.ent[slot][jj[u]];
+            const double2 A = E.a, B = E.b, C = E.c;  // C: conic yy, depth
+            const float a32 = E.f.col.x;
+            const double dx = fx - A.x, dy = fy - A.y;
+            const double m = fma(dx, fma(B.y, dy, B.x * dx), (C.x * dy) * dy);
+            const float uu = __double2float_rn(m * U_SCALE);
+            const float sgf = fminf(fabsf(a32) * ex2_neg(uu), CLAMP_F);
+            dstop[u] = C.y >= limit;
+            ok[u] = uu < U9_LO && sgf >= SKIP_F;
+            sg[u] = sgf;
+            key = fminf(key, amb_key(uu, sgf, a32));
+          }
+          // Fast commit: valid when no lane of the warp meets a decision this
+          // step can get wrong -- a depth stop, an early-stop region, an
+          // ambiguous entry.  Then both entries are blended branch-free
+          // (a skipped entry has sigma 0: T, eT-growth aside, and the sums
+          // are unchanged exactly).
+          const float s0 = (ok[0] && !done) ? sg[0] : 0.0f;
+          const float s1 = (ok[1] && !done && has1) ? sg[1] : 0.0f;
+          const float om0 = 1.0f - s0, om1 = 1.0f - s1;
+          const float T1 = T * om0;
+          const float T2 = T1 * om1;
+          const float w0 = T * s0, w1 = T1 * s1;
+          const float e1 = fmaf(w0, EPS_SIG, fmaf(eT, om0, T1 * 1.1920929e-7f));
+          const float e2 = fmaf(w1, EPS_SIG, fmaf(e1, om1, T2 * 1.1920929e-7f));
+          // T2 - 2 e2 >= STOP_NEAR implies neither entry's stop test is
+          // ambiguous or taken (T1 - 2 e1 >= (T2 - 2 e2) / (1 - s1))
+          const bool special =
+              !done && (dstop[0] || (has1 && dstop[1]) || key <= 1.0f || fmaf(-2.0f, e2, T2) < STOP_NEAR);
+          if (!__any_sync(0xffffffffu, special)) {
+            eT = e2;
+            const float4 c0 = sm.ent[slot][jj[0]].f.col, c1 = sm.ent[slot][jj[1]].f.col;
+            const float d0 = sm.ent[slot][jj[0]].f.con.w, d1 = sm.ent[slot][jj[1]].f.con.w;
+            r = fmaf(c1.y, w1, fmaf(c0.y, w0, r));
+            g = fmaf(c1.z, w1, fmaf(c0.z, w0, g));
+            bl = fmaf(c1.w, w1, fmaf(c0.w, w0, bl));
+            dacc = fmaf(d1, w1, fmaf(d0, w0, dacc));
+            acc = (acc + w0) + w1;
+            T = T2;
+            const int bb = b * BATCH;
+            last = s1 > 0.0f ? bb + jj[1] : (s0 > 0.0f ? bb + jj[0] : last);
+            if (STATS && !done) {
+              walked += has1 ? 2 : 1;
+              blended += (s0 > 0.0f) + (s1 > 0.0f);
+            }
+            continue;
+          }
+          if (__any_sync(0xffffffffu, key <= 1.0f)) {  // rare: exact per-entry re-evaluation
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+              const StageEntry& E = sm.ent[slot][jj[u]];
+              const double dx = fx - E.a.x, dy = fy - E.a.y;
+              const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
+              if (amb_key(__double2float_rn(m * U_SCALE), sg[u], E.f.col.x) <= 1.0f) {
+                const float x = exact_entry(E, fx, fy);
+                ok[u] = x >= 0.0f;
+                sg[u] = x;
+              }
+            }
+          }
+          // general path: the reference's sequential decisions, entry by entry
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            const bool act = !done && (u == 0 || has1);
+            if (STATS && act) walked++;
+            if (act && dstop[u]) done = true;  // list is depth sorted; mesh is opaque
+            const bool v = act && !dstop[u] && ok[u];
+            const float sig = v ? sg[u] : 0.0f;
+            const float om = 1.0f - sig;
+            const float test = T * om;
+            const float w = T * sig;
+            // |test - T_ref (1 - sigma_ref)| <= eT om + w EPS_SIG + test 2^-23
+            // (skipped entries only add the rounding term: conservative)
+            eT = fmaf(w, EPS_SIG, fmaf(eT, om, test * 1.1920929e-7f));
+            bool stop = false;
+            if (v && fmaf(-2.0f, eT, test) < STOP_NEAR) {  // the early-stop region
+              // the decision is ambiguous within the error band -> exact replay
+              if (fabsf(test - STOP_F) <= fmaf(eT, 1.001f, 3e-12f)) flagged = true;
+              stop = test < STOP_F;
+              if (stop) done = true;
+            }
+            const bool upd = v && !stop;
+            const StageEntry& E = sm.ent[slot][jj[u]];
+            const float wu = upd ? w : 0.0f;
+            r = fmaf(E.f.col.y, wu, r);
+            g = fmaf(E.f.col.z, wu, g);
+            bl = fmaf(E.f.col.w, wu, bl);
+            dacc = fmaf(E.f.con.w, wu, dacc);
+            acc += wu;
+            T = upd ? test : T;
+            if (upd) {
+              last = b * BATCH + jj[u];
+              if (STATS) blended++;
+            }
           }
           if (__all_sync(0xffffffffu, done)) break;
         }
@@ -347,80 +538,31 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
     fixup[1 + slot] = (int32_t)p;
     return;
   }
-  write_pixel(out, mesh, mesh_here, p, T, r, g, bl, dacc, last >= 0 ? s + last : -1, bg0, bg1, bg2, mask_variant,
-              mask_k);
+  write_pixel(out, mesh, mesh_here, p, T, r, g, bl, dacc, acc, last >= 0 ? s + last : -1, bg0, bg1, bg2,
+              mask_variant, mask_k);
 }
 
-// Exact reference walk (fp64 exp()).  With fixup != NULL: one warp per
-// flagged pixel (persistent grid-stride over the work list) -- lanes evaluate
-// 32 consecutive entries in parallel, then every lane replays the reference's
-// sequential T/colour recurrence over them in order (shuffles), so the
-// arithmetic order equals kernels.py:38-61 exactly.  With fixup == NULL: the
-// same, over every pixel.
+// The exact walk, one warp per pixel (persistent grid-stride): over the
+// fast kernel's work list of flagged pixels (fixup: count, pixel ids), or
+// over every pixel (fixup == NULL: projections without fp32 cull records).
 __global__ void __launch_bounds__(256) blend_exact_kernel(
     const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
     int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
     double mask_k, hgs_blend_out out, const int32_t* __restrict__ fixup) {
-  const int64_t npix = (int64_t)width * height;
-  const int64_t count = fixup ? fixup[0] : npix;
+  const int64_t count = fixup ? fixup[0] : (int64_t)width * height;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wi < count; wi += nwarps) {
     const int64_t p = fixup ? fixup[1 + wi] : wi;
     const int px = (int)(p % width), py = (int)(p / width);
     const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
-    const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
-    const double fx = px + 0.5, fy = py + 0.5;
     const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
     const double limit = mesh_here ? mesh.depth[p] : __longlong_as_double(0x7ff0000000000000LL);
-    double T = 1.0, r = 0.0, g = 0.0, b = 0.0, dacc = 0.0;
-    int64_t last = -1;
-    bool done = false;
-    // software-pipelined: the next chunk's record gather is in flight while
-    // the current chunk is evaluated and consumed
-    BlendRec nxt;
-    if (s + lane < e) nxt = rec[entries[s + lane]];
-    for (int64_t base = s; base < e && !done; base += 32) {
-      const int64_t k = base + lane;
-      const BlendRec q = nxt;
-      if (base + 32 + lane < e) nxt = rec[entries[base + 32 + lane]];
-      bool stop = false, use = false;
-      double sig = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, dep = 0.0;
-      if (k < e) {
-        dep = q.depth;
-        stop = q.depth >= limit;
-        const double dx = fx - q.mx, dy = fy - q.my;
-        const double m = q.ca * dx * dx + q.cb2 * dx * dy + q.cc * dy * dy;
-        if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
-          sig = q.alpha * exp(-0.5 * m);
-          if (sig > ALPHA_CLAMP) sig = ALPHA_CLAMP;
-          use = !(sig < SIGMA_SKIP);
-        }
-        cr = q.r; cg = q.g; cb = q.b;
-      }
-      const unsigned stop_mask = __ballot_sync(0xffffffffu, stop);
-      unsigned use_mask = __ballot_sync(0xffffffffu, use);
-      const int first_stop = stop_mask ? __ffs(stop_mask) - 1 : 32;
-      if (first_stop < 32) {
-        use_mask &= (1u << first_stop) - 1u;
-        done = true;
-      }
-      while (use_mask) {
-        const int i = __ffs(use_mask) - 1;
-        use_mask &= use_mask - 1;
-        const double sg = __shfl_sync(0xffffffffu, sig, i);
-        const double test_t = T * (1.0 - sg);
-        if (test_t < EARLY_STOP_T) { done = true; break; }
-        const double w = sg * T;
-        r += __shfl_sync(0xffffffffu, cr, i) * w;
-        g += __shfl_sync(0xffffffffu, cg, i) * w;
-        b += __shfl_sync(0xffffffffu, cb, i) * w;
-        dacc += __shfl_sync(0xffffffffu, dep, i) * w;
-        T = test_t;
-        last = base + i;
-      }
-    }
-    if (lane == 0) write_pixel(out, mesh, mesh_here, p, T, r, g, b, dacc, last, bg0, bg1, bg2, mask_variant, mask_k);
+    const ExactPixel q = exact_walk(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5,
+                                    limit, lane);
+    if (lane == 0)
+      write_pixel(out, mesh, mesh_here, p, q.T, q.r, q.g, q.b, q.dacc, 1.0 - q.T, q.last, bg0, bg1, bg2,
+                  mask_variant, mask_k);
   }
 }
 
@@ -458,11 +600,11 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     }
     if (out->stats)
       blend_fast_kernel<true><<<n_tiles, FAST_THREADS, smem, st>>>(
-          (const BlendRec*)proj->rec, (const float4*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
+          (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
           width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
     else
       blend_fast_kernel<false><<<n_tiles, FAST_THREADS, smem, st>>>(
-          (const BlendRec*)proj->rec, (const float4*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
+          (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
           width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
     HGS_CHECK_LAUNCH();
     // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)

@@ -30,11 +30,20 @@ constexpr int TILE_DIFF_COPIES = HGS_TILE_DIFF_COPIES;
 struct __align__(16) BlendRec {
   double mx, my;      // mean2d
   double ca, cb2, cc;  // conic xx, 2 * conic xy (exact scaling), conic yy
-  double alpha;       // sigmoid(logit)
   double depth;       // camera z
+  double alpha;       // sigmoid(logit)
   double r, g, b;     // view-evaluated colour, clamped at 0
 };
 static_assert(sizeof(BlendRec) == 80, "BlendRec must be 80 bytes");
+
+// fp32 companion record (hgs_projected.cull, 48 B): culling box + conic for
+// the per-warp sub-tile test, and the fp32 operands of the blend fast path.
+struct __align__(16) CullRec {
+  float4 box;  // mean x, mean y, 3-sigma half extents x, y (z < 0: culled row)
+  float4 con;  // conic xx, xy, yy, depth
+  float4 col;  // alpha (< 0: ill-conditioned conic -> exact evaluation), r, g, b
+};
+static_assert(sizeof(CullRec) == 16 * 3 && HGS_CULL_FLOATS == 12, "CullRec is 48 B");
 
 // numpy matmul inner-product order on x86-64 OpenBLAS (measured):
 // s = a0*b0; s = fma(a1,b1,s); s = fma(a2,b2,s)

@@ -150,9 +150,17 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
     const float slack = 1e-3f + 2.5e-7f * (float)(fabs(mx) + fabs(my));
     const float ex = (float)(3.0 * sqrt(cxx)) * (1.0f + 1e-5f) + slack;
     const float ey = (float)(3.0 * sqrt(cyy)) * (1.0f + 1e-5f) + slack;
-    float4* cr = reinterpret_cast<float4*>(out.cull) + 2 * i;
-    cr[0] = make_float4((float)mx, (float)my, ok ? ex : -1.0f, ok ? ey : -1.0f);
-    cr[1] = make_float4((float)(cyy * inv_det), (float)(-cxy * inv_det), (float)(cxx * inv_det), 0.0f);
+    // the blend fast path evaluates the conic form with FMAs; its distance
+    // from the reference's rounding is bounded by the conditioning
+    // 1 / (1 - rho^2) of the conic -- past 1e6 the entry is always
+    // evaluated in the reference's operation order (sign of alpha)
+    const double one_m_rho2 = det / (cxx * cyy);
+    const float a32 = (float)alpha;
+    CullRec cr;
+    cr.box = make_float4((float)mx, (float)my, ok ? ex : -1.0f, ok ? ey : -1.0f);
+    cr.con = make_float4((float)(cyy * inv_det), (float)(-cxy * inv_det), (float)(cxx * inv_det), (float)depth);
+    cr.col = make_float4(one_m_rho2 > 1e-6 ? a32 : -a32, (float)rec.r, (float)rec.g, (float)rec.b);
+    reinterpret_cast<CullRec*>(out.cull)[i] = cr;
   }
   if (out.cov2d) { out.cov2d[3 * i] = cxx; out.cov2d[3 * i + 1] = cxy; out.cov2d[3 * i + 2] = cyy; }
   if (out.radius) out.radius[i] = radius;

@@ -48,7 +48,7 @@ class HybridRenderer:
         self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
         self.count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
-        self.cull = torch.empty(n * 8, dtype=torch.float32, device=dev)
+        self.cull = torch.empty(n * 12, dtype=torch.float32, device=dev)
         self.sort_keys = torch.empty(n, dtype=torch.int64, device=dev)
         self.tile_diff = torch.empty(16 * (self.tiles_x + 1) * (self.tiles_y + 1), dtype=torch.int32, device=dev)
         self.fixup = torch.zeros(h * w + 1, dtype=torch.int32, device=dev)

@@ -111,7 +111,7 @@ class ProjectedGaussians:
             conic = rec[:, 2:5].clone()
             conic[:, 1] *= 0.5  # the record stores 2 * conic_xy (exact)
             f = {"kept": kept, "mean2d": rec[:, 0:2].contiguous(), "conic": conic,
-                 "alpha": rec[:, 5].contiguous(), "depth": rec[:, 6].contiguous(), "color": rec[:, 7:10].contiguous()}
+                 "alpha": rec[:, 6].contiguous(), "depth": rec[:, 5].contiguous(), "color": rec[:, 7:10].contiguous()}
             ex = self._extras or {}
             for k in ("cov2d", "radius", "t_cam", "color_pre", "view_dir", "view_dist"):
                 f[k] = ex[k][kept] if ex.get(k) is not None else None
@@ -256,7 +256,7 @@ def _preprocess(gs: GaussianSet, cam, cam_dev, tile_px: int, extras: bool) -> Pr
     rec = torch.empty(max(n, 1) * REC_BYTES, dtype=torch.uint8, device=dev)
     count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
     rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
-    cull = torch.empty(max(n, 1) * 8, dtype=torch.float32, device=dev)
+    cull = torch.empty(max(n, 1) * 12, dtype=torch.float32, device=dev)
     sort_keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     tx = (int(cam.width) + tile_px - 1) // tile_px
     ty = (int(cam.height) + tile_px - 1) // tile_px

@@ -84,7 +84,7 @@ class HybridTrainer:
         self.rec = torch.empty(max(n, 1) * REC_BYTES, dtype=torch.uint8, device=dev)
         self.count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
         self.rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
-        self.cull = torch.empty(max(n, 1) * 8, dtype=torch.float32, device=dev)
+        self.cull = torch.empty(max(n, 1) * 12, dtype=torch.float32, device=dev)
         self.sort_keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         self.screen = torch.zeros(max(n, 1) * 9, dtype=torch.float64, device=dev)
         c0 = self.cameras[0]

@@ -15,7 +15,7 @@ out = sp._blend(proj, tiles, c.width, c.height, layer, np.zeros(3))
 torch.cuda.synchronize()
 fx = sp.SCRATCH.bufs[("fixup", g.device)].view(torch.int32)
 ntiles = tiles.tiles_x * tiles.tiles_y
-print("flagged (tile counts)", int(fx[:ntiles].sum()))
+
 nflag = int(fx[0])
 print("flagged", nflag, "of", c.width * c.height)
 if nflag:
