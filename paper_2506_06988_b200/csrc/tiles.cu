@@ -9,11 +9,16 @@
 //      follow from the counts                                    (1 CTA)
 //   3. sort the visible rows by the fp64 depth bit pattern, stably
 //      (8 LSD passes) -> rows in (depth, row) order
-//   4. exclusive scan of their tile counts in that order (chained scan)
-//   5. emit (tile id, row) pairs in depth order (warp-cooperative,
-//      coalesced: one warp spreads 32 rows' rectangles over its lanes)
-//   6. stable LSD sort by tile id (1-2 passes of 8 bits)
-//      -> (tile, depth, row) order == the reference's lexsort, exactly.
+//   4. bin_kernel (tile grids up to BIN_MAX_TILES): partitions of the
+//      depth-ordered rows; per partition and warp, per-tile entry counts of
+//      the rows' rectangles (shared memory); a decoupled look-back per tile
+//      across partitions gives each partition's offset inside every tile's
+//      list; then every entry is ranked in (depth, row) order inside its
+//      tile (warp match on the tile id) and written straight to its final
+//      slot -> (tile, depth, row) order == the reference's lexsort, exactly,
+//      with no entry-level sort at all.
+//   Larger tile grids: exclusive scan of the rows' tile counts in depth
+//      order, emission of (tile id, row) pairs, stable LSD sort by tile id.
 // Positive doubles order like their IEEE bit patterns, so step 2 is exact.
 #include "sort.cuh"
 
@@ -339,6 +344,349 @@ __global__ void __launch_bounds__(256) emit_big_kernel(const uint32_t* __restric
   }
 }
 
+// ------------------------------------------------------------ rect binning
+// Two levels, no entry-level sort:
+//  coarse: the depth-ordered rows are scattered, stably, into the lists of
+//    the super-tiles (2^ss x 2^ss tiles, at most 256 of them) their
+//    rectangles touch.  coarse_hist_kernel counts the (row, super-tile)
+//    pairs per super-tile; coarse_bin_kernel takes partitions of BIN_PG rows
+//    (8 warps x BIN_SUB) in dynamic order, counts each warp's pairs per
+//    super-tile, gets every super-tile's offset from the earlier partitions
+//    with a decoupled look-back (one super-tile per thread, as in a radix
+//    pass), ranks the pairs in row order (warp match on the super-tile id
+//    over the flattened pairs, per-warp counters) and writes (row, tile
+//    rectangle) to the slot;
+//  fine: fine_bin_kernel, one CTA per super-tile, each warp owning some of
+//    its tiles, streams the super-tile's ordered list (coalesced, double
+//    buffered) and keeps the rows whose rectangle contains the tile (ballot
+//    compaction preserves order), writing them from tile_starts[t] on.
+// A row's entries in a tile list are therefore in (depth, row) order, the
+// reference's lexsort((kept, depth, tile)).
+constexpr int BIN_THREADS = 256;
+constexpr int BIN_WARPS = BIN_THREADS / 32;
+constexpr int BIN_PG = 1024;                 // depth-ordered rows per partition
+constexpr int BIN_SUB = BIN_PG / BIN_WARPS;  // rows per warp
+constexpr int BIN_MAX_SUPER = 256;           // super-tiles: one look-back digit per thread
+constexpr int FINE_WARPS = 16;
+constexpr int FINE_DEPTH = 8;  // rounds of 32 list entries in flight per warp
+
+// smallest super-tile shift with at most BIN_MAX_SUPER super-tiles (or -1)
+__host__ __device__ inline int super_shift(int tiles_x, int tiles_y) {
+  for (int ss = 2; ss <= 3; ss++) {
+    const int sx = (tiles_x + (1 << ss) - 1) >> ss, sy = (tiles_y + (1 << ss) - 1) >> ss;
+    if (sx * sy <= BIN_MAX_SUPER) return ss;
+  }
+  return -1;
+}
+
+// tile id of the l-th tile (row-major) of a rectangle of width rw in a grid
+// of width gx
+__device__ __forceinline__ uint32_t rect_tile(uint32_t l, ushort4 rc, uint32_t rw, int gx) {
+  uint32_t q = (uint32_t)((float)l * __frcp_rn((float)rw));  // exact after one correction (l < 2^24)
+  int32_t rr = (int32_t)(l - q * rw);
+  if (rr < 0) { q--; rr += rw; } else if (rr >= (int32_t)rw) { q++; rr -= rw; }
+  return (rc.z + q) * (uint32_t)gx + rc.x + (uint32_t)rr;
+}
+
+__device__ __forceinline__ ushort4 coarse_rect(ushort4 rc, int ss) {
+  return make_ushort4(rc.x >> ss, rc.y >> ss, rc.z >> ss, rc.w >> ss);
+}
+
+// Owner rows of one round of 32 consecutive flattened pairs o0 + lane: ra
+// is the owner of o0 (warp-uniform, updated to the owner of o0 + 32).  Every
+// row has at least one pair, so at most 32 rows start inside the round; lane
+// i looks at the start of row ra + 1 + i and the row starts become a bit
+// mask of the round.
+__device__ __forceinline__ int round_owner(const uint32_t* off, uint32_t o0, int& ra, int lane) {
+  const int r = ra + 1 + lane;
+  const uint32_t st = r <= BIN_SUB ? off[r] : 0xffffffffu;
+  const uint32_t rel = st - o0;  // >= 1 for the rows after ra
+  const unsigned bits = __reduce_or_sync(0xffffffffu, rel < 32 ? (1u << rel) : 0u);
+  const int own = ra + __popc(bits & ((2u << lane) - 1u));
+  ra += __popc(bits) + (__any_sync(0xffffffffu, rel == 32) ? 1 : 0);
+  return own;
+}
+
+struct CoarseSmem {
+  uint32_t cnt[BIN_WARPS][BIN_MAX_SUPER];  // per-warp counters, then per-warp slots
+  uint32_t off[BIN_WARPS][BIN_SUB + 1];    // per-warp exclusive pair offsets of the rows
+  uint32_t row[BIN_PG];
+  ushort4 rect[BIN_PG];
+  ushort4 crect[BIN_PG];
+};
+
+// Stage partition `part` (rows, coarse rectangles, per-warp pair offsets)
+// and count every warp's (row, super-tile) pairs per super-tile.  Returns
+// the warp's pair total.
+__device__ __forceinline__ uint32_t coarse_stage_count(CoarseSmem& sm, const uint32_t* __restrict__ sorted_rows,
+                                                       const ushort4* __restrict__ rect, int64_t base, int64_t m,
+                                                       int ss, int sx) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < BIN_WARPS * BIN_MAX_SUPER; i += BIN_THREADS) (&sm.cnt[0][0])[i] = 0;
+  constexpr int PER = BIN_SUB / 32;
+  const int w0 = warp * BIN_SUB;
+  uint32_t c[PER], lsum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    const int li = w0 + lane * PER + q;
+    const int64_t j = base + li;
+    c[q] = 0;
+    if (j < m) {
+      const uint32_t g = sorted_rows[j];
+      const ushort4 rc = rect[g];
+      const ushort4 cr = coarse_rect(rc, ss);
+      sm.row[li] = g;
+      sm.rect[li] = rc;
+      sm.crect[li] = cr;
+      c[q] = (uint32_t)(cr.y - cr.x + 1) * (uint32_t)(cr.w - cr.z + 1);
+    }
+    lsum += c[q];
+  }
+  uint32_t x = lsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  uint32_t run = x - lsum;
+#pragma unroll
+  for (int q = 0; q < PER; q++) {
+    sm.off[warp][lane * PER + q] = run;
+    run += c[q];
+  }
+  if (lane == 31) sm.off[warp][BIN_SUB] = x;
+  __syncthreads();
+  const uint32_t total = sm.off[warp][BIN_SUB];
+  int ra = 0;
+  for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+    const uint32_t o = o0 + lane;
+    const int r = round_owner(sm.off[warp], o0, ra, lane);
+    if (o < total) {
+      const ushort4 cr = sm.crect[w0 + r];
+      atomicAdd(&sm.cnt[warp][rect_tile(o - sm.off[warp][r], cr, (uint32_t)(cr.y - cr.x + 1), sx)], 1u);
+    }
+  }
+  __syncthreads();
+  return total;
+}
+
+// per-partition super-tile counts -> mat[part][BIN_MAX_SUPER], and their
+// totals -> hist (zeroed)
+__global__ void __launch_bounds__(BIN_THREADS) coarse_count_kernel(const uint32_t* __restrict__ sorted_rows,
+                                                                   const ushort4* __restrict__ rect,
+                                                                   const int64_t* counters, int64_t capacity, int ss,
+                                                                   int sx, int ns, uint32_t* __restrict__ mat,
+                                                                   uint32_t* __restrict__ hist) {
+  __shared__ CoarseSmem sm;
+  const int64_t m = counters[0];
+  if (counters[1] > capacity) return;  // overflow: flagged in counters[2]
+  const int64_t base = (int64_t)blockIdx.x * BIN_PG;
+  if (base >= m) return;
+  coarse_stage_count(sm, sorted_rows, rect, base, m, ss, sx);
+  if (threadIdx.x < ns) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int w = 0; w < BIN_WARPS; w++) acc += sm.cnt[w][threadIdx.x];
+    mat[(size_t)blockIdx.x * BIN_MAX_SUPER + threadIdx.x] = acc;
+    if (acc) atomicAdd(&hist[threadIdx.x], acc);
+  }
+}
+
+// List starts (exclusive scan of the histogram) and the slot of every
+// (partition, super-tile): one CTA per 32 super-tiles, 32 warps splitting
+// the partitions (lane = super-tile).
+__global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __restrict__ mat,
+                                                           const uint32_t* __restrict__ hist, const int64_t* counters,
+                                                           int64_t capacity, int ns, uint32_t* __restrict__ cstart,
+                                                           uint32_t* __restrict__ slot) {
+  __shared__ uint32_t s_sum[32][33];
+  __shared__ uint32_t s_start[32];
+  __shared__ uint32_t s_tmp[8];
+  const int64_t m = counters[0];
+  if (counters[1] > capacity) return;
+  const int nparts = (int)((m + BIN_PG - 1) / BIN_PG);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  if (warp == 0) {
+    // start of this CTA's first super-tile: sum of the histogram before it
+    uint32_t pre = 0;
+    for (int t = lane; t < blockIdx.x * 32; t += 32) pre += hist[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    uint32_t h = c < ns ? hist[c] : 0u, x = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_start[lane] = pre + x - h;
+    if (c < ns) cstart[c] = pre + x - h;
+    if (c == ns - 1) cstart[ns] = pre + x;
+  }
+  (void)s_tmp;
+  const int per = (nparts + 31) / 32;
+  const int p0 = warp * per, p1 = min(nparts, p0 + per);
+  uint32_t sum = 0;
+  if (c < ns)
+    for (int p = p0; p < p1; p++) sum += mat[(size_t)p * BIN_MAX_SUPER + c];
+  s_sum[warp][lane] = sum;
+  __syncthreads();
+  if (c >= ns) return;
+  uint32_t run = s_start[lane];
+  for (int w = 0; w < warp; w++) run += s_sum[w][lane];
+  for (int p = p0; p < p1; p++) {
+    slot[(size_t)p * BIN_MAX_SUPER + c] = run;
+    run += mat[(size_t)p * BIN_MAX_SUPER + c];
+  }
+}
+
+// in-order ranking of every warp's (row, super-tile) pairs and the scatter
+// of (row, tile rectangle) into the coarse lists
+__global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(
+    const uint32_t* __restrict__ sorted_rows, const ushort4* __restrict__ rect, const int64_t* counters,
+    int64_t capacity, int ss, int sx, int ns, const uint32_t* __restrict__ slot, uint32_t* __restrict__ crow,
+    ushort4* __restrict__ crect_out) {
+  __shared__ CoarseSmem sm;
+  const int64_t m = counters[0];
+  if (counters[1] > capacity) return;
+  const int64_t base = (int64_t)blockIdx.x * BIN_PG;
+  if (base >= m) return;
+  const uint32_t total = coarse_stage_count(sm, sorted_rows, rect, base, m, ss, sx);
+  if (threadIdx.x < ns) {  // counters -> slot of every warp
+    uint32_t acc = slot[(size_t)blockIdx.x * BIN_MAX_SUPER + threadIdx.x];
+#pragma unroll
+    for (int w = 0; w < BIN_WARPS; w++) {
+      const uint32_t v = sm.cnt[w][threadIdx.x];
+      sm.cnt[w][threadIdx.x] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w0 = warp * BIN_SUB;
+  int ra = 0;
+  for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+    const uint32_t o = o0 + lane;
+    const bool valid = o < total;
+    uint32_t sti = 0xffffffffu;
+    const int r = round_owner(sm.off[warp], o0, ra, lane);
+    if (valid) {
+      const ushort4 cr = sm.crect[w0 + r];
+      sti = rect_tile(o - sm.off[warp][r], cr, (uint32_t)(cr.y - cr.x + 1), sx);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, sti);
+    uint32_t cur = 0;
+    if (valid) cur = sm.cnt[warp][sti];
+    __syncwarp();
+    if (valid) {
+      const uint32_t pos = cur + __popc(peers & lanemask_lt());
+      crow[pos] = sm.row[w0 + r];
+      crect_out[pos] = sm.rect[w0 + r];
+      if (lane == __ffs(peers) - 1) sm.cnt[warp][sti] = cur + __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// Fine level: one CTA per super-tile (S x S tiles, S = 4 or 8).  Every list
+// entry becomes the bit mask of the super-tile's tiles its rectangle covers;
+// the 16 warps take contiguous parts of the ordered list, count per tile
+// (pass 1: byte-packed warp reductions), take their per-tile start from the
+// warp prefix, then write (pass 2: one ballot per tile keeps the list order).
+template <int S>
+struct FineMask;
+template <>
+struct FineMask<4> {
+  using T = uint32_t;
+  __device__ static T of(ushort4 rc, int sx0, int sy0) {
+    const int lx0 = max((int)rc.x - sx0, 0), lx1 = min((int)rc.y - sx0, 3);
+    const int ly0 = max((int)rc.z - sy0, 0), ly1 = min((int)rc.w - sy0, 3);
+    if (lx0 > lx1 || ly0 > ly1) return 0u;
+    const uint32_t rowbits = (2u << lx1) - (1u << lx0);
+    const uint32_t ymask = (ly1 == 3 ? 0x10000u : (1u << (4 * (ly1 + 1)))) - (1u << (4 * ly0));
+    return (rowbits * 0x1111u) & ymask;
+  }
+  __device__ static bool bit(T m, int q) { return (m >> q) & 1u; }
+  __device__ static uint32_t nibble(T m, int j) { return (m >> (4 * j)) & 0xFu; }
+};
+template <>
+struct FineMask<8> {
+  using T = unsigned long long;
+  __device__ static T of(ushort4 rc, int sx0, int sy0) {
+    const int lx0 = max((int)rc.x - sx0, 0), lx1 = min((int)rc.y - sx0, 7);
+    const int ly0 = max((int)rc.z - sy0, 0), ly1 = min((int)rc.w - sy0, 7);
+    if (lx0 > lx1 || ly0 > ly1) return 0ull;
+    const unsigned long long rowbits = (2ull << lx1) - (1ull << lx0);
+    const unsigned long long ymask = (ly1 == 7 ? 0ull : (1ull << (8 * (ly1 + 1)))) - (1ull << (8 * ly0));
+    return (rowbits * 0x0101010101010101ull) & ymask;
+  }
+  __device__ static bool bit(T m, int q) { return (m >> q) & 1ull; }
+  __device__ static uint32_t nibble(T m, int j) { return (uint32_t)(m >> (4 * j)) & 0xFu; }
+};
+
+template <int S>
+__global__ void __launch_bounds__(FINE_WARPS * 32) fine_bin_kernel(
+    const uint32_t* __restrict__ crow, const ushort4* __restrict__ crect, const uint32_t* __restrict__ cstart,
+    const int64_t* __restrict__ tile_starts, const int64_t* counters, int64_t capacity, int tiles_x, int tiles_y,
+    int sx, uint32_t* __restrict__ entries) {
+  constexpr int NT = S * S;
+  using M = FineMask<S>;
+  __shared__ uint32_t s_cnt[FINE_WARPS][NT];
+  if (counters[1] > capacity) return;
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sx0 = (s % sx) * S, sy0 = (s / sx) * S;
+  const uint32_t b = cstart[s], e = cstart[s + 1];
+  const uint32_t per = ((e - b + FINE_WARPS - 1) / FINE_WARPS + 31) & ~31u;
+  const uint32_t w0 = min(e, b + warp * per), w1 = min(e, w0 + per);
+  // pass 1: per-tile counts of this warp's part (4 tiles per byte-packed reduction)
+  uint32_t cnt[NT];
+#pragma unroll
+  for (int q = 0; q < NT; q++) cnt[q] = 0;
+  for (uint32_t k0 = w0; k0 < w1; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    const typename M::T msk = k < w1 ? M::of(__ldg(crect + k), sx0, sy0) : 0;
+#pragma unroll
+    for (int j = 0; j < NT / 4; j++) {
+      const uint32_t packed = __reduce_add_sync(0xffffffffu, (M::nibble(msk, j) * 0x00204081u) & 0x01010101u);
+#pragma unroll
+      for (int i = 0; i < 4; i++) cnt[4 * j + i] += (packed >> (8 * i)) & 0xFFu;
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NT; q++) s_cnt[warp][q] = cnt[q];
+  __syncthreads();
+  uint32_t out[NT];
+#pragma unroll
+  for (int q = 0; q < NT; q++) {
+    const int tx = sx0 + q % S, ty = sy0 + q / S;
+    uint32_t o = 0;
+    if (tx < tiles_x && ty < tiles_y) {
+      o = (uint32_t)tile_starts[ty * tiles_x + tx];
+      for (int w = 0; w < warp; w++) o += s_cnt[w][q];
+    }
+    out[q] = o;
+  }
+  // pass 2: write
+  for (uint32_t k0 = w0; k0 < w1; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    typename M::T msk = 0;
+    uint32_t g = 0;
+    if (k < w1) {
+      msk = M::of(__ldg(crect + k), sx0, sy0);
+      g = __ldg(crow + k);
+    }
+#pragma unroll
+    for (int q = 0; q < NT; q++) {
+      const bool hit = M::bit(msk, q);
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) entries[out[q] + __popc(bal & lanemask_lt())] = g;
+      out[q] += __popc(bal);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 struct TilesScratch {
@@ -354,6 +702,12 @@ struct TilesScratch {
   uint64_t* scan_status;  // 2 x (parts_n + 1)
   uint32_t* hist;         // 10 x 256
   uint32_t* part_ctr;     // 32
+  uint32_t* bin_mat;      // parts_bin x BIN_MAX_SUPER: per-partition super-tile counts
+  uint32_t* bin_slot;     // parts_bin x BIN_MAX_SUPER: slot per (partition, super-tile)
+  uint32_t* chist;        // BIN_MAX_SUPER (zeroed)
+  uint32_t* cstart;       // BIN_MAX_SUPER + 1: super-tile list starts
+  uint32_t* crow;         // capacity: coarse lists (rows)
+  ushort4* crect;         // capacity: coarse lists (tile rectangles)
   int* diff;              // (tiles_x + 1) x (tiles_y + 1)
   size_t control_bytes;
   void* control_begin;
@@ -362,7 +716,10 @@ struct TilesScratch {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned char* base, TilesScratch* s) {
+// n_super_hint > 0: size the binning arrays for that many super-tiles (the
+// scratch-size query, which only knows the tile count)
+static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned char* base, TilesScratch* s,
+                    int n_super_hint = 0) {
   const int n_tiles = tiles_x * tiles_y;
   const size_t tkw = n_tiles > 65535 ? 4 : 2;
   const int64_t nn = n > 0 ? n : 1, cc = cap > 0 ? cap : 1;
@@ -384,6 +741,14 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.tk[1] = take(tkw * cc);
   t.tv0 = (uint32_t*)take(4 * cc);
   t.tv1 = (uint32_t*)take(4 * cc);
+  const bool binned = (n_super_hint > 0 ? n_super_hint <= BIN_MAX_SUPER : super_shift(tiles_x, tiles_y) >= 0);
+  t.crow = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)cc) : nullptr;
+  t.bin_mat = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * (size_t)((nn + BIN_PG - 1) / BIN_PG))
+                     : nullptr;
+  t.bin_slot = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * (size_t)((nn + BIN_PG - 1) / BIN_PG))
+                      : nullptr;
+  t.crect = binned ? (ushort4*)take(sizeof(ushort4) * (size_t)cc) : nullptr;
+  t.cstart = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(BIN_MAX_SUPER + 1)) : nullptr;
   const size_t ctl0 = off;
   t.control_begin = base ? base + ctl0 : nullptr;
   t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 2 * parts_k));
@@ -391,6 +756,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.hist = (uint32_t*)take(sizeof(uint32_t) * 10 * RADIX);
   t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);  // [24..27]: depth key min/max (u64 x 2)
   t.diff = (int*)take(sizeof(int) * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1));
+  t.chist = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER) : nullptr;
   t.control_bytes = off - ctl0;
   t.parts_n = parts_n;
   t.parts_k = parts_k;
@@ -461,7 +827,11 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
 extern "C" size_t hgs_tiles_scratch_bytes(int64_t n, int64_t capacity, int32_t n_tiles) {
   // n_tiles is an upper bound on tiles_x * tiles_y; size the difference grid
   // for the worst aspect ratio (tiles_x + 1) * (tiles_y + 1) <= 2 * n_tiles + 1
-  return hgs::carve(n, capacity, n_tiles, 1, nullptr, nullptr) + 8 * (size_t)n_tiles + 4096;
+  // any grid of n_tiles tiles has at most ceil(n_tiles / 4) super-tiles of 4 x 4 (or is not binned):
+  // size the binning arrays whenever some aspect ratio could be binned
+  const bool may_bin = n_tiles <= 16 * hgs::BIN_MAX_SUPER * 16;
+  return hgs::carve(n, capacity, n_tiles, 1, nullptr, nullptr, may_bin ? 1 : hgs::BIN_MAX_SUPER + 1) +
+         8 * (size_t)n_tiles + 4096;
 }
 
 extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* tiles, void* stream) {
@@ -520,6 +890,34 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   depth_fixup_kernel<<<4 * sm_count(), 256, 0, st>>>(k32res, s.dv[0], (const BlendRec*)proj->rec, tiles->counters,
                                                      minmax);
   HGS_CHECK_LAUNCH();
+  const int ss = super_shift(tx, ty);
+  if (ss >= 0) {
+    // 4. two-level rect binning straight into the final (tile, depth, row) order
+    const int sx = (tx + (1 << ss) - 1) >> ss, sy = (ty + (1 << ss) - 1) >> ss, n_super = sx * sy;
+    const int parts = (int)((n + BIN_PG - 1) / BIN_PG);  // upper bound: kernels read m on the device
+    coarse_count_kernel<<<parts, BIN_THREADS, 0, st>>>(s.dv[0], (const ushort4*)proj->rect, tiles->counters,
+                                                       tiles->capacity, ss, sx, n_super, s.bin_mat, s.chist);
+    HGS_CHECK_LAUNCH();
+    coarse_scan_kernel<<<(n_super + 31) / 32, 1024, 0, st>>>(s.bin_mat, s.chist, tiles->counters, tiles->capacity,
+                                                             n_super, s.cstart, s.bin_slot);
+    HGS_CHECK_LAUNCH();
+    coarse_scatter_kernel<<<parts, BIN_THREADS, 0, st>>>(s.dv[0], (const ushort4*)proj->rect, tiles->counters,
+                                                         tiles->capacity, ss, sx, n_super, s.bin_slot, s.crow,
+                                                         s.crect);
+    HGS_CHECK_LAUNCH();
+    if (ss == 2)
+      fine_bin_kernel<4><<<n_super, FINE_WARPS * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
+                                                              tiles->counters, tiles->capacity, tx, ty, sx,
+                                                              tiles->entries);
+    else if (ss == 3)
+      fine_bin_kernel<8><<<n_super, FINE_WARPS * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
+                                                              tiles->counters, tiles->capacity, tx, ty, sx,
+                                                              tiles->entries);
+    else
+      return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large for binning");
+    HGS_CHECK_LAUNCH();
+    return HGS_OK;
+  }
   // 4. offsets of each row's entries in depth order
   offsets_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->count, s.dv[0], tiles->counters, s.offsets,
                                                      s.scan_status + s.parts_n + 1, s.part_ctr + 21, tiles->counters,

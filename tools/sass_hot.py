@@ -4,7 +4,12 @@ prints each SASS instruction with executed count and stall samples; with
 import csv, sys
 
 rows = list(csv.reader(open(sys.argv[1])))
+# a multi-kernel export repeats (kernel name, header) blocks: keep the first kernel
 hdr = rows[1]
+for k in range(2, len(rows)):
+    if rows[k] and rows[k][0] == "Kernel Name":
+        rows = rows[:k]
+        break
 ia, isrc, isamp, iexe = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 data = [(int(r[ia], 16), r[isrc].strip(), int(r[isamp] or 0), int(r[iexe] or 0)) for r in rows[2:] if len(r) > iexe]
 base = data[0][0]
