@@ -3,55 +3,40 @@
 // _chain_to_parameters (splat/render.py:185-313) + densify statistic and
 // visibility (render.py:171-178).
 //
-// K5: one CTA per 16x16 tile, warps own 8x4 sub-tiles.  Each pixel walks its
-// tile list in reverse from its last blended entry (kernels.py:120),
-// recomputing sigma; T before each entry is reconstructed by division, the
-// suffix colour starts at T_final * (mesh colour or background), exactly as
-// the reference.  Entries are staged in shared memory in batches of 256
-// (newest first) and culled per warp with the same ellipse/sub-tile test as
-// the forward pass.  The per-entry 9-vector (mean2d 2, cov 3 full-matrix
-// convention, alpha, rgb 3) is reduced over the warp (reduce-scatter in
-// fp32) and added to the per-Gaussian fp64 accumulator with one atomic per
-// component per warp.
+// K5: one CTA per 16x16 tile, warp-specialised like the forward: 8 consumer
+// warps own 8x4 sub-tiles (one pixel per lane), 1 producer warp streams the
+// tile's entries NEWEST FIRST (from the largest `last` of the tile down to
+// the first entry) through a 4-stage cp.async/mbarrier ring.  Each pixel
+// walks back from its last blended entry (kernels.py:120): T before an entry
+// is reconstructed by division, the suffix colour starts at T_final * (mesh
+// colour or background), exactly as the reference.  Per-warp ellipse cull
+// as in the forward.  The per-entry 9-vector (mean2d 2, cov 3 full-matrix
+// convention, alpha, rgb 3) is reduced over the warp (reduce-scatter) and
+// added to the per-Gaussian fp64 accumulator with one atomic per component
+// per warp.
 //
-// exp(): SFU value with a local exact fp64 recompute whenever sigma lies
-// near the 1/255 skip or the 0.99 clamp threshold, so both per-entry
-// decisions equal the reference's.
-#include "common.cuh"
+// Numerics: the per-entry decisions (support m <= 9, skip sigma < 1/255,
+// clamp at 0.99) are the reference's: fp64 conic form, fp32 sigma from the
+// SFU with guard bands (stage.cuh), and an exact fp64 re-evaluation of the
+// entry inside a band.  The gradient arithmetic is fp32.
+#include "stage.cuh"
 
 namespace hgs {
 
-constexpr int BW_THREADS = 256;
-constexpr int BW_BATCH = 256;
-constexpr double BW_LOG2E = 1.4426950408889634;
+constexpr int BW_BATCH = 128;
+constexpr int BW_NSTAGE = 4;
+constexpr int BW_CONSUMERS = 8;
+constexpr int BW_THREADS = (BW_CONSUMERS + 1) * 32;
+constexpr float CLAMP_BAND_INV = 1.0f / (2.0f * EPS_SIG * CLAMP_F);
 
 struct BwSmem {
-  double2 a[BW_BATCH];  // mean x, y
-  double2 b[BW_BATCH];  // conic xx, 2*xy
-  double2 c[BW_BATCH];  // conic yy, depth
-  double2 d[BW_BATCH];  // alpha, r
-  double2 e[BW_BATCH];  // g, b
-  float4 box[BW_BATCH];
-  float4 con[BW_BATCH];
-  uint32_t gid[BW_BATCH];
-  unsigned char list[BW_THREADS / 32][BW_BATCH];
+  StageEntry ent[BW_NSTAGE][BW_BATCH];
+  uint32_t gid[BW_NSTAGE][BW_BATCH];
+  unsigned long long full[BW_NSTAGE];
+  unsigned long long empty[BW_NSTAGE];
+  unsigned char list[BW_CONSUMERS][BW_BATCH];
   int max_last;
 };
-
-__device__ __forceinline__ bool bw_ellipse_meets_box(float4 con, float mx, float my, float x0, float x1, float y0,
-                                                     float y1) {
-  auto edge_min = [](float a, float b, float c, float u, float v0, float v1) {
-    const float v = fminf(fmaxf(-b * u / c, v0), v1);
-    return a * u * u + 2.0f * b * u * v + c * v * v;
-  };
-  const float a = con.x, b = con.y, c = con.z;
-  const float dx0 = x0 - mx, dx1 = x1 - mx, dy0 = y0 - my, dy1 = y1 - my;
-  float mn = edge_min(a, b, c, dx0, dy0, dy1);
-  mn = fminf(mn, edge_min(a, b, c, dx1, dy0, dy1));
-  mn = fminf(mn, edge_min(c, b, a, dy0, dx0, dx1));
-  mn = fminf(mn, edge_min(c, b, a, dy1, dx0, dx1));
-  return mn <= 9.05f;
-}
 
 // Sum 16 per-lane values over the warp (reduce-scatter, 16 shuffles);
 // returns the total of value index scatter16_index(lane); lanes 2k and
@@ -93,165 +78,142 @@ __device__ __forceinline__ int scatter16_index(int lane) {
   return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
 }
 
-// Per-pixel reverse-walk state.
-struct BwPix {
-  int64_t last;
-  double gr, gg, gb, gtp, t_fin, t_after, acc_r, acc_g, acc_b, fx, fy;
-  bool inside, mesh_here;
-};
-
-__device__ __forceinline__ void bw_pixel_init(BwPix& q, int px, int py, int width, int height, int64_t s,
-                                              const hgs_mesh_layer& mesh, double bg0, double bg1, double bg2,
-                                              const double* __restrict__ final_t, const int32_t* __restrict__ last_idx,
-                                              const float* __restrict__ grad_color, const float* __restrict__ grad_t,
-                                              float* __restrict__ mesh_grad, int accumulate_mesh) {
-  q.inside = px < width && py < height;
-  q.fx = px + 0.5;
-  q.fy = py + 0.5;
-  q.last = -1;
-  q.gr = q.gg = q.gb = q.gtp = 0.0;
-  q.t_fin = 1.0;
-  q.mesh_here = false;
-  const int64_t p = (int64_t)py * width + px;
-  if (q.inside) {
-    q.last = last_idx[p];
-    q.gr = grad_color[3 * p];
-    q.gg = grad_color[3 * p + 1];
-    q.gb = grad_color[3 * p + 2];
-    q.gtp = grad_t ? (double)grad_t[p] : 0.0;
-    q.t_fin = final_t[p];
-    q.mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
-    if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
-      const double f = q.mesh_here ? q.t_fin : 0.0;
-      float* mg = mesh_grad + 3 * p;
-      if (accumulate_mesh) {
-        mg[0] += (float)(q.gr * f); mg[1] += (float)(q.gg * f); mg[2] += (float)(q.gb * f);
-      } else {
-        mg[0] = (float)(q.gr * f); mg[1] = (float)(q.gg * f); mg[2] = (float)(q.gb * f);
-      }
-    }
-  }
-  q.t_after = q.t_fin;  // suffix colour starts at T_final * (mesh or background) (kernels.py:111-119)
-  if (q.mesh_here) {
-    q.acc_r = q.t_after * (double)mesh.color[3 * p];
-    q.acc_g = q.t_after * (double)mesh.color[3 * p + 1];
-    q.acc_b = q.t_after * (double)mesh.color[3 * p + 2];
-  } else {
-    q.acc_r = q.t_after * bg0;
-    q.acc_g = q.t_after * bg1;
-    q.acc_b = q.t_after * bg2;
-  }
-  if (q.last >= 0) q.last -= s;  // relative to the tile start
+// Exact per-entry evaluation in the reference's operation order
+// (kernels.py:126-133): returns sigma (or -1: no contribution), the
+// Gaussian value and whether sigma was clamped.
+__device__ __noinline__ float bw_exact_entry(const StageEntry& E, double fx, double fy, float& gauss, bool& clamped) {
+  const double dx = fx - E.a.x, dy = fy - E.a.y;
+  const double m = E.b.x * dx * dx + E.b.y * dx * dy + E.c.x * dy * dy;
+  if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0f;
+  const double g = exp(-0.5 * m);
+  double sg = E.d.x * g;
+  clamped = sg > ALPHA_CLAMP;
+  if (clamped) sg = ALPHA_CLAMP;
+  if (sg < SIGMA_SKIP) return -1.0f;
+  gauss = (float)g;
+  return (float)sg;
 }
 
-// One reverse step of kernels.py:120-160 for entry slot i (relative index
-// rel); adds this pixel's 9-vector into v.
-__device__ __forceinline__ bool bw_pixel_step(BwPix& q, const BwSmem& sm, int i, int rel, float v[16]) {
-  if (q.last < 0 || rel > q.last) return false;
-  const double2 A = sm.a[i], B = sm.b[i], C = sm.c[i];
-  const double dx = q.fx - A.x, dy = q.fy - A.y;
-  const double m = B.x * dx * dx + B.y * dx * dy + C.x * dy * dy;
-  if (m > SUPPORT_MAHAL2 || m < 0.0) return false;
-  // SFU exp, exact fp64 recompute near the skip/clamp thresholds
-  float ef;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ef) : "f"((float)(m * (-0.5 * BW_LOG2E))));
-  double gauss = (double)ef;
-  const double alpha = sm.d[i].x;
-  double sig = alpha * gauss;
-  if (fabs(sig - SIGMA_SKIP) <= 2e-6 * SIGMA_SKIP || fabs(sig - ALPHA_CLAMP) <= 2e-6) {
-    gauss = exp(-0.5 * m);
-    sig = alpha * gauss;
-  }
-  const bool clamped = sig > ALPHA_CLAMP;
-  if (clamped) sig = ALPHA_CLAMP;
-  if (sig < SIGMA_SKIP) return false;
-  const double2 D = sm.d[i], E = sm.e[i];
-  const double cr = D.y, cg = E.x, cb = E.y;
-  const double one_minus = 1.0 - sig;
-  const double inv = 1.0 / one_minus;  // one division for the five of kernels.py:135,142-146
-  const double t_before = q.t_after * inv;
-  const double w = sig * t_before;
-  const float wf = (float)w;
-  v[6] += (float)q.gr * wf;
-  v[7] += (float)q.gg * wf;
-  v[8] += (float)q.gb * wf;
-  double s_i = (q.gr * (cr * t_before - q.acc_r * inv) + q.gg * (cg * t_before - q.acc_g * inv)) +
-               q.gb * (cb * t_before - q.acc_b * inv);
-  if (q.gtp != 0.0) s_i += q.gtp * (-q.t_fin * inv);
-  if (!clamped) {
-    // no decision depends on these: fp32 from here on
-    const float dxf = (float)dx, dyf = (float)dy, cbh = 0.5f * (float)B.y;  // conic xy
-    const float qd_x = (float)B.x * dxf + cbh * dyf;
-    const float qd_y = cbh * dxf + (float)C.x * dyf;
-    const float common = (float)(s_i * sig);
-    const float hc = 0.5f * common;
-    v[0] += common * qd_x;
-    v[1] += common * qd_y;
-    v[2] += hc * qd_x * qd_x;
-    v[3] += hc * qd_x * qd_y;
-    v[4] += hc * qd_y * qd_y;
-    v[5] += (float)(s_i * gauss);
-  }
-  q.acc_r += cr * w;
-  q.acc_g += cg * w;
-  q.acc_b += cb * w;
-  q.t_after = t_before;
-  return true;
-}
-
-// 256 threads = 8 warps, each warp an 8x4 sub-tile, one pixel per lane.
 __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
-    const BlendRec* __restrict__ rec, const float4* __restrict__ cull, const uint32_t* __restrict__ entries,
+    const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, const double* __restrict__ final_t, const int32_t* __restrict__ last_idx,
     const float* __restrict__ grad_color, const float* __restrict__ grad_t, double* __restrict__ screen,
     float* __restrict__ mesh_grad, int accumulate_mesh) {
-  __shared__ BwSmem sm;
+  extern __shared__ __align__(128) unsigned char bw_smem_raw[];
+  BwSmem& sm = *reinterpret_cast<BwSmem*>(bw_smem_raw);
   const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int64_t s = tile_starts[tile];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < BW_NSTAGE; i++) {
+      mbar_init(&sm.full[i], 32);
+      mbar_init(&sm.empty[i], BW_CONSUMERS);
+    }
+    sm.max_last = -1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // ---- consumer pixel state (fp32)
   const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
   const int px = tx * 16 + sx0 + (lane & 7);
   const int py = ty * 16 + sy0 + (lane >> 3);
-  const int64_t s = tile_starts[tile];
+  const bool inside = warp < BW_CONSUMERS && px < width && py < height;
+  const int64_t p = (int64_t)py * width + px;
+  int last = -1;
+  float gr = 0.f, gg = 0.f, gb = 0.f, gtp = 0.f, t_fin = 1.f;
+  float t_after = 1.f, acc_r = 0.f, acc_g = 0.f, acc_b = 0.f;
+  if (inside) {
+    last = last_idx[p];
+    gr = grad_color[3 * p];
+    gg = grad_color[3 * p + 1];
+    gb = grad_color[3 * p + 2];
+    gtp = grad_t ? grad_t[p] : 0.f;
+    t_fin = (float)final_t[p];
+    const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
+    if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
+      const float f = mesh_here ? t_fin : 0.f;
+      float* mg = mesh_grad + 3 * p;
+      if (accumulate_mesh) {
+        mg[0] += gr * f; mg[1] += gg * f; mg[2] += gb * f;
+      } else {
+        mg[0] = gr * f; mg[1] = gg * f; mg[2] = gb * f;
+      }
+    }
+    // suffix colour starts at T_final * (mesh colour or background) (kernels.py:111-119)
+    t_after = t_fin;
+    if (mesh_here) {
+      acc_r = t_fin * mesh.color[3 * p];
+      acc_g = t_fin * mesh.color[3 * p + 1];
+      acc_b = t_fin * mesh.color[3 * p + 2];
+    } else {
+      acc_r = t_fin * (float)bg0;
+      acc_g = t_fin * (float)bg1;
+      acc_b = t_fin * (float)bg2;
+    }
+    if (last >= 0) {
+      last -= (int)s;  // relative to the tile start
+      atomicMax(&sm.max_last, last);
+    }
+  }
+  __syncthreads();
+  const int top = sm.max_last;  // newest entry any pixel of the tile used
+  const int nbatches = (top + BW_BATCH) / BW_BATCH;
+
+  if (warp == BW_CONSUMERS) {
+    // ------------------------------------------------------------ producer
+    for (int b = 0; b < nbatches; b++) {
+      const int slot = b % BW_NSTAGE;
+      if (b >= BW_NSTAGE) warp_wait(&sm.empty[slot], ((b / BW_NSTAGE) - 1) & 1, lane);
+      const int hi = top - b * BW_BATCH;  // slot i holds entry lo + i
+      const int lo = hi - BW_BATCH + 1 > 0 ? hi - BW_BATCH + 1 : 0;
+      for (int i = lane; i < BW_BATCH; i += 32) {
+        StageEntry* dst = &sm.ent[slot][i];
+        if (lo + i <= hi) {
+          const uint32_t g = __ldg(entries + s + lo + i);
+          const char* src = reinterpret_cast<const char*>(rec + g);
+          const char* cs = reinterpret_cast<const char*>(cull + g);
+          cp_async16(&dst->a, src);
+          cp_async16(&dst->b, src + 16);
+          cp_async16(&dst->c, src + 32);
+          cp_async16(&dst->d, src + 48);
+          cp_async16(&dst->f.box, cs);
+          cp_async16(&dst->f.con, cs + 16);
+          cp_async16(&dst->f.col, cs + 32);
+          cp_async4(&sm.gid[slot][i], entries + s + lo + i);
+        } else {
+          cp_async16(&dst->f.box, &g_empty_box);
+        }
+      }
+      cp_async_arrive_noinc(&sm.full[slot]);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const double fx = px + 0.5, fy = py + 0.5;
   const float wx0 = tx * 16 + sx0 + 0.5f, wx1 = wx0 + 7.0f;
   const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + 3.0f;
-  BwPix q0;
-  bw_pixel_init(q0, px, py, width, height, s, mesh, bg0, bg1, bg2, final_t, last_idx, grad_color, grad_t, mesh_grad,
-                accumulate_mesh);
-  if (threadIdx.x == 0) sm.max_last = -1;
-  __syncthreads();
-  if (q0.last >= 0) atomicMax(&sm.max_last, (int)q0.last);
-  __syncthreads();
-  const int top = sm.max_last;  // relative index of the newest entry any pixel used
   const int vidx = scatter16_index(lane);
-  for (int hi = top; hi >= 0; hi -= BW_BATCH) {
+  for (int b = 0; b < nbatches; b++) {
+    const int slot = b % BW_NSTAGE;
+    const int hi = top - b * BW_BATCH;
     const int lo = hi - BW_BATCH + 1 > 0 ? hi - BW_BATCH + 1 : 0;
     const int nb = hi - lo + 1;
-    __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += BW_THREADS) {  // slot i holds entry lo + i
-      const uint32_t g = entries[s + lo + i];
-      const double2* rp = reinterpret_cast<const double2*>(rec + g);
-      sm.a[i] = __ldg(rp);
-      sm.b[i] = __ldg(rp + 1);
-      sm.c[i] = __ldg(rp + 2);
-      sm.d[i] = __ldg(rp + 3);
-      sm.e[i] = __ldg(rp + 4);
-      sm.box[i] = __ldg(cull + 3 * (size_t)g);
-      sm.con[i] = __ldg(cull + 3 * (size_t)g + 1);
-      sm.gid[i] = g;
-    }
-    __syncthreads();
-    // per-warp list, newest first
+    warp_wait(&sm.full[slot], (b / BW_NSTAGE) & 1, lane);
+    // per-warp list of the entries touching the sub-tile, newest first
     int nl = 0;
     for (int k = 0; k < nb; k += 32) {
       const int i = nb - 1 - (k + lane);
       bool hit = false;
       if (i >= 0) {
-        const float4 b = sm.box[i];
-        const float cx = fminf(fmaxf(b.x, wx0), wx1), cy = fminf(fmaxf(b.y, wy0), wy1);
-        hit = fabsf(b.x - cx) <= b.z && fabsf(b.y - cy) <= b.w;
-        if (hit && (b.x != cx || b.y != cy)) hit = bw_ellipse_meets_box(sm.con[i], b.x, b.y, wx0, wx1, wy0, wy1);
+        const float4 q = sm.ent[slot][i].f.box;
+        const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
+        hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
+        if (hit && (q.x != cx || q.y != cy))
+          hit = ellipse_meets_box(sm.ent[slot][i].f.con, q.x, q.y, wx0, wx1, wy0, wy1);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)i;
@@ -260,15 +222,64 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
     __syncwarp();
     for (int li = 0; li < nl; li++) {
       const int i = sm.list[warp][li];
+      const StageEntry& E = sm.ent[slot][i];
+      const bool act = last >= 0 && lo + i <= last;
+      // fast evaluation: fp64 conic form, fp32 sigma
+      const double dx = fx - E.a.x, dy = fy - E.a.y;
+      const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
+      const float uu = __double2float_rn(m * U_SCALE);
+      const float a32 = E.f.col.x;
+      float gauss = ex2_neg(uu);
+      const float sraw = fabsf(a32) * gauss;
+      bool clamped = sraw > CLAMP_F;
+      float sg = fminf(sraw, CLAMP_F);
+      bool ok = act && uu < U9_LO && sg >= SKIP_F;
+      const float key = fminf(amb_key(uu, sg, a32), fabsf(fmaf(sraw, CLAMP_BAND_INV, -CLAMP_F * CLAMP_BAND_INV)));
+      if (act && key <= 1.0f) {  // rare: decide in the reference's order
+        const float x = bw_exact_entry(E, fx, fy, gauss, clamped);
+        ok = x >= 0.0f;
+        sg = x;
+      }
+      if (!__any_sync(0xffffffffu, ok)) continue;
       float v[16];
 #pragma unroll
       for (int c = 0; c < 16; c++) v[c] = 0.0f;
-      const bool c0 = bw_pixel_step(q0, sm, i, lo + i, v);
-      if (__any_sync(0xffffffffu, c0)) {
-        const float tot = warp_reduce_scatter16(v, lane);
-        if ((lane & 1) == 0 && vidx < 9 && tot != 0.0f) atomicAdd(&screen[9 * (size_t)sm.gid[i] + vidx], (double)tot);
+      if (ok) {
+        const float4 col = E.f.col;  // alpha, r, g, b
+        const float inv = __frcp_rn(1.0f - sg);  // one reciprocal for the five divisions of kernels.py:135,142-146
+        const float t_before = t_after * inv;
+        const float w = sg * t_before;
+        v[6] = gr * w;
+        v[7] = gg * w;
+        v[8] = gb * w;
+        float s_i = (gr * (col.y * t_before - acc_r * inv) + gg * (col.z * t_before - acc_g * inv)) +
+                    gb * (col.w * t_before - acc_b * inv);
+        s_i = fmaf(gtp, -t_fin * inv, s_i);
+        if (!clamped) {
+          const float4 con = E.f.con;  // conic xx, xy, yy
+          const float dxf = (float)dx, dyf = (float)dy;
+          const float qd_x = fmaf(con.x, dxf, con.y * dyf);
+          const float qd_y = fmaf(con.y, dxf, con.z * dyf);
+          const float common = s_i * sg;
+          const float hc = 0.5f * common;
+          v[0] = common * qd_x;
+          v[1] = common * qd_y;
+          v[2] = hc * qd_x * qd_x;
+          v[3] = hc * qd_x * qd_y;
+          v[4] = hc * qd_y * qd_y;
+          v[5] = s_i * gauss;
+        }
+        acc_r = fmaf(col.y, w, acc_r);
+        acc_g = fmaf(col.z, w, acc_g);
+        acc_b = fmaf(col.w, w, acc_b);
+        t_after = t_before;
       }
+      const float tot = warp_reduce_scatter16(v, lane);
+      if ((lane & 1) == 0 && vidx < 9 && tot != 0.0f)
+        atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
   }
 }
 
@@ -468,9 +479,15 @@ extern "C" int hgs_blend_backward(const hgs_projected* proj, const hgs_tiles* ti
     ml = *mesh;
   }
   const int n_tiles = tiles->tiles_x * tiles->tiles_y;
-  blend_backward_kernel<<<n_tiles, BW_THREADS, 0, (cudaStream_t)stream>>>(
-      (const BlendRec*)proj->rec, (const float4*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x, width,
-      height, ml, bg_host3[0], bg_host3[1], bg_host3[2], final_t, last, grad_color, grad_t, screen_grads,
+  const size_t smem = sizeof(BwSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(blend_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  blend_backward_kernel<<<n_tiles, BW_THREADS, smem, (cudaStream_t)stream>>>(
+      (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
+      width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], final_t, last, grad_color, grad_t, screen_grads,
       mesh_color_grad, accumulate_mesh);
   HGS_CHECK_LAUNCH();
   return HGS_OK;

@@ -29,27 +29,17 @@
 //    reference's too.  The mesh-depth stop is an exact fp64 compare.
 //  * Culled entries cannot change the result: they have no support in the
 //    sub-tile, and the depth stop is monotone along the depth-sorted list.
-#include "common.cuh"
+#include "stage.cuh"
 
 namespace hgs {
 
 constexpr int BLEND_TILE = 16;
 constexpr int BLEND_THREADS = BLEND_TILE * BLEND_TILE;
-constexpr double LOG2E = 1.4426950408889634;
 
 constexpr int BATCH = 128;
 constexpr int NSTAGE = 4;
 constexpr int CONSUMERS = 8;
 constexpr int FAST_THREADS = (CONSUMERS + 1) * 32;
-
-struct __align__(16) StageEntry {
-  double2 a;  // mean x, mean y               (BlendRec bytes 0..15)
-  double2 b;  // conic xx, 2*xy               (16..31)
-  double2 c;  // conic yy, depth              (32..47)
-  double2 d;  // alpha, r (r unused here)     (48..63)
-  CullRec f;  // fp32 box, conic + depth, alpha + colour
-};
-static_assert(sizeof(StageEntry) == 112, "stage entry is 112 B");
 
 struct FastSmem {
   StageEntry ent[NSTAGE][BATCH];
@@ -61,70 +51,6 @@ struct FastSmem {
   unsigned long long stats[2];
 };
 
-__device__ const float4 g_empty_box = {0.0f, 0.0f, -1.0f, -1.0f};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
-}
-// try_wait suspends the polling lane in hardware (until the phase completes
-// or the hint expires) instead of spinning through issue slots
-constexpr unsigned MBAR_SUSPEND_NS = 20000;
-__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "n"(MBAR_SUSPEND_NS)
-      : "memory");
-  return ok != 0;
-}
-// One lane polls (the loop is visible to the compiler, so the warp
-// reconverges at the __syncwarp that publishes the acquired state).
-__device__ __forceinline__ void warp_wait(unsigned long long* bar, unsigned parity, int lane) {
-  if (lane == 0)
-    while (!mbar_try_wait(bar, parity)) {
-    }
-  __syncwarp();
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Conservative test: does the support ellipse {m <= 9} reach any point of
-// the box [x0,x1] x [y0,y1] (centre outside the box)?  The minimum of the
-// convex quadratic m over the box lies on an edge; each edge minimum is a
-// clamped 1D vertex.  fp32 with a generous margin (sure misses only).
-__device__ __forceinline__ float edge_min(float a, float b, float c, float u, float v0, float v1) {
-  // m(u, v) = a u^2 + 2 b u v + c v^2 with u fixed, v in [v0, v1]
-  const float v = fminf(fmaxf(-b * u / c, v0), v1);
-  return a * u * u + 2.0f * b * u * v + c * v * v;
-}
-__device__ __forceinline__ bool ellipse_meets_box(float4 con, float mx, float my, float x0, float x1, float y0,
-                                                  float y1) {
-  const float a = con.x, b = con.y, c = con.z;
-  const float dx0 = x0 - mx, dx1 = x1 - mx, dy0 = y0 - my, dy1 = y1 - my;
-  float mn = edge_min(a, b, c, dx0, dy0, dy1);
-  mn = fminf(mn, edge_min(a, b, c, dx1, dy0, dy1));
-  mn = fminf(mn, edge_min(c, b, a, dy0, dx0, dx1));
-  mn = fminf(mn, edge_min(c, b, a, dy1, dx0, dx1));
-  return mn <= 9.05f;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-
 __device__ __forceinline__ double mask_value(double t, double k, int variant) {
   switch (variant) {
     case 0: return 1.0 / (1.0 + exp(-k * (t - 0.5)));
@@ -132,38 +58,6 @@ __device__ __forceinline__ double mask_value(double t, double k, int variant) {
     case 2: return 1.0;
     default: return 0.0;
   }
-}
-
-// ---- fast-path numerics -------------------------------------------------
-// exp2 argument u = m * log2(e)/2 (fp64), narrowed to fp32 round-to-nearest.
-constexpr double U_SCALE = 0.5 * LOG2E;
-constexpr float U9 = (float)(9.0 * 0.5 * LOG2E);
-constexpr float U9_LO = U9 * (1.0f - 9.5367431640625e-7f);  // 2^-20 guard band around m = 9
-constexpr float U9_BAND_INV = 1.0f / (U9 * 9.5367431640625e-7f);
-// |sigma_fast / sigma_reference - 1| <= EPS_SIG: ex2.approx (2^-22) +
-// argument (ln2 * 6.5 * 2^-24) + alpha narrowing and product (2 * 2^-24)
-constexpr float EPS_SIG = 6.5e-7f;
-constexpr float SKIP_F = (float)SIGMA_SKIP;
-constexpr float SKIP_BAND_INV = 1.0f / (2.0f * EPS_SIG * SKIP_F);
-constexpr float CLAMP_F = (float)ALPHA_CLAMP;
-constexpr float STOP_F = (float)EARLY_STOP_T;
-// T - 2 eT above this: the early-stop test is neither taken nor ambiguous
-constexpr float STOP_NEAR = (float)(EARLY_STOP_T * 1.001);
-
-// Distance of an entry's fast-path decisions from their thresholds, in
-// units of the guard bands; <= 1 means "decide exactly".  A negative alpha
-// (ill-conditioned conic, preprocess) forces the exact evaluation.  (The
-// conic form of a well-conditioned conic is never negative, so m < 0 needs
-// no separate test; alpha >= 1/255 > 1 band-unit is never a false flag.)
-__device__ __forceinline__ float amb_key(float uu, float sgf, float a32) {
-  const float k1 = fabsf(fmaf(uu, U9_BAND_INV, -U9 * U9_BAND_INV));
-  const float k2 = fabsf(fmaf(sgf, SKIP_BAND_INV, -SKIP_F * SKIP_BAND_INV));
-  return fminf(fminf(k1, k2), a32 * 1e4f);
-}
-__device__ __forceinline__ float ex2_neg(float u) {
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-u));
-  return e;
 }
 
 __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_mesh_layer& mesh, bool mesh_here,
