@@ -23,9 +23,9 @@
 
 namespace hgs {
 
-constexpr int BW_BATCH = 128;
-constexpr int BW_NSTAGE = 4;
-constexpr int BW_CONSUMERS = 8;
+constexpr int BW_BATCH = 64;
+constexpr int BW_NSTAGE = 6;
+constexpr int BW_CONSUMERS = 4;  // 8x8-pixel sub-tiles, two pixels per lane
 constexpr int BW_THREADS = (BW_CONSUMERS + 1) * 32;
 constexpr float CLAMP_BAND_INV = 1.0f / (2.0f * EPS_SIG * CLAMP_F);
 
@@ -38,63 +38,179 @@ struct BwSmem {
   int max_last;
 };
 
-// Sum 16 per-lane values over the warp (reduce-scatter, 16 shuffles);
-// returns the total of value index scatter16_index(lane); lanes 2k and
-// 2k+1 hold the same index.
-__device__ __forceinline__ float warp_reduce_scatter16(float v[16], int lane) {
+// Sum 9 per-lane values over the warp (reduce-scatter, 12 shuffles): lane L
+// ends with the total of value index reduce9_index(L) (-1: none).
+__device__ __forceinline__ float warp_reduce9(float v[9], int lane) {
+  // offset 16: lower lanes keep 0..4, upper keep 5..8
+  const bool u16 = lane & 16;
 #pragma unroll
-  for (int i = 0; i < 8; i++) {  // offset 16: keep 8 values
-    const bool upper = lane & 16;
-    const float send = upper ? v[i] : v[i + 8];
+  for (int i = 0; i < 5; i++) {
+    const float hi = i < 4 ? v[5 + i] : 0.0f;
+    const float send = u16 ? v[i] : hi;
     const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
-    v[i] = (upper ? v[i + 8] : v[i]) + recv;
+    v[i] = (u16 ? hi : v[i]) + recv;
   }
+  // now 5 values (upper lanes: 4 + a zero); offset 8: keep 0..2 / 3..4
+  const bool u8 = lane & 8;
 #pragma unroll
-  for (int i = 0; i < 4; i++) {  // offset 8
-    const bool upper = lane & 8;
-    const float send = upper ? v[i] : v[i + 4];
+  for (int i = 0; i < 3; i++) {
+    const float hi = i < 2 ? v[3 + i] : 0.0f;
+    const float send = u8 ? v[i] : hi;
     const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
-    v[i] = (upper ? v[i + 4] : v[i]) + recv;
+    v[i] = (u8 ? hi : v[i]) + recv;
   }
+  // 3 values; offset 4: keep 0..1 / 2
+  const bool u4 = lane & 4;
 #pragma unroll
-  for (int i = 0; i < 2; i++) {  // offset 4
-    const bool upper = lane & 4;
-    const float send = upper ? v[i] : v[i + 2];
+  for (int i = 0; i < 2; i++) {
+    const float hi = i < 1 ? v[2] : 0.0f;
+    const float send = u4 ? v[i] : hi;
     const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
-    v[i] = (upper ? v[i + 2] : v[i]) + recv;
+    v[i] = (u4 ? hi : v[i]) + recv;
   }
-  {  // offset 2
-    const bool upper = lane & 2;
-    const float send = upper ? v[0] : v[1];
+  // 2 values; offset 2: keep 0 / 1
+  {
+    const bool u2 = lane & 2;
+    const float send = u2 ? v[0] : v[1];
     const float recv = __shfl_xor_sync(0xffffffffu, send, 2);
-    v[0] = (upper ? v[1] : v[0]) + recv;
+    v[0] = (u2 ? v[1] : v[0]) + recv;
   }
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
   return v[0];
 }
-
-// value index held by a lane after warp_reduce_scatter16
-__device__ __forceinline__ int scatter16_index(int lane) {
-  return ((lane & 16) ? 8 : 0) + ((lane & 8) ? 4 : 0) + ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
+__device__ __forceinline__ int reduce9_index(int lane) {
+  // level 16: base 0 or 5; level 8: +0 or +3; level 4: +0 or +2; level 2: +0 or +1
+  const int b16 = (lane & 16) ? 5 : 0, b8 = (lane & 8) ? 3 : 0, b4 = (lane & 4) ? 2 : 0, b2 = (lane & 2) ? 1 : 0;
+  // the kept ranges shrink to [0,5)/[5,9), [0,3)/[3,5) ..., so an index past a range end is empty
+  const int n16 = (lane & 16) ? 4 : 5;
+  const int n8 = (lane & 8) ? n16 - 3 : (n16 < 3 ? n16 : 3);
+  const int n4 = (lane & 4) ? n8 - 2 : (n8 < 2 ? n8 : 2);
+  const int n2 = (lane & 2) ? n4 - 1 : (n4 < 1 ? n4 : 1);
+  return (n2 > 0 && (lane & 1) == 0) ? b16 + b8 + b4 + b2 : -1;  // lanes 2k, 2k+1 hold the same total
 }
 
+struct BwExact {
+  float sig, gauss;
+  bool clamped;
+};
 // Exact per-entry evaluation in the reference's operation order
-// (kernels.py:126-133): returns sigma (or -1: no contribution), the
-// Gaussian value and whether sigma was clamped.
-__device__ __noinline__ float bw_exact_entry(const StageEntry& E, double fx, double fy, float& gauss, bool& clamped) {
+// (kernels.py:126-133): sigma (or -1: no contribution), the Gaussian value
+// and whether sigma was clamped.
+__device__ __noinline__ BwExact bw_exact_entry(const StageEntry& E, double fx, double fy) {
+  BwExact r{-1.0f, 0.0f, false};
   const double dx = fx - E.a.x, dy = fy - E.a.y;
   const double m = E.b.x * dx * dx + E.b.y * dx * dy + E.c.x * dy * dy;
-  if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0f;
+  if (m > SUPPORT_MAHAL2 || m < 0.0) return r;
   const double g = exp(-0.5 * m);
   double sg = E.d.x * g;
-  clamped = sg > ALPHA_CLAMP;
-  if (clamped) sg = ALPHA_CLAMP;
-  if (sg < SIGMA_SKIP) return -1.0f;
-  gauss = (float)g;
-  return (float)sg;
+  r.clamped = sg > ALPHA_CLAMP;
+  if (r.clamped) sg = ALPHA_CLAMP;
+  if (sg < SIGMA_SKIP) return r;
+  r.gauss = (float)g;
+  r.sig = (float)sg;
+  return r;
 }
 
-__global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
+// Per-pixel reverse-walk state (fp32).
+struct BwPix {
+  int last;
+  float gr, gg, gb, gtp, t_fin, t_after, acc_r, acc_g, acc_b;
+};
+
+__device__ __forceinline__ void bw_pixel_init(BwPix& q, bool inside, int64_t p, int64_t s, const hgs_mesh_layer& mesh,
+                                              double bg0, double bg1, double bg2, const double* __restrict__ final_t,
+                                              const int32_t* __restrict__ last_idx,
+                                              const float* __restrict__ grad_color, const float* __restrict__ grad_t,
+                                              float* __restrict__ mesh_grad, int accumulate_mesh) {
+  q.last = -1;
+  q.gr = q.gg = q.gb = q.gtp = 0.f;
+  q.t_fin = q.t_after = 1.f;
+  q.acc_r = q.acc_g = q.acc_b = 0.f;
+  if (!inside) return;
+  q.last = last_idx[p];
+  q.gr = grad_color[3 * p];
+  q.gg = grad_color[3 * p + 1];
+  q.gb = grad_color[3 * p + 2];
+  q.gtp = grad_t ? grad_t[p] : 0.f;
+  q.t_fin = (float)final_t[p];
+  const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
+  if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
+    const float f = mesh_here ? q.t_fin : 0.f;
+    float* mg = mesh_grad + 3 * p;
+    if (accumulate_mesh) {
+      mg[0] += q.gr * f; mg[1] += q.gg * f; mg[2] += q.gb * f;
+    } else {
+      mg[0] = q.gr * f; mg[1] = q.gg * f; mg[2] = q.gb * f;
+    }
+  }
+  // suffix colour starts at T_final * (mesh colour or background) (kernels.py:111-119)
+  q.t_after = q.t_fin;
+  if (mesh_here) {
+    q.acc_r = q.t_fin * mesh.color[3 * p];
+    q.acc_g = q.t_fin * mesh.color[3 * p + 1];
+    q.acc_b = q.t_fin * mesh.color[3 * p + 2];
+  } else {
+    q.acc_r = q.t_fin * (float)bg0;
+    q.acc_g = q.t_fin * (float)bg1;
+    q.acc_b = q.t_fin * (float)bg2;
+  }
+  if (q.last >= 0) q.last -= (int)s;  // relative to the tile start
+}
+
+// One reverse step of kernels.py:120-160 for one pixel and entry E (relative
+// index rel): decisions, then the pixel's 9-vector added into v.
+__device__ __forceinline__ void bw_pixel_step(BwPix& q, const StageEntry& E, int rel, double fx, double fy, float v[9]) {
+  const bool act = q.last >= 0 && rel <= q.last;
+  // fast evaluation: fp64 conic form, fp32 sigma
+  const double dx = fx - E.a.x, dy = fy - E.a.y;
+  const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
+  const float uu = __double2float_rn(m * U_SCALE);
+  const float a32 = E.f.col.x;
+  float gauss = ex2_neg(uu);
+  const float sraw = fabsf(a32) * gauss;
+  bool clamped = sraw > CLAMP_F;
+  float sg = fminf(sraw, CLAMP_F);
+  bool ok = act && uu < U9_LO && sg >= SKIP_F;
+  const float key = fminf(amb_key(uu, sg, a32), fabsf(fmaf(sraw, CLAMP_BAND_INV, -CLAMP_F * CLAMP_BAND_INV)));
+  if (act && key <= 1.0f) {  // rare: decide in the reference's order
+    const BwExact x = bw_exact_entry(E, fx, fy);
+    ok = x.sig >= 0.0f;
+    sg = x.sig;
+    gauss = x.gauss;
+    clamped = x.clamped;
+  }
+  if (!ok) return;
+  const float4 col = E.f.col;  // alpha, r, g, b
+  const float inv = __frcp_rn(1.0f - sg);  // one reciprocal for the five divisions of kernels.py:135,142-146
+  const float t_before = q.t_after * inv;
+  const float w = sg * t_before;
+  v[6] = fmaf(q.gr, w, v[6]);
+  v[7] = fmaf(q.gg, w, v[7]);
+  v[8] = fmaf(q.gb, w, v[8]);
+  float s_i = (q.gr * (col.y * t_before - q.acc_r * inv) + q.gg * (col.z * t_before - q.acc_g * inv)) +
+              q.gb * (col.w * t_before - q.acc_b * inv);
+  s_i = fmaf(q.gtp, -q.t_fin * inv, s_i);
+  if (!clamped) {
+    const float4 con = E.f.con;  // conic xx, xy, yy
+    const float dxf = (float)dx, dyf = (float)dy;
+    const float qd_x = fmaf(con.x, dxf, con.y * dyf);
+    const float qd_y = fmaf(con.y, dxf, con.z * dyf);
+    const float common = s_i * sg;
+    const float hc = 0.5f * common;
+    v[0] = fmaf(common, qd_x, v[0]);
+    v[1] = fmaf(common, qd_y, v[1]);
+    v[2] = fmaf(hc * qd_x, qd_x, v[2]);
+    v[3] = fmaf(hc * qd_x, qd_y, v[3]);
+    v[4] = fmaf(hc * qd_y, qd_y, v[4]);
+    v[5] = fmaf(s_i, gauss, v[5]);
+  }
+  q.acc_r = fmaf(col.y, w, q.acc_r);
+  q.acc_g = fmaf(col.z, w, q.acc_g);
+  q.acc_b = fmaf(col.w, w, q.acc_b);
+  q.t_after = t_before;
+}
+
+__global__ void __launch_bounds__(BW_THREADS, 4) blend_backward_kernel(
     const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, const double* __restrict__ final_t, const int32_t* __restrict__ last_idx,
@@ -115,54 +231,24 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
-  // ---- consumer pixel state (fp32)
-  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
+  // consumer pixels: warp w owns the 8x8 sub-tile (w & 1, w >> 1); lane
+  // (x, y) = (lane & 7, lane >> 3) holds pixels (x, y) and (x, y + 4)
+  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
   const int px = tx * 16 + sx0 + (lane & 7);
-  const int py = ty * 16 + sy0 + (lane >> 3);
-  const bool inside = warp < BW_CONSUMERS && px < width && py < height;
-  const int64_t p = (int64_t)py * width + px;
-  int last = -1;
-  float gr = 0.f, gg = 0.f, gb = 0.f, gtp = 0.f, t_fin = 1.f;
-  float t_after = 1.f, acc_r = 0.f, acc_g = 0.f, acc_b = 0.f;
-  if (inside) {
-    last = last_idx[p];
-    gr = grad_color[3 * p];
-    gg = grad_color[3 * p + 1];
-    gb = grad_color[3 * p + 2];
-    gtp = grad_t ? grad_t[p] : 0.f;
-    t_fin = (float)final_t[p];
-    const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
-    if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
-      const float f = mesh_here ? t_fin : 0.f;
-      float* mg = mesh_grad + 3 * p;
-      if (accumulate_mesh) {
-        mg[0] += gr * f; mg[1] += gg * f; mg[2] += gb * f;
-      } else {
-        mg[0] = gr * f; mg[1] = gg * f; mg[2] = gb * f;
-      }
-    }
-    // suffix colour starts at T_final * (mesh colour or background) (kernels.py:111-119)
-    t_after = t_fin;
-    if (mesh_here) {
-      acc_r = t_fin * mesh.color[3 * p];
-      acc_g = t_fin * mesh.color[3 * p + 1];
-      acc_b = t_fin * mesh.color[3 * p + 2];
-    } else {
-      acc_r = t_fin * (float)bg0;
-      acc_g = t_fin * (float)bg1;
-      acc_b = t_fin * (float)bg2;
-    }
-    if (last >= 0) {
-      last -= (int)s;  // relative to the tile start
-      atomicMax(&sm.max_last, last);
-    }
-  }
+  const int py0 = ty * 16 + sy0 + (lane >> 3), py1 = py0 + 4;
+  const bool cons = warp < BW_CONSUMERS;
+  BwPix q0, q1;
+  bw_pixel_init(q0, cons && px < width && py0 < height, (int64_t)py0 * width + px, s, mesh, bg0, bg1, bg2, final_t,
+                last_idx, grad_color, grad_t, mesh_grad, accumulate_mesh);
+  bw_pixel_init(q1, cons && px < width && py1 < height, (int64_t)py1 * width + px, s, mesh, bg0, bg1, bg2, final_t,
+                last_idx, grad_color, grad_t, mesh_grad, accumulate_mesh);
+  const int ml = max(q0.last, q1.last);
+  if (ml >= 0) atomicMax(&sm.max_last, ml);
   __syncthreads();
   const int top = sm.max_last;  // newest entry any pixel of the tile used
   const int nbatches = (top + BW_BATCH) / BW_BATCH;
 
-  if (warp == BW_CONSUMERS) {
+  if (!cons) {
     // ------------------------------------------------------------ producer
     for (int b = 0; b < nbatches; b++) {
       const int slot = b % BW_NSTAGE;
@@ -193,10 +279,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
   }
 
   // -------------------------------------------------------------- consumers
-  const double fx = px + 0.5, fy = py + 0.5;
+  const double fx = px + 0.5, fy0 = py0 + 0.5, fy1 = py1 + 0.5;
   const float wx0 = tx * 16 + sx0 + 0.5f, wx1 = wx0 + 7.0f;
-  const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + 3.0f;
-  const int vidx = scatter16_index(lane);
+  const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + 7.0f;
+  const int vidx = reduce9_index(lane);
   for (int b = 0; b < nbatches; b++) {
     const int slot = b % BW_NSTAGE;
     const int hi = top - b * BW_BATCH;
@@ -223,60 +309,15 @@ __global__ void __launch_bounds__(BW_THREADS, 2) blend_backward_kernel(
     for (int li = 0; li < nl; li++) {
       const int i = sm.list[warp][li];
       const StageEntry& E = sm.ent[slot][i];
-      const bool act = last >= 0 && lo + i <= last;
-      // fast evaluation: fp64 conic form, fp32 sigma
-      const double dx = fx - E.a.x, dy = fy - E.a.y;
-      const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
-      const float uu = __double2float_rn(m * U_SCALE);
-      const float a32 = E.f.col.x;
-      float gauss = ex2_neg(uu);
-      const float sraw = fabsf(a32) * gauss;
-      bool clamped = sraw > CLAMP_F;
-      float sg = fminf(sraw, CLAMP_F);
-      bool ok = act && uu < U9_LO && sg >= SKIP_F;
-      const float key = fminf(amb_key(uu, sg, a32), fabsf(fmaf(sraw, CLAMP_BAND_INV, -CLAMP_F * CLAMP_BAND_INV)));
-      if (act && key <= 1.0f) {  // rare: decide in the reference's order
-        const float x = bw_exact_entry(E, fx, fy, gauss, clamped);
-        ok = x >= 0.0f;
-        sg = x;
-      }
-      if (!__any_sync(0xffffffffu, ok)) continue;
-      float v[16];
+      float v[9];
 #pragma unroll
-      for (int c = 0; c < 16; c++) v[c] = 0.0f;
-      if (ok) {
-        const float4 col = E.f.col;  // alpha, r, g, b
-        const float inv = __frcp_rn(1.0f - sg);  // one reciprocal for the five divisions of kernels.py:135,142-146
-        const float t_before = t_after * inv;
-        const float w = sg * t_before;
-        v[6] = gr * w;
-        v[7] = gg * w;
-        v[8] = gb * w;
-        float s_i = (gr * (col.y * t_before - acc_r * inv) + gg * (col.z * t_before - acc_g * inv)) +
-                    gb * (col.w * t_before - acc_b * inv);
-        s_i = fmaf(gtp, -t_fin * inv, s_i);
-        if (!clamped) {
-          const float4 con = E.f.con;  // conic xx, xy, yy
-          const float dxf = (float)dx, dyf = (float)dy;
-          const float qd_x = fmaf(con.x, dxf, con.y * dyf);
-          const float qd_y = fmaf(con.y, dxf, con.z * dyf);
-          const float common = s_i * sg;
-          const float hc = 0.5f * common;
-          v[0] = common * qd_x;
-          v[1] = common * qd_y;
-          v[2] = hc * qd_x * qd_x;
-          v[3] = hc * qd_x * qd_y;
-          v[4] = hc * qd_y * qd_y;
-          v[5] = s_i * gauss;
-        }
-        acc_r = fmaf(col.y, w, acc_r);
-        acc_g = fmaf(col.z, w, acc_g);
-        acc_b = fmaf(col.w, w, acc_b);
-        t_after = t_before;
-      }
-      const float tot = warp_reduce_scatter16(v, lane);
-      if ((lane & 1) == 0 && vidx < 9 && tot != 0.0f)
-        atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
+      for (int c = 0; c < 9; c++) v[c] = 0.0f;
+      bw_pixel_step(q0, E, lo + i, fx, fy0, v);
+      bw_pixel_step(q1, E, lo + i, fx, fy1, v);
+      const bool any = v[6] != 0.0f || v[7] != 0.0f || v[8] != 0.0f || v[5] != 0.0f || v[0] != 0.0f;
+      if (!__any_sync(0xffffffffu, any)) continue;
+      const float tot = warp_reduce9(v, lane);
+      if (vidx >= 0 && tot != 0.0f) atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);

@@ -367,8 +367,9 @@ constexpr int BIN_WARPS = BIN_THREADS / 32;
 constexpr int BIN_PG = 1024;                 // depth-ordered rows per partition
 constexpr int BIN_SUB = BIN_PG / BIN_WARPS;  // rows per warp
 constexpr int BIN_MAX_SUPER = 256;           // super-tiles: one look-back digit per thread
-constexpr int FINE_WARPS = 16;
-constexpr int FINE_DEPTH = 8;  // rounds of 32 list entries in flight per warp
+// warps per fine CTA (two CTAs per SM: the grid is one wave of super-tiles)
+__host__ __device__ constexpr int fine_warps(int S) { return S == 4 ? 16 : 8; }
+constexpr int FINE_DEPTH = 4;  // rounds of 32 list entries in flight per warp
 
 // smallest super-tile shift with at most BIN_MAX_SUPER super-tiles (or -1)
 __host__ __device__ inline int super_shift(int tiles_x, int tiles_y) {
@@ -392,54 +393,108 @@ __device__ __forceinline__ ushort4 coarse_rect(ushort4 rc, int ss) {
   return make_ushort4(rc.x >> ss, rc.y >> ss, rc.z >> ss, rc.w >> ss);
 }
 
-// Owner rows of one round of 32 consecutive flattened pairs o0 + lane: ra
-// is the owner of o0 (warp-uniform, updated to the owner of o0 + 32).  Every
-// row has at least one pair, so at most 32 rows start inside the round; lane
-// i looks at the start of row ra + 1 + i and the row starts become a bit
-// mask of the round.
-__device__ __forceinline__ int round_owner(const uint32_t* off, uint32_t o0, int& ra, int lane) {
-  const int r = ra + 1 + lane;
-  const uint32_t st = r <= BIN_SUB ? off[r] : 0xffffffffu;
-  const uint32_t rel = st - o0;  // >= 1 for the rows after ra
-  const unsigned bits = __reduce_or_sync(0xffffffffu, rel < 32 ? (1u << rel) : 0u);
-  const int own = ra + __popc(bits & ((2u << lane) - 1u));
-  ra += __popc(bits) + (__any_sync(0xffffffffu, rel == 32) ? 1 : 0);
-  return own;
+// ---- coarse level, partitioned by (row, super-tile) pairs ---------------
+// The depth-ordered rows are flattened into their coarse pairs; pair
+// offsets come from three small prep kernels; then every warp owns exactly
+// CP_WARP consecutive pairs and every partition CP_PART (a huge near-camera
+// rectangle is spread over many warps instead of stalling one).
+constexpr int CP_WARP = 512;
+constexpr int CP_PART = CP_WARP * BIN_WARPS;
+constexpr int PREP_ROWS = 4096;  // rows per prep block (256 threads x 16)
+
+__device__ __forceinline__ uint32_t coarse_pairs(ushort4 rc, int ss) {
+  return (uint32_t)((rc.y >> ss) - (rc.x >> ss) + 1) * (uint32_t)((rc.w >> ss) - (rc.z >> ss) + 1);
 }
 
-struct CoarseSmem {
-  uint32_t cnt[BIN_WARPS][BIN_MAX_SUPER];  // per-warp counters, then per-warp slots
-  uint32_t off[BIN_WARPS][BIN_SUB + 1];    // per-warp exclusive pair offsets of the rows
-  uint32_t row[BIN_PG];
-  ushort4 rect[BIN_PG];
-  ushort4 crect[BIN_PG];
-};
+// prep 1: rectangles in depth order, per-block pair sums
+__global__ void __launch_bounds__(256) coarse_prep_sum_kernel(const uint32_t* __restrict__ sorted_rows,
+                                                              const ushort4* __restrict__ rect, const int64_t* counters,
+                                                              int ss, ushort4* __restrict__ rsort,
+                                                              uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t s_w[8];
+  const int64_t m = counters[0];
+  const int64_t b0 = (int64_t)blockIdx.x * PREP_ROWS;
+  if (b0 >= m) return;
+  uint32_t sum = 0;
+  for (int i = threadIdx.x; i < PREP_ROWS; i += 256) {
+    const int64_t j = b0 + i;
+    if (j < m) {
+      const ushort4 rc = rect[sorted_rows[j]];
+      rsort[j] = rc;
+      sum += coarse_pairs(rc, ss);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; w++) t += s_w[w];
+    bsum[blockIdx.x] = t;
+  }
+}
 
-// Stage partition `part` (rows, coarse rectangles, per-warp pair offsets)
-// and count every warp's (row, super-tile) pairs per super-tile.  Returns
-// the warp's pair total.
-__device__ __forceinline__ uint32_t coarse_stage_count(CoarseSmem& sm, const uint32_t* __restrict__ sorted_rows,
-                                                       const ushort4* __restrict__ rect, int64_t base, int64_t m,
-                                                       int ss, int sx) {
+// prep 2 (one CTA): exclusive scan of the block sums; pair total -> *npairs
+__global__ void __launch_bounds__(1024) coarse_prep_scan_kernel(const int64_t* counters, uint32_t* __restrict__ bsum,
+                                                                uint32_t* __restrict__ npairs) {
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  const int64_t m = counters[0];
+  const int nblk = (int)((m + PREP_ROWS - 1) / PREP_ROWS);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < BIN_WARPS * BIN_MAX_SUPER; i += BIN_THREADS) (&sm.cnt[0][0])[i] = 0;
-  constexpr int PER = BIN_SUB / 32;
-  const int w0 = warp * BIN_SUB;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nblk; b0 += 1024) {
+    const int i = b0 + threadIdx.x;
+    const uint32_t v = i < nblk ? bsum[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_w[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t carry = s_carry;
+    const uint32_t excl = carry + (warp ? s_w[warp - 1] : 0u) + x - v;
+    if (i < nblk) bsum[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = carry + s_w[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *npairs = s_carry;
+}
+
+// prep 3: pair offset of every row (pair_off[m] = total) and the first row
+// of every CP_WARP-pair warp range
+__global__ void __launch_bounds__(256) coarse_prep_offsets_kernel(const ushort4* __restrict__ rsort,
+                                                                  const int64_t* counters, int ss,
+                                                                  const uint32_t* __restrict__ bpre,
+                                                                  const uint32_t* __restrict__ npairs,
+                                                                  uint32_t* __restrict__ pair_off,
+                                                                  uint32_t* __restrict__ wstart) {
+  __shared__ uint32_t s_w[8];
+  const int64_t m = counters[0];
+  const int64_t b0 = (int64_t)blockIdx.x * PREP_ROWS;
+  if (b0 >= m) return;
+  constexpr int PER = PREP_ROWS / 256;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t c[PER], lsum = 0;
 #pragma unroll
   for (int q = 0; q < PER; q++) {
-    const int li = w0 + lane * PER + q;
-    const int64_t j = base + li;
-    c[q] = 0;
-    if (j < m) {
-      const uint32_t g = sorted_rows[j];
-      const ushort4 rc = rect[g];
-      const ushort4 cr = coarse_rect(rc, ss);
-      sm.row[li] = g;
-      sm.rect[li] = rc;
-      sm.crect[li] = cr;
-      c[q] = (uint32_t)(cr.y - cr.x + 1) * (uint32_t)(cr.w - cr.z + 1);
-    }
+    const int64_t j = b0 + threadIdx.x * PER + q;
+    c[q] = j < m ? coarse_pairs(rsort[j], ss) : 0u;
     lsum += c[q];
   }
   uint32_t x = lsum;
@@ -448,47 +503,116 @@ __device__ __forceinline__ uint32_t coarse_stage_count(CoarseSmem& sm, const uin
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  uint32_t run = x - lsum;
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  uint32_t run = bpre[blockIdx.x] + x - lsum;
+  for (int w = 0; w < warp; w++) run += s_w[w];
 #pragma unroll
   for (int q = 0; q < PER; q++) {
-    sm.off[warp][lane * PER + q] = run;
+    const int64_t j = b0 + threadIdx.x * PER + q;
+    if (j < m) {
+      pair_off[j] = run;
+      for (uint32_t k = (run + CP_WARP - 1) / CP_WARP; k * CP_WARP < run + c[q]; k++) wstart[k] = (uint32_t)j;
+    }
     run += c[q];
   }
-  if (lane == 31) sm.off[warp][BIN_SUB] = x;
-  __syncthreads();
-  const uint32_t total = sm.off[warp][BIN_SUB];
-  int ra = 0;
-  for (uint32_t o0 = 0; o0 < total; o0 += 32) {
-    const uint32_t o = o0 + lane;
-    const int r = round_owner(sm.off[warp], o0, ra, lane);
-    if (o < total) {
-      const ushort4 cr = sm.crect[w0 + r];
-      atomicAdd(&sm.cnt[warp][rect_tile(o - sm.off[warp][r], cr, (uint32_t)(cr.y - cr.x + 1), sx)], 1u);
-    }
-  }
-  __syncthreads();
-  return total;
+  if (b0 + PREP_ROWS >= m && threadIdx.x == 0) pair_off[m] = *npairs;
 }
 
-// per-partition super-tile counts -> mat[part][BIN_MAX_SUPER], and their
-// totals -> hist (zeroed)
-__global__ void __launch_bounds__(BIN_THREADS) coarse_count_kernel(const uint32_t* __restrict__ sorted_rows,
-                                                                   const ushort4* __restrict__ rect,
-                                                                   const int64_t* counters, int64_t capacity, int ss,
-                                                                   int sx, int ns, uint32_t* __restrict__ mat,
+// Walk the CP_WARP pairs of warp range k in rounds of 32 (lane = pair):
+// f(valid, super-tile, row, fine rectangle).  Lane i looks at row ra + 1 + i
+// (coalesced): the row starts inside the round become a bit mask, each
+// lane's owner is ra + (starts at or before it), and the owner's data comes
+// over a shuffle (every row has at least one pair, so at most 32 rows start
+// inside a round).
+template <typename F>
+__device__ __forceinline__ void walk_pairs(uint32_t k, uint32_t P, int64_t m, const uint32_t* __restrict__ pair_off,
+                                           const ushort4* __restrict__ rsort, const uint32_t* __restrict__ sorted_rows,
+                                           const uint32_t* __restrict__ wstart, int ss, int sx, int lane, F f) {
+  const uint32_t ob = k * CP_WARP, oe = min(P, ob + CP_WARP);
+  if (ob >= oe) return;
+  int64_t ra = wstart[k];
+  uint32_t offA = pair_off[ra], gA = sorted_rows[ra];
+  ushort4 rcA = rsort[ra];
+  for (uint32_t o0 = ob; o0 < oe; o0 += 32) {
+    const int64_t r = ra + 1 + lane;
+    const uint32_t st = r <= m ? pair_off[r] : 0xffffffffu;
+    ushort4 rcL = make_ushort4(0, 0, 0, 0);
+    uint32_t gL = 0;
+    if (r < m) {
+      rcL = rsort[r];
+      gL = sorted_rows[r];
+    }
+    const uint32_t rel = st - o0;  // >= 1: ra owns o0
+    const unsigned bits = __reduce_or_sync(0xffffffffu, rel < 32 ? (1u << rel) : 0u);
+    const int kown = __popc(bits & ((2u << lane) - 1u));
+    const int src = kown > 0 ? kown - 1 : 0;
+    const uint32_t rlo = (uint32_t)rcL.x | ((uint32_t)rcL.y << 16), rhi = (uint32_t)rcL.z | ((uint32_t)rcL.w << 16);
+    const uint32_t o_off = __shfl_sync(0xffffffffu, st, src);
+    const uint32_t o_g = __shfl_sync(0xffffffffu, gL, src);
+    const uint32_t o_lo = __shfl_sync(0xffffffffu, rlo, src), o_hi = __shfl_sync(0xffffffffu, rhi, src);
+    const uint32_t off = kown ? o_off : offA, g = kown ? o_g : gA;
+    const ushort4 rc = kown ? make_ushort4(o_lo & 0xffffu, o_lo >> 16, o_hi & 0xffffu, o_hi >> 16) : rcA;
+    const uint32_t o = o0 + lane;
+    const bool valid = o < oe;
+    uint32_t sti = 0xffffffffu;
+    if (valid) {
+      const ushort4 cr = coarse_rect(rc, ss);
+      sti = rect_tile(o - off, cr, (uint32_t)(cr.y - cr.x + 1), sx);
+    }
+    f(valid, sti, g, rc);
+    const int adv = __popc(bits) + (__any_sync(0xffffffffu, rel == 32) ? 1 : 0);
+    if (adv > 0) {
+      offA = __shfl_sync(0xffffffffu, st, adv - 1);
+      gA = __shfl_sync(0xffffffffu, gL, adv - 1);
+      const uint32_t a_lo = __shfl_sync(0xffffffffu, rlo, adv - 1), a_hi = __shfl_sync(0xffffffffu, rhi, adv - 1);
+      rcA = make_ushort4(a_lo & 0xffffu, a_lo >> 16, a_hi & 0xffffu, a_hi >> 16);
+      ra += adv;
+    }
+  }
+}
+
+struct CoarseArgs {
+  const uint32_t* sorted_rows;
+  const ushort4* rsort;
+  const uint32_t* pair_off;
+  const uint32_t* wstart;
+  const uint32_t* npairs;
+  const int64_t* counters;
+  int64_t capacity;
+  int ss, sx, ns;
+};
+
+// per-partition super-tile counts -> mat[part][BIN_MAX_SUPER], totals -> hist
+__global__ void __launch_bounds__(BIN_THREADS) coarse_count_kernel(CoarseArgs a, uint32_t* __restrict__ mat,
+                                                                   uint32_t* __restrict__ wmat,
                                                                    uint32_t* __restrict__ hist) {
-  __shared__ CoarseSmem sm;
-  const int64_t m = counters[0];
-  if (counters[1] > capacity) return;  // overflow: flagged in counters[2]
-  const int64_t base = (int64_t)blockIdx.x * BIN_PG;
-  if (base >= m) return;
-  coarse_stage_count(sm, sorted_rows, rect, base, m, ss, sx);
-  if (threadIdx.x < ns) {
-    uint32_t acc = 0;
+  __shared__ uint32_t cnt[BIN_WARPS][BIN_MAX_SUPER];
+  const int64_t m = a.counters[0];
+  if (a.counters[1] > a.capacity) return;  // overflow: flagged in counters[2]
+  const uint32_t P = *a.npairs;
+  const int nparts = (int)((P + CP_PART - 1) / CP_PART);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int part = blockIdx.x; part < nparts; part += gridDim.x) {
+    for (int i = threadIdx.x; i < BIN_WARPS * BIN_MAX_SUPER; i += BIN_THREADS) (&cnt[0][0])[i] = 0;
+    __syncthreads();
+    walk_pairs((uint32_t)part * BIN_WARPS + warp, P, m, a.pair_off, a.rsort, a.sorted_rows, a.wstart, a.ss, a.sx, lane,
+               [&](bool valid, uint32_t sti, uint32_t, ushort4) {
+                 if (valid) atomicAdd(&cnt[warp][sti], 1u);
+               });
+    __syncthreads();
+    if (threadIdx.x < a.ns) {  // per-warp exclusive prefix (for the scatter) and partition total
+      uint32_t acc = 0;
 #pragma unroll
-    for (int w = 0; w < BIN_WARPS; w++) acc += sm.cnt[w][threadIdx.x];
-    mat[(size_t)blockIdx.x * BIN_MAX_SUPER + threadIdx.x] = acc;
-    if (acc) atomicAdd(&hist[threadIdx.x], acc);
+      for (int w = 0; w < BIN_WARPS; w++) {
+        const uint32_t v = cnt[w][threadIdx.x];
+        wmat[((size_t)part * BIN_WARPS + w) * BIN_MAX_SUPER + threadIdx.x] = acc;
+        acc += v;
+      }
+      mat[(size_t)part * BIN_MAX_SUPER + threadIdx.x] = acc;
+      if (acc) atomicAdd(&hist[threadIdx.x], acc);
+    }
+    __syncthreads();
   }
 }
 
@@ -497,14 +621,13 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_count_kernel(const uint32_
 // the partitions (lane = super-tile).
 __global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __restrict__ mat,
                                                            const uint32_t* __restrict__ hist, const int64_t* counters,
-                                                           int64_t capacity, int ns, uint32_t* __restrict__ cstart,
+                                                           int64_t capacity, const uint32_t* __restrict__ npairs,
+                                                           int ns, uint32_t* __restrict__ cstart,
                                                            uint32_t* __restrict__ slot) {
   __shared__ uint32_t s_sum[32][33];
   __shared__ uint32_t s_start[32];
-  __shared__ uint32_t s_tmp[8];
-  const int64_t m = counters[0];
   if (counters[1] > capacity) return;
-  const int nparts = (int)((m + BIN_PG - 1) / BIN_PG);
+  const int nparts = (int)((*npairs + CP_PART - 1) / CP_PART);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   if (warp == 0) {
@@ -513,7 +636,8 @@ __global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __res
     for (int t = lane; t < blockIdx.x * 32; t += 32) pre += hist[t];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
-    uint32_t h = c < ns ? hist[c] : 0u, x = h;
+    const uint32_t h = c < ns ? hist[c] : 0u;
+    uint32_t x = h;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -523,7 +647,6 @@ __global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __res
     if (c < ns) cstart[c] = pre + x - h;
     if (c == ns - 1) cstart[ns] = pre + x;
   }
-  (void)s_tmp;
   const int per = (nparts + 31) / 32;
   const int p0 = warp * per, p1 = min(nparts, p0 + per);
   uint32_t sum = 0;
@@ -540,51 +663,71 @@ __global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __res
   }
 }
 
-// in-order ranking of every warp's (row, super-tile) pairs and the scatter
-// of (row, tile rectangle) into the coarse lists
-__global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(
-    const uint32_t* __restrict__ sorted_rows, const ushort4* __restrict__ rect, const int64_t* counters,
-    int64_t capacity, int ss, int sx, int ns, const uint32_t* __restrict__ slot, uint32_t* __restrict__ crow,
-    ushort4* __restrict__ crect_out) {
-  __shared__ CoarseSmem sm;
-  const int64_t m = counters[0];
-  if (counters[1] > capacity) return;
-  const int64_t base = (int64_t)blockIdx.x * BIN_PG;
-  if (base >= m) return;
-  const uint32_t total = coarse_stage_count(sm, sorted_rows, rect, base, m, ss, sx);
-  if (threadIdx.x < ns) {  // counters -> slot of every warp
-    uint32_t acc = slot[(size_t)blockIdx.x * BIN_MAX_SUPER + threadIdx.x];
-#pragma unroll
-    for (int w = 0; w < BIN_WARPS; w++) {
-      const uint32_t v = sm.cnt[w][threadIdx.x];
-      sm.cnt[w][threadIdx.x] = acc;
-      acc += v;
-    }
-  }
-  __syncthreads();
+// in-order ranking of every warp's pairs and the scatter of (row, tile
+// rectangle) into the coarse lists
+// The partition's pairs are first placed in shared memory in (super-tile,
+// rank) order, then written out as contiguous runs per super-tile
+// (coalesced: a random (row, super-tile) scatter would touch a fresh 32 B
+// sector per pair).
+struct ScatterSmem {
+  uint4 stage[CP_PART];                      // row, rect lo, rect hi, super-tile
+  uint32_t cnt[BIN_WARPS][BIN_MAX_SUPER];    // per-warp local positions
+  uint32_t lstart[BIN_MAX_SUPER + 1];        // partition-local run starts
+  uint32_t gslot[BIN_MAX_SUPER];             // global slot of each run
+  uint32_t warp_tmp[8];
+};
+
+__global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs a, const uint32_t* __restrict__ mat,
+                                                                     const uint32_t* __restrict__ slot,
+                                                                     const uint32_t* __restrict__ wmat,
+                                                                     uint32_t* __restrict__ crow,
+                                                                     ushort4* __restrict__ crect_out) {
+  extern __shared__ __align__(16) unsigned char sc_raw[];
+  ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(sc_raw);
+  const int64_t m = a.counters[0];
+  if (a.counters[1] > a.capacity) return;
+  const uint32_t P = *a.npairs;
+  const int nparts = (int)((P + CP_PART - 1) / CP_PART);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int w0 = warp * BIN_SUB;
-  int ra = 0;
-  for (uint32_t o0 = 0; o0 < total; o0 += 32) {
-    const uint32_t o = o0 + lane;
-    const bool valid = o < total;
-    uint32_t sti = 0xffffffffu;
-    const int r = round_owner(sm.off[warp], o0, ra, lane);
-    if (valid) {
-      const ushort4 cr = sm.crect[w0 + r];
-      sti = rect_tile(o - sm.off[warp][r], cr, (uint32_t)(cr.y - cr.x + 1), sx);
+  for (int part = blockIdx.x; part < nparts; part += gridDim.x) {
+    const uint32_t k = (uint32_t)part * BIN_WARPS + warp;
+    {  // partition-local run starts (exclusive scan over super-tiles; one per thread)
+      const uint32_t c = threadIdx.x < a.ns ? mat[(size_t)part * BIN_MAX_SUPER + threadIdx.x] : 0u;
+      uint32_t tot;
+      const uint32_t e = block_exclusive_scan<uint32_t>(c, sm.warp_tmp, tot);
+      sm.lstart[threadIdx.x] = e;
+      if (threadIdx.x == 0) sm.lstart[BIN_MAX_SUPER] = tot;
+      sm.gslot[threadIdx.x] = threadIdx.x < a.ns ? slot[(size_t)part * BIN_MAX_SUPER + threadIdx.x] : 0u;
+      __syncthreads();
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, sti);
-    uint32_t cur = 0;
-    if (valid) cur = sm.cnt[warp][sti];
-    __syncwarp();
-    if (valid) {
-      const uint32_t pos = cur + __popc(peers & lanemask_lt());
-      crow[pos] = sm.row[w0 + r];
-      crect_out[pos] = sm.rect[w0 + r];
-      if (lane == __ffs(peers) - 1) sm.cnt[warp][sti] = cur + __popc(peers);
+    for (int i = threadIdx.x; i < BIN_WARPS * BIN_MAX_SUPER; i += BIN_THREADS) {
+      const int t = i % BIN_MAX_SUPER;
+      (&sm.cnt[0][0])[i] = t < a.ns ? sm.lstart[t] + wmat[(size_t)part * BIN_WARPS * BIN_MAX_SUPER + i] : 0u;
     }
-    __syncwarp();
+    __syncthreads();
+    walk_pairs(k, P, m, a.pair_off, a.rsort, a.sorted_rows, a.wstart, a.ss, a.sx, lane,
+               [&](bool valid, uint32_t sti, uint32_t g, ushort4 rc) {
+                 const unsigned peers = __match_any_sync(0xffffffffu, sti);
+                 uint32_t cur = 0;
+                 if (valid) cur = sm.cnt[warp][sti];
+                 __syncwarp();
+                 if (valid) {
+                   const uint32_t pos = cur + __popc(peers & lanemask_lt());
+                   sm.stage[pos] = make_uint4(g, (uint32_t)rc.x | ((uint32_t)rc.y << 16),
+                                              (uint32_t)rc.z | ((uint32_t)rc.w << 16), sti);
+                   if (lane == __ffs(peers) - 1) sm.cnt[warp][sti] = cur + __popc(peers);
+                 }
+                 __syncwarp();
+               });
+    __syncthreads();
+    const uint32_t n = sm.lstart[BIN_MAX_SUPER];
+    for (uint32_t i = threadIdx.x; i < n; i += BIN_THREADS) {
+      const uint4 v = sm.stage[i];
+      const uint32_t pos = sm.gslot[v.w] + (i - sm.lstart[v.w]);
+      crow[pos] = v.x;
+      crect_out[pos] = make_ushort4(v.y & 0xffffu, v.y >> 16, v.z & 0xffffu, v.z >> 16);
+    }
+    __syncthreads();
   }
 }
 
@@ -625,12 +768,13 @@ struct FineMask<8> {
 };
 
 template <int S>
-__global__ void __launch_bounds__(FINE_WARPS * 32) fine_bin_kernel(
+__global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
     const uint32_t* __restrict__ crow, const ushort4* __restrict__ crect, const uint32_t* __restrict__ cstart,
     const int64_t* __restrict__ tile_starts, const int64_t* counters, int64_t capacity, int tiles_x, int tiles_y,
     int sx, uint32_t* __restrict__ entries) {
   constexpr int NT = S * S;
   using M = FineMask<S>;
+  constexpr int FINE_WARPS = fine_warps(S);
   __shared__ uint32_t s_cnt[FINE_WARPS][NT];
   if (counters[1] > capacity) return;
   const int s = blockIdx.x;
@@ -639,18 +783,29 @@ __global__ void __launch_bounds__(FINE_WARPS * 32) fine_bin_kernel(
   const uint32_t b = cstart[s], e = cstart[s + 1];
   const uint32_t per = ((e - b + FINE_WARPS - 1) / FINE_WARPS + 31) & ~31u;
   const uint32_t w0 = min(e, b + warp * per), w1 = min(e, w0 + per);
-  // pass 1: per-tile counts of this warp's part (4 tiles per byte-packed reduction)
+  // pass 1: per-tile counts of this warp's part (4 tiles per byte-packed
+  // reduction); the next FINE_DEPTH rounds' rectangles are in flight
   uint32_t cnt[NT];
 #pragma unroll
   for (int q = 0; q < NT; q++) cnt[q] = 0;
-  for (uint32_t k0 = w0; k0 < w1; k0 += 32) {
-    const uint32_t k = k0 + lane;
-    const typename M::T msk = k < w1 ? M::of(__ldg(crect + k), sx0, sy0) : 0;
+  ushort4 rq[FINE_DEPTH];
 #pragma unroll
-    for (int j = 0; j < NT / 4; j++) {
-      const uint32_t packed = __reduce_add_sync(0xffffffffu, (M::nibble(msk, j) * 0x00204081u) & 0x01010101u);
+  for (int d = 0; d < FINE_DEPTH; d++) {
+    const uint32_t k = w0 + d * 32 + lane;
+    rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
+  }
+  for (uint32_t k0 = w0; k0 < w1; k0 += 32 * FINE_DEPTH) {
 #pragma unroll
-      for (int i = 0; i < 4; i++) cnt[4 * j + i] += (packed >> (8 * i)) & 0xFFu;
+    for (int d = 0; d < FINE_DEPTH; d++) {
+      const typename M::T msk = M::of(rq[d], sx0, sy0);
+      const uint32_t k = k0 + (d + FINE_DEPTH) * 32 + lane;
+      rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
+#pragma unroll
+      for (int j = 0; j < NT / 4; j++) {
+        const uint32_t packed = __reduce_add_sync(0xffffffffu, (M::nibble(msk, j) * 0x00204081u) & 0x01010101u);
+#pragma unroll
+        for (int i = 0; i < 4; i++) cnt[4 * j + i] += (packed >> (8 * i)) & 0xFFu;
+      }
     }
   }
   if (lane == 0)
@@ -668,21 +823,29 @@ __global__ void __launch_bounds__(FINE_WARPS * 32) fine_bin_kernel(
     }
     out[q] = o;
   }
-  // pass 2: write
-  for (uint32_t k0 = w0; k0 < w1; k0 += 32) {
-    const uint32_t k = k0 + lane;
-    typename M::T msk = 0;
-    uint32_t g = 0;
-    if (k < w1) {
-      msk = M::of(__ldg(crect + k), sx0, sy0);
-      g = __ldg(crow + k);
-    }
+  // pass 2: write (same prefetch ring)
+  uint32_t gq[FINE_DEPTH];
 #pragma unroll
-    for (int q = 0; q < NT; q++) {
-      const bool hit = M::bit(msk, q);
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (hit) entries[out[q] + __popc(bal & lanemask_lt())] = g;
-      out[q] += __popc(bal);
+  for (int d = 0; d < FINE_DEPTH; d++) {
+    const uint32_t k = w0 + d * 32 + lane;
+    rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
+    gq[d] = k < w1 ? __ldg(crow + k) : 0u;
+  }
+  for (uint32_t k0 = w0; k0 < w1; k0 += 32 * FINE_DEPTH) {
+#pragma unroll
+    for (int d = 0; d < FINE_DEPTH; d++) {
+      const typename M::T msk = M::of(rq[d], sx0, sy0);
+      const uint32_t g = gq[d];
+      const uint32_t k = k0 + (d + FINE_DEPTH) * 32 + lane;
+      rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
+      gq[d] = k < w1 ? __ldg(crow + k) : 0u;
+#pragma unroll
+      for (int q = 0; q < NT; q++) {
+        const bool hit = M::bit(msk, q);
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) entries[out[q] + __popc(bal & lanemask_lt())] = g;
+        out[q] += __popc(bal);
+      }
     }
   }
 }
@@ -704,8 +867,14 @@ struct TilesScratch {
   uint32_t* part_ctr;     // 32
   uint32_t* bin_mat;      // parts_bin x BIN_MAX_SUPER: per-partition super-tile counts
   uint32_t* bin_slot;     // parts_bin x BIN_MAX_SUPER: slot per (partition, super-tile)
+  uint32_t* bin_wmat;     // parts_bin x 8 x BIN_MAX_SUPER: per-warp exclusive counts
   uint32_t* chist;        // BIN_MAX_SUPER (zeroed)
   uint32_t* cstart;       // BIN_MAX_SUPER + 1: super-tile list starts
+  ushort4* rsort;         // n: tile rectangles in depth order
+  uint32_t* pair_off;     // n + 1: coarse pair offsets in depth order
+  uint32_t* bsum;         // prep blocks
+  uint32_t* wstart;       // capacity / CP_WARP + 2: first row of every warp range
+  uint32_t* npairs;       // 1
   uint32_t* crow;         // capacity: coarse lists (rows)
   ushort4* crect;         // capacity: coarse lists (tile rectangles)
   int* diff;              // (tiles_x + 1) x (tiles_y + 1)
@@ -743,10 +912,15 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.tv1 = (uint32_t*)take(4 * cc);
   const bool binned = (n_super_hint > 0 ? n_super_hint <= BIN_MAX_SUPER : super_shift(tiles_x, tiles_y) >= 0);
   t.crow = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)cc) : nullptr;
-  t.bin_mat = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * (size_t)((nn + BIN_PG - 1) / BIN_PG))
-                     : nullptr;
-  t.bin_slot = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * (size_t)((nn + BIN_PG - 1) / BIN_PG))
-                      : nullptr;
+  const size_t cparts = (size_t)(cc / CP_PART + 2);
+  t.bin_mat = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * cparts) : nullptr;
+  t.bin_slot = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * cparts) : nullptr;
+  t.bin_wmat = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * BIN_WARPS * cparts) : nullptr;
+  t.rsort = binned ? (ushort4*)take(sizeof(ushort4) * (size_t)nn) : nullptr;
+  t.pair_off = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(nn + 1)) : nullptr;
+  t.bsum = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(nn / PREP_ROWS + 2)) : nullptr;
+  t.wstart = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(cc / CP_WARP + 2)) : nullptr;
+  t.npairs = binned ? (uint32_t*)take(sizeof(uint32_t) * 4) : nullptr;
   t.crect = binned ? (ushort4*)take(sizeof(ushort4) * (size_t)cc) : nullptr;
   t.cstart = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(BIN_MAX_SUPER + 1)) : nullptr;
   const size_t ctl0 = off;
@@ -894,23 +1068,36 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   if (ss >= 0) {
     // 4. two-level rect binning straight into the final (tile, depth, row) order
     const int sx = (tx + (1 << ss) - 1) >> ss, sy = (ty + (1 << ss) - 1) >> ss, n_super = sx * sy;
-    const int parts = (int)((n + BIN_PG - 1) / BIN_PG);  // upper bound: kernels read m on the device
-    coarse_count_kernel<<<parts, BIN_THREADS, 0, st>>>(s.dv[0], (const ushort4*)proj->rect, tiles->counters,
-                                                       tiles->capacity, ss, sx, n_super, s.bin_mat, s.chist);
+    const int pblk = (int)((n + PREP_ROWS - 1) / PREP_ROWS);  // upper bound: kernels read m on the device
+    coarse_prep_sum_kernel<<<pblk, 256, 0, st>>>(s.dv[0], (const ushort4*)proj->rect, tiles->counters, ss, s.rsort,
+                                                 s.bsum);
+    HGS_CHECK_LAUNCH();
+    coarse_prep_scan_kernel<<<1, 1024, 0, st>>>(tiles->counters, s.bsum, s.npairs);
+    HGS_CHECK_LAUNCH();
+    coarse_prep_offsets_kernel<<<pblk, 256, 0, st>>>(s.rsort, tiles->counters, ss, s.bsum, s.npairs, s.pair_off,
+                                                     s.wstart);
+    HGS_CHECK_LAUNCH();
+    CoarseArgs ca{s.dv[0], s.rsort, s.pair_off, s.wstart, s.npairs, tiles->counters, tiles->capacity, ss, sx, n_super};
+    static int cgrid = 0, sgrid = 0;
+    if (cgrid == 0) {
+      cgrid = persistent_grid((const void*)coarse_count_kernel, BIN_THREADS, 0);
+      cudaFuncSetAttribute(coarse_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
+      sgrid = persistent_grid((const void*)coarse_scatter_kernel, BIN_THREADS, sizeof(ScatterSmem));
+    }
+    coarse_count_kernel<<<cgrid, BIN_THREADS, 0, st>>>(ca, s.bin_mat, s.bin_wmat, s.chist);
     HGS_CHECK_LAUNCH();
     coarse_scan_kernel<<<(n_super + 31) / 32, 1024, 0, st>>>(s.bin_mat, s.chist, tiles->counters, tiles->capacity,
-                                                             n_super, s.cstart, s.bin_slot);
+                                                             s.npairs, n_super, s.cstart, s.bin_slot);
     HGS_CHECK_LAUNCH();
-    coarse_scatter_kernel<<<parts, BIN_THREADS, 0, st>>>(s.dv[0], (const ushort4*)proj->rect, tiles->counters,
-                                                         tiles->capacity, ss, sx, n_super, s.bin_slot, s.crow,
-                                                         s.crect);
+    coarse_scatter_kernel<<<sgrid, BIN_THREADS, sizeof(ScatterSmem), st>>>(ca, s.bin_mat, s.bin_slot, s.bin_wmat,
+                                                                          s.crow, s.crect);
     HGS_CHECK_LAUNCH();
     if (ss == 2)
-      fine_bin_kernel<4><<<n_super, FINE_WARPS * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
+      fine_bin_kernel<4><<<n_super, fine_warps(4) * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
                                                               tiles->counters, tiles->capacity, tx, ty, sx,
                                                               tiles->entries);
     else if (ss == 3)
-      fine_bin_kernel<8><<<n_super, FINE_WARPS * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
+      fine_bin_kernel<8><<<n_super, fine_warps(8) * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
                                                               tiles->counters, tiles->capacity, tx, ty, sx,
                                                               tiles->entries);
     else
