@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(BW_THREADS, 4) blend_backward_kernel(
         const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
         hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
         if (hit && (q.x != cx || q.y != cy))
-          hit = ellipse_meets_box(sm.ent[slot][i].f.con, q.x, q.y, wx0, wx1, wy0, wy1);
+          hit = ellipse_meets_box(sm.ent[slot][i].f.con, q, wx0, wx1, wy0, wy1);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)i;

@@ -146,10 +146,16 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
   }
 
   if (out.cull) {
-    // conservative extents of the m <= 9 ellipse (|dx| <= 3 sqrt(cov_xx)), inflated for the fp32 compare
+    // Where can this Gaussian blend at all?  sigma = alpha exp(-m/2) >= 1/255
+    // needs m <= 2 ln(255 alpha) on top of the support m <= 9 (kernels.py:
+    // 45-51): the per-warp cull of the blend kernels uses that effective
+    // ellipse m <= mcut (margin 1e-4 relative; the tile rectangles stay the
+    // reference's 3-sigma ones).  Box = its conservative extents
+    // (|dx| <= sqrt(mcut cov_xx)), inflated for the fp32 compare.
+    const double mcut = fmin(SUPPORT_MAHAL2, 2.0 * log(alpha / SIGMA_SKIP)) * (1.0 + 1e-4) + 1e-6;
     const float slack = 1e-3f + 2.5e-7f * (float)(fabs(mx) + fabs(my));
-    const float ex = (float)(3.0 * sqrt(cxx)) * (1.0f + 1e-5f) + slack;
-    const float ey = (float)(3.0 * sqrt(cyy)) * (1.0f + 1e-5f) + slack;
+    const float ex = (float)sqrt(mcut * cxx) * (1.0f + 1e-5f) + slack;
+    const float ey = (float)sqrt(mcut * cyy) * (1.0f + 1e-5f) + slack;
     // the blend fast path evaluates the conic form with FMAs; its distance
     // from the reference's rounding is bounded by the conditioning
     // 1 / (1 - rho^2) of the conic -- past 1e6 the entry is always

@@ -59,24 +59,31 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Conservative test: does the support ellipse {m <= 9} reach any point of
-// the box [x0,x1] x [y0,y1] (centre outside the box)?  The minimum of the
-// convex quadratic m over the box lies on an edge; each edge minimum is a
-// clamped 1D vertex.  fp32 with a generous margin (sure misses only).
+// Conservative test: does the ellipse {m <= mcut} reach any point of the
+// box [x0,x1] x [y0,y1] (centre outside the box)?  mcut is recovered from
+// the box half-width ex of the cull record (ex^2 = mcut cov_xx, cov_xx =
+// c / (ac - b^2) for the conic (a, b, c)).  The minimum of the convex
+// quadratic m over the box lies on an edge; each edge minimum is a clamped
+// 1D vertex.  fp32 with a relative margin (sure misses only; the evaluation
+// error is below 3e-4 relative for 1 - rho^2 >= 1e-3).
 __device__ __forceinline__ float edge_min(float a, float b, float c, float u, float v0, float v1) {
   // m(u, v) = a u^2 + 2 b u v + c v^2 with u fixed, v in [v0, v1]
   const float v = fminf(fmaxf(__fdividef(-b * u, c), v0), v1);
   return a * u * u + 2.0f * b * u * v + c * v * v;
 }
-__device__ __forceinline__ bool ellipse_meets_box(float4 con, float mx, float my, float x0, float x1, float y0,
-                                                  float y1) {
+__device__ __forceinline__ bool ellipse_meets_box(float4 con, float4 box, float x0, float x1, float y0, float y1) {
   const float a = con.x, b = con.y, c = con.z;
-  const float dx0 = x0 - mx, dx1 = x1 - mx, dy0 = y0 - my, dy1 = y1 - my;
+  const float det = fmaf(a, c, -b * b);
+  // poorly conditioned conic (1 - rho^2 < 1e-3): fp32 cannot bound m to the
+  // margin -- keep the entry (the box test already passed)
+  if (!(det >= 1e-3f * a * c)) return true;
+  const float mcut = box.z * box.z * __fdividef(det, c);
+  const float dx0 = x0 - box.x, dx1 = x1 - box.x, dy0 = y0 - box.y, dy1 = y1 - box.y;
   float mn = edge_min(a, b, c, dx0, dy0, dy1);
   mn = fminf(mn, edge_min(a, b, c, dx1, dy0, dy1));
   mn = fminf(mn, edge_min(c, b, a, dy0, dx0, dx1));
   mn = fminf(mn, edge_min(c, b, a, dy1, dx0, dx1));
-  return mn <= 9.05f;
+  return mn <= fmaf(mcut, 1.002f, 0.01f);
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {
