@@ -148,9 +148,16 @@ __global__ void __launch_bounds__(256) raster_group_kernel(const double3* __rest
     TriSetup t;
     if (!tri_setup(vproj, tris, f, width, height, cam->near_, t)) continue;
     const int bw = t.x1 - t.x0 + 1;
-    const int64_t area = (int64_t)bw * (t.y1 - t.y0 + 1);
-    for (int64_t q = r; q < area; q += GROUP)
-      raster_pixel<PASS>(t, f, t.x0 + (int)(q % bw), t.y0 + (int)(q / bw), width, zbuf, idbuf);
+    const int area = bw * (t.y1 - t.y0 + 1);  // < 2^31: clipped to the image
+    // box position of q without a division: a running (column, row) pair
+    int qy = r / bw, qx = r - qy * bw;
+    const int sy = GROUP / bw, sx = GROUP - sy * bw;  // GROUP = sy rows + sx columns
+    for (int q = r; q < area; q += GROUP) {
+      raster_pixel<PASS>(t, f, t.x0 + qx, t.y0 + qy, width, zbuf, idbuf);
+      qx += sx;
+      qy += sy;
+      if (qx >= bw) { qx -= bw; qy++; }
+    }
   }
 }
 
