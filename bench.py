@@ -241,6 +241,22 @@ def run_ours(args):
     ms, e2e_ms = float(t[0]), float(t[1])
     _, _, ovf = r.check()
     assert not ovf, "tile-entry capacity overflow during the timed region"
+    # the reference's own bench_fps boundary (metrics.py:44-64): project +
+    # build_tiles + rasterize_forward with the mesh fragments precomputed
+    # (texture sampling kept in the frame)
+    r.capture(rasterize_mesh=False)
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        r.replay()
+    g_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    g_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        g_s[i].record(stream)
+        r.replay()
+        g_e[i].record(stream)
+    torch.cuda.synchronize()
+    gs_ms = float(sum(s_.elapsed_time(e_) for s_, e_ in zip(g_s, g_e))) / args.steps
 
     # live per-kernel timing of the dominant kernel (blend) and the binning
     # stage, on the launching stream, outside the graph
@@ -305,12 +321,16 @@ def run_ours(args):
             "roofline": {"kernel": "blend_fast_kernel (K4)", "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": prof.get("dram_bytes"),
                          "algorithmic_bytes": blend_bytes, "peak_kind": peak_kind, "kernel_ms": blend_ms,
-                         "fp64_pipe_active": prof.get("fp64_pipe_active"),
-                         "note": "K4 is fp64-issue bound, not HBM bound (records are L2-resident): frac is far below "
-                                 "1 by construction; fp64_pipe_active (ncu, profiles/r01_blend_ncu.json) and "
-                                 "compute_rate.blend_evaluations_per_s are the relevant figures"},
+                         "issue_active": prof.get("issue_active"), "fp64_pipe_active": prof.get("fp64_pipe_active"),
+                         "note": "K4 is instruction-issue bound, not HBM bound (the staged records are L2-resident): "
+                                 "frac is far below 1 by construction; issue_active (ncu, "
+                                 "profiles/r01_blend_ncu.json) and compute_rate.blend_evaluations_per_s are the "
+                                 "relevant figures"},
             "compute_rate": {"blend_evaluations_per_s": walked / (blend_ms * 1e-3),
-                             "tiles_stage_ms": tiles_ms, "blend_ms": blend_ms}}
+                             "tiles_stage_ms": tiles_ms, "blend_ms": blend_ms},
+            "gs_frame": {"value": 1000.0 / gs_ms, "unit": UNIT, "ms_per_step": gs_ms,
+                         "note": "the reference's bench_fps boundary (metrics.py:44-64): mesh fragments precomputed, "
+                                 "texture sampling + project + build_tiles + blend per frame"}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         fps_cpu, frames, dt, th = cpu_frames(sc, max_seconds=args.cpu_seconds, max_frames=20,
                                              threads=len(os.sched_getaffinity(0)))
