@@ -169,6 +169,79 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const K* __restrict__ k
   }
 }
 
+// Reduce-then-scan variant of an LSD pass (no look-back chain: for a
+// million keys the decoupled look-back's frontier latency dominates).
+// Upsweep: per-partition digit counts -> pcnt[part][256].
+template <typename K, int IPT>
+__global__ void __launch_bounds__(RS_THREADS) radix_upsweep_kernel(const K* __restrict__ kin, const int64_t* count_ptr,
+                                                                   int64_t cap, int shift, uint32_t* __restrict__ pcnt) {
+  __shared__ uint32_t h[RS_WARPS][RADIX];
+  constexpr int TILE = RS_THREADS * IPT;
+  int64_t n = count_ptr ? *count_ptr : cap;
+  if (n > cap) n = cap;
+  const int64_t base = (int64_t)blockIdx.x * TILE;
+  if (base >= n) return;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_WARPS * RADIX; i += RS_THREADS) (&h[0][0])[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < IPT; j++) {
+    const int64_t i = base + (int64_t)j * RS_THREADS + threadIdx.x;
+    if (i < n) atomicAdd(&h[warp][digit_of<K>(kin[i], shift)], 1u);
+  }
+  __syncthreads();
+  uint32_t c = 0;
+#pragma unroll
+  for (int w = 0; w < RS_WARPS; w++) c += h[w][threadIdx.x];
+  pcnt[(size_t)blockIdx.x * RADIX + threadIdx.x] = c;
+}
+
+// Scan: poff[part][d] = digit base (from the pass histogram) + counts of d
+// in the earlier partitions.  16 CTAs x 16 digits; 64 partition groups per
+// digit (each thread sums a short, independent run of partitions).
+constexpr int RSCAN_DIGITS = 16, RSCAN_GROUPS = 64;
+__global__ void __launch_bounds__(RSCAN_DIGITS * RSCAN_GROUPS) radix_scan_kernel(const uint32_t* __restrict__ hist,
+                                                                                const int64_t* count_ptr, int64_t cap,
+                                                                                int tile, uint32_t* __restrict__ pcnt) {
+  __shared__ uint32_t s_sum[RSCAN_GROUPS][RSCAN_DIGITS + 1];
+  __shared__ uint32_t s_base[RSCAN_DIGITS];
+  int64_t n = count_ptr ? *count_ptr : cap;
+  if (n > cap) n = cap;
+  const int nparts = (int)((n + tile - 1) / tile);
+  const int dl = threadIdx.x % RSCAN_DIGITS, grp = threadIdx.x / RSCAN_DIGITS;
+  const int d = blockIdx.x * RSCAN_DIGITS + dl;
+  if (threadIdx.x < 32) {  // bases of this CTA's digits: histogram sums below them
+    const int lane = threadIdx.x;
+    uint32_t below = 0;
+    for (int t = lane; t < blockIdx.x * RSCAN_DIGITS; t += 32) below += hist[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+    const uint32_t h = lane < RSCAN_DIGITS ? hist[blockIdx.x * RSCAN_DIGITS + lane] : 0u;
+    uint32_t x = h;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane < RSCAN_DIGITS) s_base[lane] = below + x - h;
+  }
+  const int per = (nparts + RSCAN_GROUPS - 1) / RSCAN_GROUPS;
+  const int p0 = grp * per, p1 = min(nparts, p0 + per);
+  uint32_t sum = 0;
+#pragma unroll 4
+  for (int p = p0; p < p1; p++) sum += pcnt[(size_t)p * RADIX + d];
+  s_sum[grp][dl] = sum;
+  __syncthreads();
+  uint32_t run = s_base[dl];
+  for (int g = 0; g < grp; g++) run += s_sum[g][dl];
+#pragma unroll 4
+  for (int p = p0; p < p1; p++) {
+    const uint32_t c = pcnt[(size_t)p * RADIX + d];
+    pcnt[(size_t)p * RADIX + d] = run;
+    run += c;
+  }
+}
+
 template <typename K, int IPT = RS_IPT>
 struct RadixSmem {
   K keys[RS_THREADS * IPT];
@@ -181,7 +254,8 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
                                                                 K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                                 const int64_t* count_ptr, int64_t cap, int shift,
                                                                 const uint32_t* __restrict__ hist, uint32_t* status,
-                                                                int nparts_cap, uint32_t* part_ctr, int write_keys) {
+                                                                int nparts_cap, uint32_t* part_ctr, int write_keys,
+                                                                const uint32_t* __restrict__ poff = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RadixSmem<K, IPT>& sm = *reinterpret_cast<RadixSmem<K, IPT>*>(smem_raw);
   constexpr int TILE = RS_THREADS * IPT;
@@ -201,8 +275,11 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
     uint32_t e = block_exclusive_scan<uint32_t>(hist[tid], s_warp, tot);
     s_digit_base[tid] = e;
   }
+  int iter = 0;
   while (true) {
-    if (tid == 0) s_part = (int)atomicAdd(part_ctr, 1u);
+    // reduce-then-scan mode: static partitions (offsets are precomputed)
+    if (tid == 0) s_part = poff ? (int)blockIdx.x + iter * (int)gridDim.x : (int)atomicAdd(part_ctr, 1u);
+    iter++;
     for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&whist[0][0])[i] = 0;
     __syncthreads();
     const int part = s_part;
@@ -246,6 +323,9 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
       whist[w][tid] = cnt;
       cnt += c;
     }
+    if (poff) {
+      s_gstart[tid] = poff[(size_t)part * RADIX + tid];
+    } else {
     // decoupled look-back for this digit: status is [partition][digit] (a
     // warp's 32 digits are one 128 B line); each round trip reads a window of
     // 16 predecessors (independent coalesced loads)
@@ -283,6 +363,7 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
         st_relaxed(st + (size_t)part * RADIX, RS_FLAG_INC | (excl + cnt));
       }
       s_gstart[tid] = s_digit_base[tid] + excl;
+    }
     }
     {
       uint32_t tot;

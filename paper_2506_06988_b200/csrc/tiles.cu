@@ -78,14 +78,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
   }
 }
 
-// Depth keys -> 32 bits, order preserving: (bits - min) >> shift, where
+// Depth keys -> DEPTH_KEY_BITS bits, order preserving: (bits - min) >> shift, where
 // shift drops the low bits the visible range does not need.  Equal 32-bit
 // keys from distinct fp64 depths are re-ordered exactly by depth_fixup_kernel.
+// Depth keys are sorted on DEPTH_KEY_BITS bits (3 LSD passes); the exact
+// order of keys that collide after the shift is restored by
+// depth_fixup_kernel (1M keys: ~1e4 short runs).
+constexpr int DEPTH_KEY_BITS = 24;
 __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
   const unsigned long long lo = ~minmax[0], hi = minmax[1];
   const unsigned long long range = hi > lo ? hi - lo : 0;
   const int bits = range ? 64 - __clzll((long long)range) : 0;
-  return bits > 32 ? bits - 32 : 0;
+  return bits > DEPTH_KEY_BITS ? bits - DEPTH_KEY_BITS : 0;
 }
 
 __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __restrict__ keys, const int64_t* counters,
@@ -960,10 +964,14 @@ static int persistent_grid(const void* fn, int threads, size_t smem) {
 // shift0: one histogram kernel for all passes, then one single-pass
 // (decoupled look-back) kernel per pass.  The last pass writes its values to
 // final_vals when given.
+// pcnt != nullptr: reduce-then-scan passes (upsweep counts, one scan CTA,
+// rank + scatter from precomputed offsets; pcnt holds parts x 256 words)
+// instead of the single-pass decoupled look-back.
 template <typename K, int IPT = RS_IPT>
 static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_vals, const int64_t* count_ptr,
                       int64_t cap, int shift0, int npasses, uint32_t* hist, bool hist_ready, uint32_t* status,
-                      int64_t parts, uint32_t* part_ctr, cudaStream_t st, K** keys_result, bool last_keys) {
+                      int64_t parts, uint32_t* part_ctr, cudaStream_t st, K** keys_result, bool last_keys,
+                      uint32_t** vals_result = nullptr, uint32_t* pcnt = nullptr) {
   const size_t smem = sizeof(RadixSmem<K, IPT>);
   static int grid = 0;
   if (grid == 0) {
@@ -984,15 +992,23 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
   for (int p = 0; p < npasses; p++) {
     const bool last = p == npasses - 1;
     uint32_t* vdst = last && final_vals ? final_vals : vout;
+    if (pcnt) {
+      radix_upsweep_kernel<K, IPT><<<(int)parts, RS_THREADS, 0, st>>>(kin, count_ptr, cap, shift0 + 8 * p, pcnt);
+      HGS_CHECK_LAUNCH();
+      radix_scan_kernel<<<RADIX / RSCAN_DIGITS, RSCAN_DIGITS * RSCAN_GROUPS, 0, st>>>(hist + RADIX * p, count_ptr, cap,
+                                                                                 (int)tile, pcnt);
+      HGS_CHECK_LAUNCH();
+    }
     radix_pass_kernel<K, IPT><<<g, RS_THREADS, smem, st>>>(kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
                                                       hist + RADIX * p, status + (size_t)p * parts * RADIX, (int)parts,
-                                                      part_ctr + p, (!last || last_keys) ? 1 : 0);
+                                                      part_ctr + p, (!last || last_keys) ? 1 : 0, pcnt);
     HGS_CHECK_LAUNCH();
     std::swap(kin, kout);
     vin = vdst;
     vout = (vdst == v1) ? v0 : v1;
   }
   if (keys_result) *keys_result = kin;
+  if (vals_result) *vals_result = vin;
   return HGS_OK;
 }
 
@@ -1051,17 +1067,19 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   HGS_CHECK_LAUNCH();
   if (n == 0) return HGS_OK;
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
-  // 32-bit order-preserving remap of the depth keys, 4 passes, exact fix-up of truncation ties
+  // order-preserving remap of the depth keys to DEPTH_KEY_BITS, LSD passes, exact fix-up of truncation ties
   uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
   uint32_t* k32b = k32a + (n > 0 ? n : 1);
   unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
   depth_remap_kernel<<<4 * sm_count(), 256, 0, st>>>(s.dk[0], tiles->counters, minmax, k32a);
   HGS_CHECK_LAUNCH();
   uint32_t* k32res = nullptr;
-  int rc = radix_sort<uint32_t, 8>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0, 4, s.hist, false,
-                                s.rs_status, s.parts_n, s.part_ctr, st, &k32res, true);
+  uint32_t* rows = nullptr;  // visible rows in (depth, row) order
+  int rc = radix_sort<uint32_t, 8>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0,
+                                   DEPTH_KEY_BITS / 8, s.hist, false, s.rs_status, s.parts_n, s.part_ctr, st,
+                                   &k32res, true, &rows);
   if (rc) return rc;
-  depth_fixup_kernel<<<4 * sm_count(), 256, 0, st>>>(k32res, s.dv[0], (const BlendRec*)proj->rec, tiles->counters,
+  depth_fixup_kernel<<<4 * sm_count(), 256, 0, st>>>(k32res, rows, (const BlendRec*)proj->rec, tiles->counters,
                                                      minmax);
   HGS_CHECK_LAUNCH();
   const int ss = super_shift(tx, ty);
@@ -1069,7 +1087,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     // 4. two-level rect binning straight into the final (tile, depth, row) order
     const int sx = (tx + (1 << ss) - 1) >> ss, sy = (ty + (1 << ss) - 1) >> ss, n_super = sx * sy;
     const int pblk = (int)((n + PREP_ROWS - 1) / PREP_ROWS);  // upper bound: kernels read m on the device
-    coarse_prep_sum_kernel<<<pblk, 256, 0, st>>>(s.dv[0], (const ushort4*)proj->rect, tiles->counters, ss, s.rsort,
+    coarse_prep_sum_kernel<<<pblk, 256, 0, st>>>(rows, (const ushort4*)proj->rect, tiles->counters, ss, s.rsort,
                                                  s.bsum);
     HGS_CHECK_LAUNCH();
     coarse_prep_scan_kernel<<<1, 1024, 0, st>>>(tiles->counters, s.bsum, s.npairs);
@@ -1077,7 +1095,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     coarse_prep_offsets_kernel<<<pblk, 256, 0, st>>>(s.rsort, tiles->counters, ss, s.bsum, s.npairs, s.pair_off,
                                                      s.wstart);
     HGS_CHECK_LAUNCH();
-    CoarseArgs ca{s.dv[0], s.rsort, s.pair_off, s.wstart, s.npairs, tiles->counters, tiles->capacity, ss, sx, n_super};
+    CoarseArgs ca{rows, s.rsort, s.pair_off, s.wstart, s.npairs, tiles->counters, tiles->capacity, ss, sx, n_super};
     static int cgrid = 0, sgrid = 0;
     if (cgrid == 0) {
       cgrid = persistent_grid((const void*)coarse_count_kernel, BIN_THREADS, 0);
@@ -1106,7 +1124,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     return HGS_OK;
   }
   // 4. offsets of each row's entries in depth order
-  offsets_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->count, s.dv[0], tiles->counters, s.offsets,
+  offsets_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->count, rows, tiles->counters, s.offsets,
                                                      s.scan_status + s.parts_n + 1, s.part_ctr + 21, tiles->counters,
                                                      tiles->capacity);
   HGS_CHECK_LAUNCH();
@@ -1117,11 +1135,11 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   uint32_t* rs_tile_status = s.rs_status + (size_t)8 * s.parts_n * RADIX;
   if (tpasses > 2) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: more than 65536 tiles");
   if (n_tiles > 65535) {
-    emit_kernel<uint32_t><<<4 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+    emit_kernel<uint32_t><<<4 * sm_count(), 256, 0, st>>>(rows, s.offsets, (const ushort4*)proj->rect,
                                                           tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],
                                                           s.tv0, s.big_rows, s.part_ctr + 22);
     HGS_CHECK_LAUNCH();
-    emit_big_kernel<uint32_t><<<2 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+    emit_big_kernel<uint32_t><<<2 * sm_count(), 256, 0, st>>>(rows, s.offsets, (const ushort4*)proj->rect,
                                                               tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],
                                                               s.tv0, s.big_rows, s.part_ctr + 22);
     HGS_CHECK_LAUNCH();
@@ -1129,11 +1147,11 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                               tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, true, rs_tile_status,
                               s.parts_k, s.part_ctr + 8, st, nullptr, false);
   } else {
-    emit_kernel<uint16_t><<<4 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+    emit_kernel<uint16_t><<<4 * sm_count(), 256, 0, st>>>(rows, s.offsets, (const ushort4*)proj->rect,
                                                           tiles->counters, tx, tiles->capacity, (uint16_t*)s.tk[0],
                                                           s.tv0, s.big_rows, s.part_ctr + 22);
     HGS_CHECK_LAUNCH();
-    emit_big_kernel<uint16_t><<<2 * sm_count(), 256, 0, st>>>(s.dv[0], s.offsets, (const ushort4*)proj->rect,
+    emit_big_kernel<uint16_t><<<2 * sm_count(), 256, 0, st>>>(rows, s.offsets, (const ushort4*)proj->rect,
                                                               tiles->counters, tx, tiles->capacity, (uint16_t*)s.tk[0],
                                                               s.tv0, s.big_rows, s.part_ctr + 22);
     HGS_CHECK_LAUNCH();
