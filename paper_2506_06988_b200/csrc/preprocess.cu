@@ -53,6 +53,15 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
   bool ok = (depth > c.near_) && (depth < c.far_);
   const double alpha = 1.0 / (1.0 + exp(-(double)gs.logits[i]));
   ok = ok && (alpha >= SIGMA_SKIP);
+  if (!ok) {
+    // culled before projection (near/far/opacity, project.py:80-83): no
+    // consumer reads anything but the count, the key and the empty box
+    out.count[i] = 0;
+    reinterpret_cast<ushort4*>(out.rect)[i] = make_ushort4(0, 0, 0, 0);
+    if (out.sort_keys) out.sort_keys[i] = ~0ull;
+    if (out.cull) reinterpret_cast<CullRec*>(out.cull)[i].box = make_float4(0.f, 0.f, -1.0f, -1.0f);
+    return;
+  }
   const double tz = ok ? depth : 1.0;
   const double mx = c.fx * t[0] / tz + c.cx;
   const double my = c.fy * t[1] / tz + c.cy;
