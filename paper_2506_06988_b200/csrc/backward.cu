@@ -345,40 +345,30 @@ __device__ __forceinline__ void quat_rot(const double* q, double* Rq, double* qn
   Rq[8] = 1.0 - 2.0 * (x * x + y * y);
 }
 
-__global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera* __restrict__ cam_ptr, hgs_gaussians gs,
-                                                               const int32_t* __restrict__ count,
-                                                               const double* __restrict__ screen,
-                                                               hgs_gaussian_grads out, float scale, int accumulate) {
-  __shared__ ChainCam cc;
-  if (threadIdx.x == 0) {
-    cc.fx = cam_ptr->fx; cc.fy = cam_ptr->fy;
-    cc.W = (double)cam_ptr->width; cc.H = (double)cam_ptr->height;
-    for (int k = 0; k < 9; k++) cc.R[k] = cam_ptr->R[k];
-    for (int k = 0; k < 3; k++) { cc.T[k] = cam_ptr->T[k]; cc.center[k] = cam_ptr->center[k]; }
-    cc.limx = cam_ptr->limx; cc.limy = cam_ptr->limy;
-  }
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= gs.n) return;
-  const bool vis = count[i] > 0;
-  auto put = [&](float* dst, int64_t idx, double v) {
-    if (accumulate) dst[idx] += (float)(v * scale);
-    else dst[idx] = (float)(v * scale);
-  };
-  if (out.visible) {
-    if (accumulate) out.visible[i] |= (uint8_t)vis;
-    else out.visible[i] = (uint8_t)vis;
-  }
-  if (!vis) {
-    if (!accumulate) {
-      for (int k = 0; k < 3; k++) { out.centers[3 * i + k] = 0.f; out.log_scales[3 * i + k] = 0.f; out.colors_dc[3 * i + k] = 0.f; }
-      for (int k = 0; k < 4; k++) out.rotations[4 * i + k] = 0.f;
-      out.logits[i] = 0.f;
-      if (out.colors_rest) for (int k = 0; k < 9; k++) out.colors_rest[9 * i + k] = 0.f;
-      if (out.densify_norm) out.densify_norm[i] = 0.f;
+// Chain rule of one visible Gaussian i (render.py:185-313).
+__device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& gs, const double* __restrict__ screen,
+                                       const hgs_gaussian_grads& out, float scale, int accumulate, int64_t i) {
+  // accumulation: every old gradient value is loaded up front (independent
+  // loads, overlapping the arithmetic) instead of 24 serialised
+  // read-modify-writes through possibly aliasing pointers
+  float o_lg = 0.f, o_dn = 0.f, o_c[3] = {0.f, 0.f, 0.f}, o_s[3] = {0.f, 0.f, 0.f}, o_dc[3] = {0.f, 0.f, 0.f};
+  float o_r[4] = {0.f, 0.f, 0.f, 0.f}, o_rest[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (accumulate) {
+    o_lg = *(out.logits + i);
+    if (out.densify_norm) o_dn = *(out.densify_norm + i);
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      o_c[k] = *(out.centers + 3 * i + k);
+      o_s[k] = *(out.log_scales + 3 * i + k);
+      o_dc[k] = *(out.colors_dc + 3 * i + k);
     }
-    return;
+#pragma unroll
+    for (int k = 0; k < 4; k++) o_r[k] = *(out.rotations + 4 * i + k);
+    if (out.colors_rest)
+#pragma unroll
+      for (int k = 0; k < 9; k++) o_rest[k] = *(out.colors_rest + 9 * i + k);
   }
+  auto put = [&](float* dst, int64_t idx, double v, float old) { dst[idx] = old + (float)(v * scale); };
   const double* pg = screen + 9 * i;
   const double gm0 = pg[0], gm1 = pg[1];
   const double gcov[4] = {pg[2], pg[3], pg[3], pg[4]};
@@ -387,7 +377,7 @@ __global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera*
   const double* Rw = cc.R;
   // opacity: sigma = alpha G, alpha = sigmoid(logit)   (render.py:199-200)
   const double alpha = 1.0 / (1.0 + exp(-(double)gs.logits[i]));
-  put(out.logits, i, ga * alpha * (1.0 - alpha));
+  put(out.logits, i, ga * alpha * (1.0 - alpha), o_lg);
   // colour (render.py:202-220)
   const double c0 = gs.centers[3 * i], c1 = gs.centers[3 * i + 1], c2 = gs.centers[3 * i + 2];
   double pre[3], gpre[3], gc[3] = {0.0, 0.0, 0.0};
@@ -402,9 +392,9 @@ __global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera*
       pre[ch] = pre[ch] + SH_C1 * ((-y * (double)rr[ch] + z * (double)rr[3 + ch]) - x * (double)rr[6 + ch]);
     for (int ch = 0; ch < 3; ch++) gpre[ch] = pg[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
     for (int ch = 0; ch < 3; ch++) {
-      put(out.colors_rest, 9 * i + 0 * 3 + ch, -SH_C1 * y * gpre[ch]);
-      put(out.colors_rest, 9 * i + 1 * 3 + ch, SH_C1 * z * gpre[ch]);
-      put(out.colors_rest, 9 * i + 2 * 3 + ch, -SH_C1 * x * gpre[ch]);
+      put(out.colors_rest, 9 * i + 0 * 3 + ch, -SH_C1 * y * gpre[ch], o_rest[ch]);
+      put(out.colors_rest, 9 * i + 1 * 3 + ch, SH_C1 * z * gpre[ch], o_rest[3 + ch]);
+      put(out.colors_rest, 9 * i + 2 * 3 + ch, -SH_C1 * x * gpre[ch], o_rest[6 + ch]);
     }
     const double s2 = (gpre[0] * rr[6] + gpre[1] * rr[7]) + gpre[2] * rr[8];
     const double s0 = (gpre[0] * rr[0] + gpre[1] * rr[1]) + gpre[2] * rr[2];
@@ -416,7 +406,7 @@ __global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera*
   } else {
     for (int ch = 0; ch < 3; ch++) gpre[ch] = pg[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
   }
-  for (int ch = 0; ch < 3; ch++) put(out.colors_dc, 3 * i + ch, SH_C0 * gpre[ch]);
+  for (int ch = 0; ch < 3; ch++) put(out.colors_dc, 3 * i + ch, SH_C0 * gpre[ch], o_dc[ch]);
   // forward intermediates (render.py:222-248)
   double t[3];
   for (int j = 0; j < 3; j++) t[j] = dot3(c0, c1, c2, Rw[j * 3], Rw[j * 3 + 1], Rw[j * 3 + 2]) + cc.T[j];
@@ -466,7 +456,7 @@ __global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera*
   gt[2] += ((gJ[0] * (-fx * inv_tz2) + gJ[4] * (-fy * inv_tz2)) + gJ[2] * fx * (in_x * rx_raw + rx) * inv_tz2) +
            gJ[5] * fy * (in_y * ry_raw + ry) * inv_tz2;
   for (int c = 0; c < 3; c++) gc[c] += dot3(gt[0], gt[1], gt[2], Rw[c], Rw[3 + c], Rw[6 + c]);
-  for (int c = 0; c < 3; c++) put(out.centers, 3 * i + c, gc[c]);
+  for (int c = 0; c < 3; c++) put(out.centers, 3 * i + c, gc[c], o_c[c]);
   // Sigma = M M^T, M = R diag(s) (render.py:273-277)
   double gM[9], gR[9], gsc[3] = {0.0, 0.0, 0.0};
   for (int a = 0; a < 3; a++)
@@ -480,7 +470,7 @@ __global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera*
       gR[a * 3 + c] = gM[a * 3 + c] * s[c];
       gsc[c] += gM[a * 3 + c] * Rq[a * 3 + c];
     }
-  for (int j = 0; j < 3; j++) put(out.log_scales, 3 * i + j, gsc[j] * s[j]);
+  for (int j = 0; j < 3; j++) put(out.log_scales, 3 * i + j, gsc[j] * s[j], o_s[j]);
   // rotation through dR/dq and the normalisation (render.py:279-284, 290-313)
   const double w = qn[0], x = qn[1], y = qn[2], z = qn[3];
   const double D[4][9] = {{0, -z, y, z, 0, -x, -y, x, 0},
@@ -494,11 +484,59 @@ __global__ void __launch_bounds__(128) project_backward_kernel(const hgs_camera*
     gqn[k] = acc;
   }
   const double dq = ((gqn[0] * qn[0] + gqn[1] * qn[1]) + gqn[2] * qn[2]) + gqn[3] * qn[3];
-  for (int k = 0; k < 4; k++) put(out.rotations, 4 * i + k, (gqn[k] - qn[k] * dq) / nrm);
+  for (int k = 0; k < 4; k++) put(out.rotations, 4 * i + k, (gqn[k] - qn[k] * dq) / nrm, o_r[k]);
   if (out.densify_norm) {
     const double sx = gm0 * (cc.W / 2.0), sy = gm1 * (cc.H / 2.0);
-    put(out.densify_norm, i, sqrt(sx * sx + sy * sy) / (double)scale);
+    put(out.densify_norm, i, sqrt(sx * sx + sy * sy) / (double)scale, o_dn);
   }
+}
+
+// One CTA per PB_SPAN consecutive Gaussians: flags and (without
+// accumulation) zeros for the invisible ones, then the visible ones -- a
+// few percent of them for a training view -- compacted in shared memory
+// so every thread runs the long fp64 chain on a visible Gaussian.
+constexpr int PB_THREADS = 128;
+constexpr int PB_SPAN = 32 * PB_THREADS;
+__global__ void __launch_bounds__(PB_THREADS) project_backward_kernel(const hgs_camera* __restrict__ cam_ptr,
+                                                                      hgs_gaussians gs,
+                                                                      const int32_t* __restrict__ count,
+                                                                      const double* __restrict__ screen,
+                                                                      hgs_gaussian_grads out, float scale,
+                                                                      int accumulate) {
+  __shared__ ChainCam cc;
+  __shared__ int32_t list[PB_SPAN];
+  __shared__ int nlist;
+  if (threadIdx.x == 0) {
+    cc.fx = cam_ptr->fx; cc.fy = cam_ptr->fy;
+    cc.W = (double)cam_ptr->width; cc.H = (double)cam_ptr->height;
+    for (int k = 0; k < 9; k++) cc.R[k] = cam_ptr->R[k];
+    for (int k = 0; k < 3; k++) { cc.T[k] = cam_ptr->T[k]; cc.center[k] = cam_ptr->center[k]; }
+    cc.limx = cam_ptr->limx; cc.limy = cam_ptr->limy;
+    nlist = 0;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * PB_SPAN;
+  for (int k = threadIdx.x; k < PB_SPAN; k += PB_THREADS) {
+    const int64_t i = base + k;
+    if (i >= gs.n) break;
+    const bool vis = count[i] > 0;
+    if (out.visible) {
+      if (accumulate) out.visible[i] |= (uint8_t)vis;
+      else out.visible[i] = (uint8_t)vis;
+    }
+    if (vis) {
+      list[atomicAdd(&nlist, 1)] = (int32_t)k;
+    } else if (!accumulate) {
+      for (int q = 0; q < 3; q++) { out.centers[3 * i + q] = 0.f; out.log_scales[3 * i + q] = 0.f; out.colors_dc[3 * i + q] = 0.f; }
+      for (int q = 0; q < 4; q++) out.rotations[4 * i + q] = 0.f;
+      out.logits[i] = 0.f;
+      if (out.colors_rest) for (int q = 0; q < 9; q++) out.colors_rest[9 * i + q] = 0.f;
+      if (out.densify_norm) out.densify_norm[i] = 0.f;
+    }
+  }
+  __syncthreads();
+  const int nl = nlist;
+  for (int j = threadIdx.x; j < nl; j += PB_THREADS) chain_one(cc, gs, screen, out, scale, accumulate, base + list[j]);
 }
 
 }  // namespace hgs
@@ -544,7 +582,8 @@ extern "C" int hgs_project_backward(const hgs_camera* cam, const hgs_gaussians* 
     return hgs_set_error(HGS_ERR_INVALID, "hgs_project_backward: missing gradient pointer");
   if ((gs->colors_rest == nullptr) != (grads->colors_rest == nullptr))
     return hgs_set_error(HGS_ERR_INVALID, "hgs_project_backward: colors_rest presence mismatch");
-  project_backward_kernel<<<ceil_div(gs->n, 128), 128, 0, (cudaStream_t)stream>>>(cam, *gs, proj->count, screen_grads,
+  project_backward_kernel<<<ceil_div(gs->n, PB_SPAN), PB_THREADS, 0, (cudaStream_t)stream>>>(cam, *gs, proj->count,
+                                                                                         screen_grads,
                                                                                  *grads, scale, accumulate);
   HGS_CHECK_LAUNCH();
   return HGS_OK;
