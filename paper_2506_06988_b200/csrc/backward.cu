@@ -161,6 +161,7 @@ __device__ __forceinline__ void bw_pixel_init(BwPix& q, bool inside, int64_t p, 
 // index rel): decisions, then the pixel's 9-vector added into v.
 __device__ __forceinline__ void bw_pixel_step(BwPix& q, const StageEntry& E, int rel, double fx, double fy, float v[9]) {
   const bool act = q.last >= 0 && rel <= q.last;
+  if (!act) return;  // entry after this pixel's last blended one
   // fast evaluation: fp64 conic form, fp32 sigma
   const double dx = fx - E.a.x, dy = fy - E.a.y;
   const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
@@ -283,6 +284,9 @@ __global__ void __launch_bounds__(BW_THREADS, 4) blend_backward_kernel(
   const float wx0 = tx * 16 + sx0 + 0.5f, wx1 = wx0 + 7.0f;
   const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + 7.0f;
   const int vidx = reduce9_index(lane);
+  int wlast = max(q0.last, q1.last);  // newest entry any pixel of this warp used
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
   for (int b = 0; b < nbatches; b++) {
     const int slot = b % BW_NSTAGE;
     const int hi = top - b * BW_BATCH;
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(BW_THREADS, 4) blend_backward_kernel(
     for (int k = 0; k < nb; k += 32) {
       const int i = nb - 1 - (k + lane);
       bool hit = false;
-      if (i >= 0) {
+      if (i >= 0 && lo + i <= wlast) {
         const float4 q = sm.ent[slot][i].f.box;
         const float cx = fminf(fmaxf(q.x, wx0), wx1), cy = fminf(fmaxf(q.y, wy0), wy1);
         hit = fabsf(q.x - cx) <= q.z && fabsf(q.y - cy) <= q.w;
