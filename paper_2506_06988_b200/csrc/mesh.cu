@@ -5,15 +5,14 @@
 // The reference walks triangles in index order with a strict z test, so a
 // pixel ends up owned by the lexicographic minimum of (z, triangle index)
 // over the fragments that pass its edge tests.  The GPU reproduces exactly
-// that without ordering:
-//   pass 0: every covered fragment does atomicMin(zbuf[p], bits(z))
-//           (positive doubles order like their bit patterns);
-//   pass 1: fragments whose z equals the minimum do atomicMin(idbuf[p], f);
-//   resolve: one thread per pixel recomputes the winner's barycentrics,
-//           depth and uv with the reference's arithmetic (fp64, no FMA).
+// that without ordering, in one pass: every covered fragment lowers the
+// pixel's 16-byte record {bits(z), f} to min((z, f), record) with a 128-bit
+// compare-and-swap loop (positive doubles order like their bit patterns);
+// then resolve: one thread per pixel recomputes the winner's barycentrics,
+// depth and uv with the reference's arithmetic (fp64, no FMA).
 // Work is binned by screen bounding-box area: tiny triangles one thread
 // each, medium ones one warp each (lanes stride the box), large ones one
-// CTA each; the bins are built in pass 0 and reused by pass 1.
+// CTA each (binned by the one-thread-per-triangle pass).
 #include "common.cuh"
 
 namespace hgs {
@@ -96,18 +95,35 @@ __global__ void mesh_project_kernel(const hgs_camera* __restrict__ cam, const fl
   out[i] = make_double3(cam->fx * t[0] / safe + cam->cx, cam->fy * t[1] / safe + cam->cy, t[2]);
 }
 
+__device__ __forceinline__ void zrec_min(unsigned long long* rec, unsigned long long zb, unsigned long long f) {
+  // lexicographic (z bits, triangle) minimum; the CAS returns the current
+  // record, so a torn initial read only costs one more iteration
+  unsigned long long cz = rec[0], cf = rec[1];
+  while (zb < cz || (zb == cz && f < cf)) {
+    unsigned long long oz, of;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 n, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, n;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(oz), "=l"(of)
+        : "l"(cz), "l"(cf), "l"(zb), "l"(f), "l"(rec)
+        : "memory");
+    if (oz == cz && of == cf) return;
+    cz = oz;
+    cf = of;
+  }
+}
+
 template <int PASS>
 __device__ __forceinline__ void raster_pixel(const TriSetup& t, int64_t f, int px, int py, int width,
                                              unsigned long long* zbuf, int32_t* idbuf) {
   double l0, l1, l2, z;
   if (!tri_fragment(t, px, py, l0, l1, l2, z)) return;
   const int64_t p = (int64_t)py * width + px;
-  const unsigned long long zb = (unsigned long long)__double_as_longlong(z);
-  if (PASS == 0) {
-    if (zb < zbuf[p]) atomicMin(&zbuf[p], zb);
-  } else {
-    if (zb == zbuf[p]) atomicMin(&idbuf[p], (int32_t)f);
-  }
+  zrec_min(zbuf + 2 * p, (unsigned long long)__double_as_longlong(z), (unsigned long long)f);
+  (void)idbuf;
 }
 
 template <int PASS>
@@ -161,11 +177,10 @@ __global__ void __launch_bounds__(256) raster_group_kernel(const double3* __rest
   }
 }
 
-__global__ void raster_init_kernel(unsigned long long* zbuf, int32_t* idbuf, int64_t npix) {
+__global__ void raster_init_kernel(unsigned long long* zbuf, int64_t npix) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npix) return;
-  zbuf[p] = 0x7ff0000000000000ull;  // +inf
-  idbuf[p] = 0x7fffffff;
+  reinterpret_cast<ulonglong2*>(zbuf)[p] = make_ulonglong2(0x7ff0000000000000ull, 0x7fffffffull);  // +inf, none
 }
 
 // Winner recompute, meshraster.py:97-116.
@@ -173,10 +188,11 @@ __global__ void __launch_bounds__(256) raster_resolve_kernel(const double3* __re
                                                              const int32_t* __restrict__ tris,
                                                              const float* __restrict__ uvs, int width, int height,
                                                              const hgs_camera* __restrict__ cam,
-                                                             const int32_t* __restrict__ idbuf, hgs_fragments out) {
+                                                             const unsigned long long* __restrict__ zbuf,
+                                                             hgs_fragments out) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (int64_t)width * height) return;
-  const int32_t f = idbuf[p];
+  const int32_t f = (int32_t)zbuf[2 * p + 1];
   const int px = (int)(p % width), py = (int)(p / width);
   double b0 = 0.0, b1 = 0.0, b2 = 0.0, z = __longlong_as_double(0x7ff0000000000000LL), u = 0.0, v = 0.0;
   int32_t tid = -1;
@@ -273,7 +289,7 @@ extern "C" size_t hgs_raster_scratch_bytes(int64_t n_vertices, int64_t n_faces, 
   using hgs::align_up;
   const int64_t npix = (int64_t)width * height;
   return align_up(sizeof(double3) * (size_t)(n_vertices > 0 ? n_vertices : 1), 256) +
-         align_up(8 * (size_t)npix, 256) + align_up(4 * (size_t)npix, 256) +
+         align_up(16 * (size_t)npix, 256) +
          align_up(8 * (size_t)(n_faces > 0 ? n_faces : 1), 256) + 256;
 }
 
@@ -291,15 +307,14 @@ extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int
   unsigned char* base = (unsigned char*)scratch;
   double3* vproj = (double3*)base;
   base += align_up(sizeof(double3) * (size_t)(mesh->n_vertices > 0 ? mesh->n_vertices : 1), 256);
-  unsigned long long* zbuf = (unsigned long long*)base;
-  base += align_up(8 * (size_t)npix, 256);
-  int32_t* idbuf = (int32_t*)base;
-  base += align_up(4 * (size_t)npix, 256);
+  unsigned long long* zbuf = (unsigned long long*)base;  // {bits(z), triangle} per pixel
+  base += align_up(16 * (size_t)npix, 256);
+  int32_t* idbuf = nullptr;
   int32_t* lists = (int32_t*)base;  // [warp list | CTA list], n_faces each
   base += align_up(8 * (size_t)(mesh->n_faces > 0 ? mesh->n_faces : 1), 256);
   int32_t* list_counts = (int32_t*)base;
   cudaMemsetAsync(list_counts, 0, 2 * sizeof(int32_t), st);
-  raster_init_kernel<<<ceil_div(npix, 256), 256, 0, st>>>(zbuf, idbuf, npix);
+  raster_init_kernel<<<ceil_div(npix, 256), 256, 0, st>>>(zbuf, npix);
   HGS_CHECK_LAUNCH();
   if (mesh->n_faces > 0) {
     if (!mesh->vertices || !mesh->triangles) return hgs_set_error(HGS_ERR_INVALID, "hgs_rasterize_fragments: missing mesh arrays");
@@ -322,18 +337,9 @@ extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int
     raster_group_kernel<0, 256><<<2 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
                                                          lists + nf, list_counts + 1);
     HGS_CHECK_LAUNCH();
-    raster_small_kernel<1><<<gf, 256, 0, st>>>(vproj, mesh->triangles, nf, width, height, cam, zbuf, idbuf, lists,
-                                              list_counts);
-    HGS_CHECK_LAUNCH();
-    raster_group_kernel<1, 32><<<8 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
-                                                        lists, list_counts);
-    HGS_CHECK_LAUNCH();
-    raster_group_kernel<1, 256><<<2 * sms, 256, 0, st>>>(vproj, mesh->triangles, width, height, cam, zbuf, idbuf,
-                                                         lists + nf, list_counts + 1);
-    HGS_CHECK_LAUNCH();
   }
   raster_resolve_kernel<<<ceil_div(npix, 256), 256, 0, st>>>(vproj, mesh->triangles, mesh->uvs, width, height, cam,
-                                                             idbuf, *out);
+                                                             zbuf, *out);
   HGS_CHECK_LAUNCH();
   return HGS_OK;
 }
