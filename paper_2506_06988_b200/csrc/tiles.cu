@@ -92,14 +92,29 @@ __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
   return bits > DEPTH_KEY_BITS ? bits - DEPTH_KEY_BITS : 0;
 }
 
+// ... and the digit histograms of the remapped keys for the LSD passes
+// (hist: DEPTH_KEY_BITS / 8 x 256, zeroed), in the same read.
 __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __restrict__ keys, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax,
-                                                          uint32_t* __restrict__ k32) {
+                                                          uint32_t* __restrict__ k32, uint32_t* __restrict__ hist) {
+  constexpr int NP = DEPTH_KEY_BITS / 8;
+  __shared__ uint32_t sh_h[NP][256];
+  for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) (&sh_h[0][0])[i] = 0;
+  __syncthreads();
   const int64_t m = counters[0];
   const unsigned long long lo = ~minmax[0];
   const int sh = depth_shift(minmax);
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
-    k32[j] = (uint32_t)((keys[j] - lo) >> sh);
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = (uint32_t)((keys[j] - lo) >> sh);
+    k32[j] = k;
+#pragma unroll
+    for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) {
+    const uint32_t c = (&sh_h[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
 }
 
 // After the stable 32-bit sort, rows with equal truncated keys are in row
@@ -1071,12 +1086,12 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
   uint32_t* k32b = k32a + (n > 0 ? n : 1);
   unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
-  depth_remap_kernel<<<4 * sm_count(), 256, 0, st>>>(s.dk[0], tiles->counters, minmax, k32a);
+  depth_remap_kernel<<<4 * sm_count(), 256, 0, st>>>(s.dk[0], tiles->counters, minmax, k32a, s.hist);
   HGS_CHECK_LAUNCH();
   uint32_t* k32res = nullptr;
   uint32_t* rows = nullptr;  // visible rows in (depth, row) order
   int rc = radix_sort<uint32_t, 8>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0,
-                                   DEPTH_KEY_BITS / 8, s.hist, false, s.rs_status, s.parts_n, s.part_ctr, st,
+                                   DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr, st,
                                    &k32res, true, &rows);
   if (rc) return rc;
   depth_fixup_kernel<<<4 * sm_count(), 256, 0, st>>>(k32res, rows, (const BlendRec*)proj->rec, tiles->counters,
