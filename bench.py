@@ -182,10 +182,10 @@ def run_ours(args):
     from paper_2506_06988_b200.engine import HybridRenderer
 
     rank, world, local = _dist_env()
-    if world > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local)  # before the process group: NCCL binds to the current device
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     sc = syn.make_config(args.config, seed=0)
     hcam = sc.cameras[0]
     gs = hgs.GaussianSet.from_any(sc.gaussians)
