@@ -72,6 +72,7 @@ class HybridRenderer:
         self.capacity = 0
         self._alloc_entries(capacity if capacity is not None else 16 * n)
         self.graph = None
+        self._side = None
 
     # ------------------------------------------------------------------
     def _alloc_entries(self, capacity: int):
@@ -101,22 +102,37 @@ class HybridRenderer:
         return ps, ts
 
     def enqueue(self, rasterize_mesh: bool = True, mesh_layer: Optional[MeshLayer] = None) -> None:
-        """Enqueue one frame for the camera currently in cam_dev."""
+        """Enqueue one frame for the camera currently in cam_dev.
+
+        The mesh layer (raster + texture fetch) does not depend on the
+        Gaussians: it runs on a side stream forked from the current one and
+        joined before the blend, overlapping preprocess and tile binning
+        (the fork/join is captured into the CUDA graph as well)."""
         L = _lib.load()
-        st = _stream_ptr(self.dev)
+        main = torch.cuda.current_stream(self.dev)
+        st = main.cuda_stream
         w, h = self.width, self.height
         ml = _lib.HGSMeshLayer()
+        joined = None
         if self.mesh is not None and mesh_layer is None:
+            if self._side is None:
+                self._side = torch.cuda.Stream(self.dev)
+                self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
+            self._ev_fork.record(main)
+            self._side.wait_event(self._ev_fork)
+            side = self._side.cuda_stream
             if rasterize_mesh:
                 fr = _lib.HGSFragments()
                 fr.triangle_id, fr.depth, fr.uv = _lib.ptr(self.frag_tri), _lib.ptr(self.frag_depth), _lib.ptr(self.frag_uv)
                 _lib.check(L.hgs_rasterize_fragments(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.mesh.struct()),
                                                      ctypes.byref(fr), _lib.ptr(self.raster_scratch),
-                                                     self.raster_scratch.numel(), st), "rasterize_fragments")
+                                                     self.raster_scratch.numel(), side), "rasterize_fragments")
             tex = self.mesh.texture
             _lib.check(L.hgs_sample_texture(_lib.ptr(tex), tex.shape[0], tex.shape[1], _lib.ptr(self.frag_uv),
-                                            _lib.ptr(self.frag_tri), w * h, _lib.ptr(self.mesh_color), st),
+                                            _lib.ptr(self.frag_tri), w * h, _lib.ptr(self.mesh_color), side),
                        "sample_texture")
+            self._ev_join.record(self._side)
+            joined = self._ev_join
             ml.color, ml.depth, ml.triangle_id = _lib.ptr(self.mesh_color), _lib.ptr(self.frag_depth), _lib.ptr(self.frag_tri)
         elif mesh_layer is not None:
             ml = mesh_layer.struct()
@@ -133,6 +149,8 @@ class HybridRenderer:
             out.mask = _lib.ptr(self.mask_out)
         out.stats = _lib.ptr(self.stats)
         out.fixup = _lib.ptr(self.fixup)
+        if joined is not None:
+            main.wait_event(joined)  # the blend reads the mesh layer
         _lib.check(L.hgs_blend_forward(ctypes.byref(ps), ctypes.byref(ts), w, h, ctypes.byref(ml), _c_f64_3(self.bg),
                                        variant, k, ctypes.byref(out), st), "blend_forward")
 
