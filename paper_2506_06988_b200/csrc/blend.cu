@@ -118,12 +118,23 @@ __device__ __noinline__ ExactPixel exact_walk(const BlendRec* __restrict__ rec, 
   double T = 1.0, pr = 0.0, pg = 0.0, pb = 0.0, pd = 0.0;
   int64_t last = -1;
   bool done = false;
-  BlendRec nxt;
-  if (s + lane < e) nxt = rec[entries[s + lane]];
+  // software pipeline: entry indices four chunks ahead, records two ahead
+  // (one warp per pixel: registers are cheap, the gather latency is not)
+  uint32_t ix[4];
+#pragma unroll
+  for (int d = 0; d < 4; d++) ix[d] = (s + d * 32 + lane < e) ? __ldg(entries + s + d * 32 + lane) : 0u;
+  BlendRec r0, r1;
+  if (s + lane < e) r0 = rec[ix[0]];
+  if (s + 32 + lane < e) r1 = rec[ix[1]];
   for (int64_t base = s; base < e && !done; base += 32) {
     const int64_t k = base + lane;
-    const BlendRec c = nxt;
-    if (base + 32 + lane < e) nxt = rec[entries[base + 32 + lane]];
+    const BlendRec c = r0;
+    r0 = r1;
+    if (base + 64 + lane < e) r1 = rec[ix[2]];
+    ix[0] = ix[1];
+    ix[1] = ix[2];
+    ix[2] = ix[3];
+    if (base + 128 + lane < e) ix[3] = __ldg(entries + base + 128 + lane);
     bool stop = false, use = false;
     double sig = 0.0;
     if (k < e) {
