@@ -75,6 +75,8 @@ typedef struct hgs_gaussian_grads {
   float* colors_rest; /* NULL iff colors_rest is NULL */
   float* densify_norm; /* N, may be NULL */
   uint8_t* visible;    /* N, may be NULL */
+  float* visible_count; /* N, may be NULL: += 1 where visible (density-control denominator,
+                           densify.py:31-33) */
 } hgs_gaussian_grads;
 
 /* Per-Gaussian projection state, indexed by ORIGINAL row (uncompacted).

@@ -44,7 +44,7 @@ class HGSGaussians(ctypes.Structure):
 class HGSGaussianGrads(ctypes.Structure):
     _fields_ = [("centers", c_void_p), ("rotations", c_void_p), ("log_scales", c_void_p), ("logits", c_void_p),
                 ("colors_dc", c_void_p), ("colors_rest", c_void_p), ("densify_norm", c_void_p),
-                ("visible", c_void_p)]
+                ("visible", c_void_p), ("visible_count", c_void_p)]
 
 
 class HGSProjected(ctypes.Structure):

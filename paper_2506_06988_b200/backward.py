@@ -24,13 +24,14 @@ class GradBuffer:
     """Flat fp32 gradient buffer with the parameter layout of a GaussianSet."""
 
     def __init__(self, gs: GaussianSet, flat: Optional[torch.Tensor] = None,
-                 densify_norm: Optional[torch.Tensor] = None):
+                 densify_norm: Optional[torch.Tensor] = None, visible_count: Optional[torch.Tensor] = None):
         self.gs = gs
         self.flat = flat if flat is not None else torch.zeros_like(gs.params)
         assert self.flat.numel() == gs.params.numel() and self.flat.dtype == torch.float32
         self.densify_norm = densify_norm if densify_norm is not None else torch.zeros(
             max(len(gs), 1), dtype=torch.float32, device=gs.device)
         self.visible = torch.zeros(max(len(gs), 1), dtype=torch.uint8, device=gs.device)
+        self.visible_count = visible_count  # optional: views in which each row was visible
 
     def group(self, name: str) -> Optional[torch.Tensor]:
         if name not in self.gs.layout:
@@ -48,6 +49,8 @@ class GradBuffer:
         self.flat.zero_()
         self.densify_norm.zero_()
         self.visible.zero_()
+        if self.visible_count is not None:
+            self.visible_count.zero_()
 
     def struct(self) -> _lib.HGSGaussianGrads:
         s = _lib.HGSGaussianGrads()
@@ -59,6 +62,7 @@ class GradBuffer:
                 setattr(s, field, base + self.gs.layout[name][0] * elt)
         s.densify_norm = self.densify_norm.data_ptr()
         s.visible = self.visible.data_ptr()
+        s.visible_count = self.visible_count.data_ptr() if self.visible_count is not None else None
         return s
 
 

@@ -528,6 +528,10 @@ __global__ void __launch_bounds__(PB_THREADS) project_backward_kernel(const hgs_
       if (accumulate) out.visible[i] |= (uint8_t)vis;
       else out.visible[i] = (uint8_t)vis;
     }
+    if (out.visible_count) {
+      if (accumulate) out.visible_count[i] += vis ? 1.0f : 0.0f;
+      else out.visible_count[i] = vis ? 1.0f : 0.0f;
+    }
     if (vis) {
       list[atomicAdd(&nlist, 1)] = (int32_t)k;
     } else if (!accumulate) {

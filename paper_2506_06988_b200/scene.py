@@ -232,6 +232,16 @@ class Camera:
                       np.asarray(cam.world_to_camera), cam.near, cam.far)
 
 
+def camera_extent(cameras) -> float:
+    """scene.py:314-322: 1.1 x the largest distance of a camera centre from
+    their mean."""
+    if not cameras:
+        raise SceneError("camera_extent needs at least one camera")
+    centers = np.stack([Camera.from_any(c).center() for c in cameras])
+    mean = centers.mean(axis=0)
+    return 1.1 * float(np.linalg.norm(centers - mean, axis=1).max())
+
+
 def camera_struct(cam) -> _lib.HGSCamera:
     """hgs_camera with the derived fields computed like the reference."""
     W = np.asarray(cam.world_to_camera, dtype=np.float64)

@@ -43,7 +43,8 @@ def shard_views(n_views: int, rank: int, world: int) -> List[int]:
 
 class HybridTrainer:
     def __init__(self, gs: GaussianSet, mesh: Optional[TexturedMesh], cameras: Sequence, images: Sequence, config,
-                 rank: int = 0, world: int = 1, process_group=None, allreduce=None):
+                 rank: int = 0, world: int = 1, process_group=None, allreduce=None, density_control: bool = False,
+                 extent: Optional[float] = None, rng: Optional[np.random.Generator] = None):
         self.gs = gs
         self.mesh = mesh
         self.cfg = config
@@ -59,12 +60,7 @@ class HybridTrainer:
         self.images = [im.to(dev, torch.float32).contiguous() for im in self.images]
         self.bg = np.asarray(config.background, dtype=np.float64).reshape(3)
         n = len(gs)
-        # one flat bucket: Gaussian grads | texture grad | densify norms
-        p_sz = gs.params.numel()
-        t_sz = mesh.texture.numel() if (mesh is not None and mesh.texture is not None) else 0
-        self.bucket = torch.zeros(p_sz + t_sz + max(n, 1), dtype=torch.float32, device=dev)
-        self.grads = GradBuffer(gs, self.bucket[:p_sz], self.bucket[p_sz + t_sz:])
-        self.tex_grad = self.bucket[p_sz:p_sz + t_sz].view_as(mesh.texture) if t_sz else None
+        self._alloc_bucket()
         # optimiser state (loop.py:92-117)
         names = [g for g in ("centers", "rotations", "log_scales", "logit_opacities", "colors_dc", "colors_rest")
                  if g in gs.layout]
@@ -75,18 +71,22 @@ class HybridTrainer:
                "colors_rest": config.lr_color / 20.0}
         self.opt = Adam(params, {k: lrs[k] for k in names})
         self.pos_lr = exponential_lr(config.lr_position, config.lr_position_final, config.max_iters)
-        self.tex_opt = Adam({"texture": mesh.texture}, {"texture": config.lr_texture}) if t_sz else None
+        self.tex_opt = Adam({"texture": mesh.texture}, {"texture": config.lr_texture}) if self.tex_grad is not None else None
+        # adaptive density control (loop.py:226-233, densify.py), opt-in
+        self.density_control = density_control
+        if density_control:
+            from .densify import DensifyState
+            from .scene import camera_extent
+            self.extent = extent if extent is not None else (
+                camera_extent(self.cameras) if len(self.cameras) > 1 else 1.0)
+            self.rng = rng if rng is not None else np.random.default_rng(config.seed)
+            self.dstate = DensifyState.zeros(n, dev)
+            self.density_stats: List[dict] = []
         # per-camera fragments, rasterized once (loop.py:172-175)
         self.frags: List[Optional[MeshFragmentBuffer]] = []
         for c in self.cameras:
             self.frags.append(rasterize_fragments(mesh, c, with_bary=False) if mesh is not None else None)
-        # per-view work buffers (reused sequentially on one stream)
-        self.rec = torch.empty(max(n, 1) * REC_BYTES, dtype=torch.uint8, device=dev)
-        self.count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-        self.rect = torch.zeros(max(n, 1) * 4, dtype=torch.int16, device=dev)
-        self.cull = torch.empty(max(n, 1) * 12, dtype=torch.float32, device=dev)
-        self.sort_keys = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
-        self.screen = torch.zeros(max(n, 1) * 9, dtype=torch.float64, device=dev)
+        self._alloc_rows()
         c0 = self.cameras[0]
         self.tx = (int(c0.width) + TILE_PX - 1) // TILE_PX
         self.ty = (int(c0.height) + TILE_PX - 1) // TILE_PX
@@ -99,6 +99,46 @@ class HybridTrainer:
         self._size_entries()
 
     # ------------------------------------------------------------------
+    def _alloc_bucket(self):
+        """One flat bucket, all-reduced once per step: Gaussian grads |
+        texture grad | densify norm sums | visible-view counts."""
+        gs, mesh, dev = self.gs, self.mesh, self.dev
+        n = max(len(gs), 1)
+        p_sz = gs.params.numel()
+        t_sz = mesh.texture.numel() if (mesh is not None and mesh.texture is not None) else 0
+        self.bucket = torch.zeros(p_sz + t_sz + 2 * n, dtype=torch.float32, device=dev)
+        o = p_sz + t_sz
+        self.grads = GradBuffer(gs, self.bucket[:p_sz], self.bucket[o:o + n], self.bucket[o + n:o + 2 * n])
+        self.tex_grad = self.bucket[p_sz:p_sz + t_sz].view_as(mesh.texture) if t_sz else None
+
+    def _alloc_rows(self):
+        """Per-view work buffers sized by the Gaussian count (reused
+        sequentially on one stream)."""
+        n, dev = max(len(self.gs), 1), self.dev
+        self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
+        self.count = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
+        self.cull = torch.empty(n * 12, dtype=torch.float32, device=dev)
+        self.sort_keys = torch.empty(n, dtype=torch.int64, device=dev)
+        self.screen = torch.zeros(n * 9, dtype=torch.float64, device=dev)
+
+    def _density_step(self, it: int) -> None:
+        """loop.py:226-233 after the optimiser steps of iteration ``it``."""
+        from .densify import densify_and_prune, reset_opacity
+        cfg = self.cfg
+        if it >= cfg.densify_until_iter:
+            return
+        self.dstate.update(self.grads.visible_count, self.grads.densify_norm)
+        if it >= cfg.densify_from_iter and it % cfg.densify_interval == 0:
+            self.gs, stats = densify_and_prune(self.gs, self.opt, self.dstate, self.extent, cfg, self.rng)
+            stats["iter"] = it
+            self.density_stats.append(stats)
+            self._alloc_bucket()
+            self._alloc_rows()
+            self._size_entries()
+        if it % cfg.opacity_reset_interval == 0:
+            reset_opacity(self.gs, self.opt)
+
     def _size_entries(self):
         """Tile-entry capacity: max K over this rank's views x 1.2 (one sync)."""
         from .splat import _preprocess
@@ -202,4 +242,6 @@ class HybridTrainer:
         self.opt.step({k: self.grads.group(k) for k in self.names}, renorm=("rotations",))
         if self.tex_opt is not None:
             self.tex_opt.step({"texture": self.tex_grad}, clamp=("texture",))
+        if self.density_control:
+            self._density_step(it)
         return self.loss_sum
