@@ -65,6 +65,25 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
   const double tz = ok ? depth : 1.0;
   const double mx = c.fx * t[0] / tz + c.cx;
   const double my = c.fy * t[1] / tz + c.cy;
+  {
+    // Conservative screen pre-cull (project.py:118-119): the reference's
+    // radius 3 sqrt(lambda_max(J W Sigma W^T J^T + 0.3 I)) is at most
+    // 3 sqrt(|J|_F^2 max(s)^2 + 0.3); a Gaussian whose box with that bound
+    // misses the screen is culled by the reference too -- skip its covariance
+    // (most rows of a training view fall here).
+    const double lsm = fmax(fmax((double)gs.log_scales[3 * i], (double)gs.log_scales[3 * i + 1]),
+                            (double)gs.log_scales[3 * i + 2]);
+    const double rxc = clampd(t[0] / tz, -c.limx, c.limx), ryc = clampd(t[1] / tz, -c.limy, c.limy);
+    const double jf2 = (c.fx * c.fx * (1.0 + rxc * rxc) + c.fy * c.fy * (1.0 + ryc * ryc)) / (tz * tz);
+    const double r_ub = 3.0 * sqrt(jf2 * exp(2.0 * lsm) + COV_FLOOR) * (1.0 + 1e-6) + 1e-6;
+    if (mx + r_ub <= 0.0 || mx - r_ub >= c.W || my + r_ub <= 0.0 || my - r_ub >= c.H) {
+      out.count[i] = 0;
+      reinterpret_cast<ushort4*>(out.rect)[i] = make_ushort4(0, 0, 0, 0);
+      if (out.sort_keys) out.sort_keys[i] = ~0ull;
+      if (out.cull) reinterpret_cast<CullRec*>(out.cull)[i].box = make_float4(0.f, 0.f, -1.0f, -1.0f);
+      return;
+    }
+  }
 
   // 3D covariance: Sigma = M M^T, M = R diag(s)   (project.py:91-94)
   double Rq[9], M[9], sig[9];
