@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(BW_THREADS, 4) blend_backward_kernel(
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, const double* __restrict__ final_t, const int32_t* __restrict__ last_idx,
     const float* __restrict__ grad_color, const float* __restrict__ grad_t, double* __restrict__ screen,
-    float* __restrict__ mesh_grad, int accumulate_mesh) {
+    float* __restrict__ mesh_grad, int accumulate_mesh, const int64_t* __restrict__ counters) {
+  if (counters && counters[2]) return;  // overflowed bins: no valid forward to differentiate
   extern __shared__ __align__(128) unsigned char bw_smem_raw[];
   BwSmem& sm = *reinterpret_cast<BwSmem*>(bw_smem_raw);
   const int tile = blockIdx.x;
@@ -575,7 +576,7 @@ extern "C" int hgs_blend_backward(const hgs_projected* proj, const hgs_tiles* ti
   blend_backward_kernel<<<n_tiles, BW_THREADS, smem, (cudaStream_t)stream>>>(
       (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
       width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], final_t, last, grad_color, grad_t, screen_grads,
-      mesh_color_grad, accumulate_mesh);
+      mesh_color_grad, accumulate_mesh, tiles->counters);
   HGS_CHECK_LAUNCH();
   return HGS_OK;
 }

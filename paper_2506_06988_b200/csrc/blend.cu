@@ -210,7 +210,9 @@ template <bool STATS>
 __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
     const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
-    double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup) {
+    double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
+    const int64_t* __restrict__ counters) {
+  if (counters && counters[2]) return;  // entry buffer overflowed: bins are invalid, the caller re-renders
   extern __shared__ __align__(128) unsigned char fast_smem_raw[];
   FastSmem& sm = *reinterpret_cast<FastSmem*>(fast_smem_raw);
   const int tile = blockIdx.x;
@@ -453,7 +455,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
 __global__ void __launch_bounds__(256) blend_exact_kernel(
     const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
     int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
-    double mask_k, hgs_blend_out out, const int32_t* __restrict__ fixup) {
+    double mask_k, hgs_blend_out out, const int32_t* __restrict__ fixup, const int64_t* __restrict__ counters) {
+  if (counters && counters[2]) return;  // overflowed bins (see blend_fast_kernel)
   const int64_t count = fixup ? fixup[0] : (int64_t)width * height;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -506,23 +509,23 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     if (out->stats)
       blend_fast_kernel<true><<<n_tiles, FAST_THREADS, smem, st>>>(
           (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
-          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
+          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
     else
       blend_fast_kernel<false><<<n_tiles, FAST_THREADS, smem, st>>>(
           (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
-          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup);
+          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
     HGS_CHECK_LAUNCH();
     // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)
     blend_exact_kernel<<<2 * NUM_SMS, 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,
                                                     tiles->tile_starts, tiles->tiles_x, width, height, ml,
                                                     bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
-                                                    mask_k, *out, out->fixup);
+                                                    mask_k, *out, out->fixup, tiles->counters);
     HGS_CHECK_LAUNCH();
   } else {
     blend_exact_kernel<<<ceil_div(npix * 32, 256), 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,
                                                             tiles->tile_starts, tiles->tiles_x, width, height, ml,
                                                             bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
-                                                            mask_k, *out, nullptr);
+                                                            mask_k, *out, nullptr, tiles->counters);
     HGS_CHECK_LAUNCH();
   }
   return HGS_OK;

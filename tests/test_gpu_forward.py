@@ -210,3 +210,26 @@ def test_large_grid_bins_and_blend_match_oracle(wh, n, cuda_device):
     assert np.array_equal(np_(ctx.last_consumed), last)
     assert_close(np_(out.color), color, atol=1e-5, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+
+
+def test_engine_entry_overflow_grows_and_rerenders(cuda_device):
+    """An entry buffer far below K: the overflowed pass must not touch memory
+    past the buffer (binning, blend and backward all skip on counters[2]);
+    frame(sync_check=True) grows it and the re-rendered frame equals the
+    functional render bit for bit."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    from paper_2506_06988_b200 import synthetic as syn
+    from paper_2506_06988_b200.engine import HybridRenderer
+    sc = syn.make_config("c2", seed=0)
+    g, c, m = dev_scene(sc.gaussians, sc.cameras[0], sc.mesh)
+    r = HybridRenderer(g, m, c.width, c.height, capacity=2048)
+    r.set_camera(c)
+    r.enqueue()
+    _, k, ovf = r.check()
+    assert ovf and r.capacity > k  # grown
+    r.frame(c, sync_check=True)
+    _, k2, ovf2 = r.check()
+    assert not ovf2 and k2 == k
+    out, _ = hgs.render(g, c, background=(0, 0, 0), mesh=mr.mesh_layer(m, c))
+    assert torch.equal(r.color, out.color) and torch.equal(r.trans, out.transmittance)
