@@ -13,7 +13,7 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhgs.so")
+LIB_PATH = os.environ.get("HGS_LIB") or os.path.join(_HERE, "libhgs.so")  # HGS_LIB: A/B builds (tools/)
 CSRC = os.path.join(_HERE, "csrc")
 
 HGS_OK = 0

@@ -23,8 +23,14 @@
 
 namespace hgs {
 
-constexpr int BW_BATCH = 64;
-constexpr int BW_NSTAGE = 6;
+#ifndef HGS_BW_BATCH
+#define HGS_BW_BATCH 64
+#endif
+#ifndef HGS_BW_NSTAGE
+#define HGS_BW_NSTAGE 6
+#endif
+constexpr int BW_BATCH = HGS_BW_BATCH;
+constexpr int BW_NSTAGE = HGS_BW_NSTAGE;
 constexpr int BW_CONSUMERS = 4;  // 8x8-pixel sub-tiles, two pixels per lane
 constexpr int BW_THREADS = (BW_CONSUMERS + 1) * 32;
 constexpr float CLAMP_BAND_INV = 1.0f / (2.0f * EPS_SIG * CLAMP_F);

@@ -36,8 +36,17 @@ namespace hgs {
 constexpr int BLEND_TILE = 16;
 constexpr int BLEND_THREADS = BLEND_TILE * BLEND_TILE;
 
-constexpr int BATCH = 128;
-constexpr int NSTAGE = 4;
+#ifndef HGS_FAST_BATCH
+#define HGS_FAST_BATCH 128
+#endif
+#ifndef HGS_FAST_NSTAGE
+#define HGS_FAST_NSTAGE 2
+#endif
+#ifndef HGS_FAST_MINB
+#define HGS_FAST_MINB 4
+#endif
+constexpr int BATCH = HGS_FAST_BATCH;
+constexpr int NSTAGE = HGS_FAST_NSTAGE;
 constexpr int CONSUMERS = 8;
 constexpr int FAST_THREADS = (CONSUMERS + 1) * 32;
 
@@ -207,7 +216,7 @@ __device__ __noinline__ ExactPixel exact_walk(const BlendRec* __restrict__ rec, 
 }
 
 template <bool STATS>
-__global__ void __launch_bounds__(FAST_THREADS, 3) blend_fast_kernel(
+__global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel(
     const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
@@ -504,6 +513,8 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     if (!attr) {
       cudaFuncSetAttribute(blend_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(blend_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(blend_fast_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(blend_fast_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       attr = true;
     }
     if (out->stats)
