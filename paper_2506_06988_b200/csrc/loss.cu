@@ -2,8 +2,10 @@
 // transmittance_mask (:79-91), L1 (:41-44), SSIM / D-SSIM (:47-76, 11-tap
 // sigma 1.5 zero-padded separable filter, scipy convolve1d along H then W),
 // texture loss (:103-116) and the composite schedule (:139-174).  All
-// reductions stay on the device (fp64 atomics); intermediate SSIM maps are
-// fp64.  Images are (H, W, 3) fp32 row-major.
+// reductions stay on the device (fp64 atomics); the SSIM filter arithmetic is
+// fp64 (B200 issues fp64 FMA at half the fp32 rate), the per-pixel SSIM
+// derivative maps handed from the forward to the backward tile are fp32.
+// Images are (H, W, 3) fp32 row-major.
 #include "common.cuh"
 
 namespace hgs {
@@ -33,111 +35,6 @@ __global__ void mask_kernel(const float* __restrict__ t, int64_t n, double k, in
   if (i < n) out[i] = (float)mask_val((double)t[i], k, variant);
 }
 
-template <int NV>
-__device__ __forceinline__ void block_sum_atomic(double (&v)[NV], double* dst) {
-  __shared__ double s[NV][8];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int c = 0; c < NV; c++) {
-    double x = v[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s[c][warp] = x;
-  }
-  __syncthreads();
-  if (threadIdx.x < NV) {
-    double x = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) x += s[threadIdx.x][w];
-    atomicAdd(&dst[threadIdx.x], x);
-  }
-}
-
-// Separable 11-tap zero-padded filter of NQ quantities along H (pass 0) or W
-// (pass 1).  Pass 0 inputs are built from x, y (q = x, y, x*x, y*y, x*y) when
-// from_images, else read from `in` (NQ fp64 maps).
-template <int NQ, bool FROM_IMAGES>
-__global__ void __launch_bounds__(256) ssim_filter_kernel(const float* __restrict__ x, const float* __restrict__ y,
-                                                          const double* __restrict__ in, double* __restrict__ out,
-                                                          int h, int w, int axis, LossWin win) {
-  const int64_t n = (int64_t)h * w * 3;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int ch = (int)(i % 3);
-  const int64_t pix = i / 3;
-  const int px = (int)(pix % w), py = (int)(pix / w);
-  double acc[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; q++) acc[q] = 0.0;
-  for (int k = -5; k <= 5; k++) {
-    const int yy = axis == 0 ? py + k : py, xx = axis == 0 ? px : px + k;
-    if (yy < 0 || yy >= h || xx < 0 || xx >= w) continue;
-    const int64_t j = ((int64_t)yy * w + xx) * 3 + ch;
-    const double wk = win.w[k + 5];
-    if (FROM_IMAGES) {
-      const double a = x[j], b = y[j];
-      acc[0] += a * wk;
-      acc[1] += b * wk;
-      acc[2] += (a * a) * wk;
-      acc[3] += (b * b) * wk;
-      acc[4] += (a * b) * wk;
-    } else {
-#pragma unroll
-      for (int q = 0; q < NQ; q++) acc[q] += in[(size_t)q * n + j] * wk;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; q++) out[(size_t)q * n + i] = acc[q];
-}
-
-// per-element SSIM terms (losses.py:57-66) -> ds_dux, ds_dvx, ds_dvxy maps and
-// sum(s); scalars[6] += sum(s)
-__global__ void __launch_bounds__(256) ssim_terms_kernel(const double* __restrict__ u, double* __restrict__ d,
-                                                         int64_t n, double* __restrict__ acc) {
-  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double v[1] = {0.0};
-  if (i < n) {
-    const double ux = u[i], uy = u[n + i], vx = u[2 * n + i], vy = u[3 * n + i], vxy = u[4 * n + i];
-    const double a1 = 2 * ux * uy + C1;
-    const double a2 = 2 * (vxy - ux * uy) + C2;
-    const double b1 = ux * ux + uy * uy + C1;
-    const double b2 = (vx - ux * ux) + (vy - uy * uy) + C2;
-    const double q = b1 * b2;
-    const double s = (a1 * a2) / q;
-    d[i] = 2 * uy * (a2 - a1) / q - 2 * ux * s / b1 + 2 * ux * s / b2;
-    d[n + i] = -s / b2;
-    d[2 * n + i] = 2 * a1 / q;
-    v[0] = s;
-  }
-  block_sum_atomic<1>(v, acc);
-}
-
-// L1 + texture-loss sums: acc[0] sum|d|, acc[1] covered count, acc[2]
-// sum(mask * sq) over covered, acc[3] sum T over covered
-__global__ void __launch_bounds__(256) loss_sums_kernel(const float* __restrict__ gt, const float* __restrict__ ih,
-                                                        const float* __restrict__ im, const int32_t* __restrict__ tri,
-                                                        const float* __restrict__ t, int64_t npix, double mask_k,
-                                                        int variant, int tex_active, double* __restrict__ acc) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  if (p < npix) {
-    for (int c = 0; c < 3; c++) v[0] += fabs((double)ih[3 * p + c] - (double)gt[3 * p + c]);
-    if (tri && tri[p] >= 0) {
-      v[1] = 1.0;
-      v[3] = t[p];
-      if (tex_active) {
-        double sq = 0.0;
-        for (int c = 0; c < 3; c++) {
-          const double dd = (double)im[3 * p + c] - (double)gt[3 * p + c];
-          sq += dd * dd;
-        }
-        v[2] = mask_val((double)t[p], mask_k, variant) * sq;
-      }
-    }
-  }
-  block_sum_atomic<4>(v, acc);
-}
-
 // scalars: l1, dssim, l_c, l_t, total, mean_T_on_mesh (acc: 0 sum|d|, 1 n_cov,
 // 2 sum(mask sq), 3 sum T cov, 6 sum s)
 __global__ void loss_scalars_kernel(const double* __restrict__ acc, int64_t n, double lam, int tex_active,
@@ -156,158 +53,200 @@ __global__ void loss_scalars_kernel(const double* __restrict__ acc, int64_t n, d
   scalars[5] = (has_mesh && ncov > 0) ? acc[3] / ncov : __longlong_as_double(0x7ff8000000000000LL);
 }
 
-// gradients: grad_ih = (1-lam) sign(d)/n + lam * (-0.5) * (f1 + 2x f2 + y f3)/n,
-// grad_im = tex_w (2/ncov) mask diff, grad_t = tex_w mask' sq / ncov
-__global__ void __launch_bounds__(256) loss_grads_kernel(const float* __restrict__ gt, const float* __restrict__ ih,
-                                                         const float* __restrict__ im, const int32_t* __restrict__ tri,
-                                                         const float* __restrict__ t, const double* __restrict__ f,
-                                                         const double* __restrict__ acc, int64_t npix, double lam,
-                                                         int tex_active, double tex_w, double mask_k, int variant,
-                                                         double scale, float* __restrict__ g_ih,
-                                                         float* __restrict__ g_im, float* __restrict__ g_t) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npix) return;
-  const int64_t n = npix * 3;
-  const double ncov = acc[1];
-  const bool cov = tri && tri[p] >= 0;
-  const double mk = (tex_active && cov) ? mask_val((double)t[p], mask_k, variant) : 0.0;
-  double sq = 0.0;
-  for (int c = 0; c < 3; c++) {
-    const int64_t i = 3 * p + c;
-    const double x = ih[i], y = gt[i];
-    const double d = x - y;
-    const double gl1 = (d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0)) / (double)n;
-    const double gss = (f[i] + 2 * x * f[n + i] + y * f[2 * n + i]) / (double)n;
-    g_ih[i] = (float)(scale * ((1.0 - lam) * gl1 + lam * (-0.5 * gss)));
-    if (g_im) {
-      const double dm = cov ? (double)im[i] - y : 0.0;
-      sq += dm * dm;
-      g_im[i] = (float)(scale * ((tex_active && ncov > 0) ? tex_w * ((2.0 / ncov) * mk * dm) : 0.0));
-    }
+
+// ---- fused SSIM tiles ------------------------------------------------------
+// One CTA (256 threads) per 16x16 output tile, all three channels.  The tile
+// plus a 5-pixel halo of the inputs is staged once in shared memory with
+// coalesced loads of the interleaved RGB rows (zeros outside the image = the
+// reference's zero padding: an fma with a zero operand leaves the sum
+// exactly unchanged, so no tap needs a bounds test).  The separable filter
+// is register-blocked: in the H pass a thread slides down one halo column
+// producing 5-6 outputs (each input row is read, squared and multiplied
+// once, not once per tap); in the W pass a thread slides along one row
+// producing 3-4 outputs.  Every output is still the taps k = -5..5 summed in
+// order with fma (the reference's convolve1d order, 1 ulp per tap).  Shared
+// rows of the H-filtered maps are padded to 27 doubles so the W pass (lanes
+// = rows) is bank-conflict free.
+constexpr int SS_T = 16, SS_H = SS_T + 10, SS_P = SS_H + 1;
+
+struct SsimFwdSmem {
+  union {
+    float in[2][3][SS_H][SS_H];      // [render, target][channel][row][col]
+    float dout[3][SS_T][SS_T * 3];   // staged derivative maps [map][row][px*3+ch]
+  };
+  double v[3][5][SS_T][SS_P];        // H-filtered (x, y, xx, yy, xy) [ch][q][row][col]
+};
+
+// Stage NA interleaved-RGB (or derivative-map) sources over the halo'd tile:
+// all of a thread's loads are issued before its shared stores (8 in flight
+// per source), rows are contiguous 78-float runs of global memory.
+template <int NA>
+__device__ __forceinline__ void ssim_stage(float (*dst)[3][SS_H][SS_H], const float* __restrict__ s0,
+                                           const float* __restrict__ s1, const float* __restrict__ s2, int x0, int y0,
+                                           int h, int w) {
+  constexpr int E = SS_H * SS_H * 3, IT = (E + 255) / 256;
+  const float* src[3] = {s0, s1, s2};
+  float v[NA][IT];
+#pragma unroll
+  for (int j = 0; j < IT; j++) {
+    const int i = threadIdx.x + 256 * j;
+    const int r = i / (SS_H * 3), k = i - r * (SS_H * 3);
+    const int gx = x0 + k / 3, gy = y0 + r;
+    const bool ok = i < E && gx >= 0 && gx < w && gy >= 0 && gy < h;
+    const int64_t jj = ok ? ((int64_t)gy * w + x0) * 3 + k : 0;
+#pragma unroll
+    for (int q = 0; q < NA; q++) v[q][j] = ok ? __ldg(src[q] + jj) : 0.f;
   }
-  if (g_t) {
-    double gtv = 0.0;
-    if (tex_active && cov && ncov > 0) gtv = tex_w * (mask_der((double)t[p], mask_k, variant) * sq / ncov);
-    g_t[p] = (float)(scale * gtv);
+#pragma unroll
+  for (int j = 0; j < IT; j++) {
+    const int i = threadIdx.x + 256 * j;
+    if (i < E) {
+      const int r = i / (SS_H * 3), k = i - r * (SS_H * 3);
+      const int cc = k / 3, ch = k - cc * 3;
+#pragma unroll
+      for (int q = 0; q < NA; q++) dst[q][ch][r][cc] = v[q][j];
+    }
   }
 }
 
-// ---- fused tiles ---------------------------------------------------------
-// One CTA per SS_T x SS_T output tile, all three channels.  The tile plus a
-// 5-pixel halo of the inputs is staged in shared memory (zeros outside the
-// image = the reference's zero padding), the H pass runs over the halo
-// columns into shared memory, the W pass produces the output tile: the same
-// per-element arithmetic and summation order as the separate passes, with
-// no fp64 map through HBM.
-constexpr int SS_T = 16, SS_H = SS_T + 10;
-
-struct SsimFwdSmem {
-  float x[SS_H][SS_H];
-  float y[SS_H][SS_H];
-  double v[SS_T][SS_H][5];  // H-filtered quantities of one channel over the halo columns
-};
-
-// SSIM terms (losses.py:57-66) -> d maps, sum(s) -> acc[6]; plus the L1 /
-// texture sums of loss_sums_kernel over the tile's pixels.  Channels one at
-// a time (small shared footprint: many CTAs per SM hide the loads).
-__global__ void __launch_bounds__(256) ssim_fwd_tile_kernel(const float* __restrict__ gt, const float* __restrict__ ih,
-                                                            const float* __restrict__ im,
-                                                            const int32_t* __restrict__ tri, const float* __restrict__ t,
-                                                            int h, int w, LossWin win, double mask_k, int variant,
-                                                            int tex_active, double* __restrict__ d,
-                                                            double* __restrict__ acc) {
-  __shared__ SsimFwdSmem sm;
+// SSIM terms (losses.py:57-66) -> derivative maps d (fp32, 3 planes of n),
+// sum(s) -> acc[6]; plus the L1 / coverage / texture sums over the tile's
+// pixels (acc[0..3]).
+__global__ void __launch_bounds__(256, 3) ssim_fwd_tile_kernel(const float* __restrict__ gt,
+                                                               const float* __restrict__ ih,
+                                                               const float* __restrict__ im,
+                                                               const int32_t* __restrict__ tri,
+                                                               const float* __restrict__ t, int h, int w, LossWin win,
+                                                               double mask_k, int variant, int tex_active,
+                                                               float* __restrict__ d, double* __restrict__ acc) {
+  extern __shared__ __align__(16) unsigned char ssf_raw[];
+  SsimFwdSmem& sm = *reinterpret_cast<SsimFwdSmem*>(ssf_raw);
   const int x0 = blockIdx.x * SS_T - 5, y0 = blockIdx.y * SS_T - 5;
   const int64_t n = (int64_t)h * w * 3;
   const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  // this thread's pixel for the L1 / coverage / texture sums: its loads are
+  // in flight during the staging
+  const int pr = threadIdx.x / SS_T, pc = threadIdx.x % SS_T;  // 256 threads = the tile's pixels
+  const int pgx = x0 + 5 + pc, pgy = y0 + 5 + pr;
+  const bool pin = pgx < w && pgy < h;
+  const int64_t p = pin ? (int64_t)pgy * w + pgx : 0;
+  const bool pcov = pin && tri && tri[p] >= 0;
+  const float pt = pcov ? t[p] : 0.f;
+  float pim[3] = {0.f, 0.f, 0.f};
+  if (pcov && tex_active)
+    for (int ch = 0; ch < 3; ch++) pim[ch] = im[3 * p + ch];
+  ssim_stage<2>(sm.in, ih, gt, nullptr, x0, y0, h, w);
+  __syncthreads();
+  double v4[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (pin) {
+    for (int ch = 0; ch < 3; ch++)
+      v4[0] += fabs((double)sm.in[0][ch][pr + 5][pc + 5] - (double)sm.in[1][ch][pr + 5][pc + 5]);
+    if (pcov) {
+      v4[1] = 1.0;
+      v4[3] = pt;
+      if (tex_active) {
+        double sq = 0.0;
+        for (int ch = 0; ch < 3; ch++) {
+          const double dd = (double)pim[ch] - (double)sm.in[1][ch][pr + 5][pc + 5];
+          sq += dd * dd;
+        }
+        v4[2] = mask_val((double)pt, mask_k, variant) * sq;
+      }
+    }
+  }
+  // H pass: item = (halo column, channel, row group of 5/5/6 output rows)
+  if (threadIdx.x < SS_H * 3 * 3) {
+    const int c = threadIdx.x % SS_H, rest = threadIdx.x / SS_H;
+    const int ch = rest % 3, g = rest / 3;
+    const int r0 = g * 5, nr = g == 2 ? 6 : 5;
+    double q[6][5];
+#pragma unroll
+    for (int o = 0; o < 6; o++)
+#pragma unroll
+      for (int k = 0; k < 5; k++) q[o][k] = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < 16; ii++) {
+      if (ii < nr + 10) {
+        const double a = sm.in[0][ch][r0 + ii][c], b = sm.in[1][ch][r0 + ii][c];
+        const double f[5] = {a, b, a * a, b * b, a * b};
+#pragma unroll
+        for (int o = 0; o < 6; o++) {
+          const int k = ii - o;
+          if (k >= 0 && k <= 10) {
+            const double wk = win.w[k];
+#pragma unroll
+            for (int m = 0; m < 5; m++) q[o][m] = fma(f[m], wk, q[o][m]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 6; o++)
+      if (o < nr)
+#pragma unroll
+        for (int m = 0; m < 5; m++) sm.v[ch][m][r0 + o][c] = q[o][m];
+  }
+  __syncthreads();
+  // W pass + SSIM terms: item = (row, channel, column group of 3/3/3/3/4)
   double ssum = 0.0;
-  for (int ch = 0; ch < 3; ch++) {
-    for (int i = threadIdx.x; i < SS_H * SS_H; i += blockDim.x) {
-      const int c = i % SS_H, r = i / SS_H;
-      const int gx = x0 + c, gy = y0 + r;
-      float a = 0.f, b = 0.f;
-      if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
-        const int64_t j = ((int64_t)gy * w + gx) * 3 + ch;
-        a = ih[j];
-        b = gt[j];
-      }
-      sm.x[r][c] = a;
-      sm.y[r][c] = b;
-    }
-    __syncthreads();
-    // pass along H (axis 0) for the tile's rows, all halo columns
-    for (int i = threadIdx.x; i < SS_T * SS_H; i += blockDim.x) {
-      const int c = i % SS_H, r = i / SS_H;
-      double q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      const int gx = x0 + c;
-      if (gx >= 0 && gx < w) {
-        for (int k = -5; k <= 5; k++) {
-          const int rr = r + 5 + k, gy = y0 + rr;
-          if (gy < 0 || gy >= h) continue;  // skipped taps (zero padding)
-          const double wk = win.w[k + 5];
-          const double a = sm.x[rr][c], b = sm.y[rr][c];
-          q[0] = fma(a, wk, q[0]);  // fused taps: within 1 ulp per tap of the reference's order
-          q[1] = fma(b, wk, q[1]);
-          q[2] = fma(a * a, wk, q[2]);
-          q[3] = fma(b * b, wk, q[3]);
-          q[4] = fma(a * b, wk, q[4]);
+  if (threadIdx.x < SS_T * 3 * 5) {
+    const int r = threadIdx.x % SS_T, rest = threadIdx.x / SS_T;
+    const int ch = rest % 3, g = rest / 3;
+    const int c0 = g * 3, nc = g == 4 ? 4 : 3;
+    double u[4][5];
+#pragma unroll
+    for (int o = 0; o < 4; o++)
+#pragma unroll
+      for (int k = 0; k < 5; k++) u[o][k] = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < 14; ii++) {
+      if (ii < nc + 10) {
+        double f[5];
+#pragma unroll
+        for (int m = 0; m < 5; m++) f[m] = sm.v[ch][m][r][c0 + ii];
+#pragma unroll
+        for (int o = 0; o < 4; o++) {
+          const int k = ii - o;
+          if (k >= 0 && k <= 10) {
+            const double wk = win.w[k];
+#pragma unroll
+            for (int m = 0; m < 5; m++) u[o][m] = fma(f[m], wk, u[o][m]);
+          }
         }
       }
-#pragma unroll
-      for (int k = 0; k < 5; k++) sm.v[r][c][k] = q[k];
     }
-    __syncthreads();
-    // pass along W (axis 1), SSIM terms: one pixel per thread
-    {
-      const int c = threadIdx.x % SS_T, r = threadIdx.x / SS_T;
-      const int gx = x0 + 5 + c, gy = y0 + 5 + r;
-      if (gx < w && gy < h) {
-        double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int k = -5; k <= 5; k++) {
-          const int cc = c + 5 + k, gxx = x0 + cc;
-          if (gxx < 0 || gxx >= w) continue;
-          const double wk = win.w[k + 5];
+    const int gy = y0 + 5 + r;
 #pragma unroll
-          for (int q = 0; q < 5; q++) u[q] = fma(sm.v[r][cc][q], wk, u[q]);
-        }
-        const double ux = u[0], uy = u[1], vx = u[2], vy = u[3], vxy = u[4];
+    for (int o = 0; o < 4; o++) {
+      const int gx = x0 + 5 + c0 + o;
+      if (o < nc && gx < w && gy < h) {
+        const double ux = u[o][0], uy = u[o][1], vx = u[o][2], vy = u[o][3], vxy = u[o][4];
         const double a1 = 2 * ux * uy + C1;
         const double a2 = 2 * (vxy - ux * uy) + C2;
         const double b1 = ux * ux + uy * uy + C1;
         const double b2 = (vx - ux * ux) + (vy - uy * uy) + C2;
-        const double qq = b1 * b2;
-        const double sv = (a1 * a2) / qq;
-        const int64_t j = ((int64_t)gy * w + gx) * 3 + ch;
-        d[j] = 2 * uy * (a2 - a1) / qq - 2 * ux * sv / b1 + 2 * ux * sv / b2;
-        d[n + j] = -sv / b2;
-        d[2 * n + j] = 2 * a1 / qq;
+        // two fp64 reciprocals instead of six divisions (1/qq = 1/b1 1/b2):
+        // a few ulp of fp64 from the reference's quotients
+        const double rb1 = 1.0 / b1, rb2 = 1.0 / b2;
+        const double rq = rb1 * rb2;
+        const double sv = (a1 * a2) * rq;
+        const int k = (c0 + o) * 3 + ch;
+        sm.dout[0][r][k] = (float)(2 * uy * (a2 - a1) * rq - 2 * ux * sv * rb1 + 2 * ux * sv * rb2);
+        sm.dout[1][r][k] = (float)(-sv * rb2);
+        sm.dout[2][r][k] = (float)(2 * a1 * rq);
         ssum += sv;
       }
     }
-    __syncthreads();
   }
-  // L1 / coverage / texture sums of the tile's pixels (loss_sums_kernel)
-  double v4[5] = {0.0, 0.0, 0.0, 0.0, ssum};
-  {
-    const int r = threadIdx.x / SS_T, c = threadIdx.x % SS_T;  // 256 threads = the tile's pixels
-    const int gx = x0 + 5 + c, gy = y0 + 5 + r;
-    if (gx < w && gy < h) {
-      const int64_t p = (int64_t)gy * w + gx;
-      for (int ch = 0; ch < 3; ch++) v4[0] += fabs((double)ih[3 * p + ch] - (double)gt[3 * p + ch]);
-      if (tri && tri[p] >= 0) {
-        v4[1] = 1.0;
-        v4[3] = t[p];
-        if (tex_active) {
-          double sq = 0.0;
-          for (int ch = 0; ch < 3; ch++) {
-            const double dd = (double)im[3 * p + ch] - (double)gt[3 * p + ch];
-            sq += dd * dd;
-          }
-          v4[2] = mask_val((double)t[p], mask_k, variant) * sq;
-        }
-      }
-    }
+  __syncthreads();
+  // coalesced write of the derivative maps (48 contiguous floats per row)
+  for (int i = threadIdx.x; i < 3 * SS_T * SS_T * 3; i += blockDim.x) {
+    const int m = i / (SS_T * SS_T * 3), rest = i - m * (SS_T * SS_T * 3);
+    const int r = rest / (SS_T * 3), k = rest - r * (SS_T * 3);
+    const int gy = y0 + 5 + r, gx = x0 + 5 + k / 3;
+    if (gx < w && gy < h) d[m * n + ((int64_t)gy * w + x0 + 5) * 3 + k] = sm.dout[m][r][k];
   }
+  v4[4] = ssum;
   __shared__ double red[5][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -326,91 +265,107 @@ __global__ void __launch_bounds__(256) ssim_fwd_tile_kernel(const float* __restr
 }
 
 struct SsimBwdSmem {
-  double d[SS_H][SS_H][3];
-  double v[SS_T][SS_H][3];
+  union {
+    float in[3][3][SS_H][SS_H];      // derivative maps [map][ch][row][col]
+    double f[9][SS_T][SS_T + 1];     // filtered [map*3+ch][row][col]
+  };
+  double v[9][SS_T][SS_P];           // H-filtered [map*3+ch][row][col]
 };
 
-// adjoint filter of the d maps (the window is symmetric) and the loss
-// gradients of loss_grads_kernel for the tile's pixels, channel by channel
-__global__ void __launch_bounds__(256) ssim_bwd_tile_kernel(const float* __restrict__ gt, const float* __restrict__ ih,
-                                                            const float* __restrict__ im,
-                                                            const int32_t* __restrict__ tri, const float* __restrict__ t,
-                                                            int h, int w, LossWin win, const double* __restrict__ d,
-                                                            const double* __restrict__ acc, double lam, int tex_active,
-                                                            double tex_w, double mask_k, int variant, double scale,
-                                                            float* __restrict__ g_ih, float* __restrict__ g_im,
-                                                            float* __restrict__ g_t) {
-  extern __shared__ __align__(16) unsigned char ss_raw[];
-  SsimBwdSmem& sm = *reinterpret_cast<SsimBwdSmem*>(ss_raw);
+// Adjoint filter of the d maps (the window is symmetric) and the loss
+// gradients (losses.py:41-76, 103-116): grad_ih = (1-lam) sign(d)/n +
+// lam (-0.5) (f1 + 2x f2 + y f3)/n, grad_im = tex_w (2/ncov) mask diff,
+// grad_t = tex_w mask' sq / ncov.
+__global__ void __launch_bounds__(256, 3) ssim_bwd_tile_kernel(const float* __restrict__ gt,
+                                                               const float* __restrict__ ih,
+                                                               const float* __restrict__ im,
+                                                               const int32_t* __restrict__ tri,
+                                                               const float* __restrict__ t, int h, int w, LossWin win,
+                                                               const float* __restrict__ d,
+                                                               const double* __restrict__ acc, double lam,
+                                                               int tex_active, double tex_w, double mask_k,
+                                                               int variant, double scale, float* __restrict__ g_ih,
+                                                               float* __restrict__ g_im, float* __restrict__ g_t) {
+  extern __shared__ __align__(16) unsigned char ssb_raw[];
+  SsimBwdSmem& sm = *reinterpret_cast<SsimBwdSmem*>(ssb_raw);
   const int x0 = blockIdx.x * SS_T - 5, y0 = blockIdx.y * SS_T - 5;
   const int64_t n = (int64_t)h * w * 3;
   const int r = threadIdx.x / SS_T, c = threadIdx.x % SS_T;  // output pixel of this thread
   const int gx = x0 + 5 + c, gy = y0 + 5 + r;
-  const bool inside = gx < w && gy < h;
-  const int64_t p = inside ? (int64_t)gy * w + gx : 0;
-  const double ncov = acc[1];
-  const bool cov = inside && tri && tri[p] >= 0;
-  const double mk = (tex_active && cov) ? mask_val((double)t[p], mask_k, variant) : 0.0;
-  double sq = 0.0;
-  for (int ch = 0; ch < 3; ch++) {
-    for (int i = threadIdx.x; i < SS_H * SS_H; i += blockDim.x) {
-      const int cc = i % SS_H, rr = i / SS_H;
-      const int gxx = x0 + cc, gyy = y0 + rr;
-      double a = 0.0, b = 0.0, e = 0.0;
-      if (gxx >= 0 && gxx < w && gyy >= 0 && gyy < h) {
-        const int64_t j = ((int64_t)gyy * w + gxx) * 3 + ch;
-        a = d[j];
-        b = d[n + j];
-        e = d[2 * n + j];
-      }
-      sm.d[rr][cc][0] = a;
-      sm.d[rr][cc][1] = b;
-      sm.d[rr][cc][2] = e;
+  const bool pin = gx < w && gy < h;
+  const int64_t p = pin ? (int64_t)gy * w + gx : 0;
+  // this pixel's inputs: in flight during the staging and the filter passes
+  float px_[3] = {0.f, 0.f, 0.f}, py_[3] = {0.f, 0.f, 0.f}, pim[3] = {0.f, 0.f, 0.f};
+  const bool cov = pin && tri && tri[p] >= 0;
+  const float pt = (pin && tex_active && cov) ? t[p] : 0.f;
+  if (pin)
+    for (int ch = 0; ch < 3; ch++) {
+      px_[ch] = ih[3 * p + ch];
+      py_[ch] = gt[3 * p + ch];
+      if (g_im && cov) pim[ch] = im[3 * p + ch];
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < SS_T * SS_H; i += blockDim.x) {
-      const int cc = i % SS_H, rr = i / SS_H;
-      double q[3] = {0.0, 0.0, 0.0};
-      const int gxx = x0 + cc;
-      if (gxx >= 0 && gxx < w) {
-        for (int k = -5; k <= 5; k++) {
-          const int r2 = rr + 5 + k, gyy = y0 + r2;
-          if (gyy < 0 || gyy >= h) continue;
-          const double wk = win.w[k + 5];
+  ssim_stage<3>(sm.in, d, d + n, d + 2 * n, x0, y0, h, w);
+  __syncthreads();
+  // H pass: item = (halo column, map x channel), the whole 16-row strip
+  if (threadIdx.x < SS_H * 9) {
+    const int c = threadIdx.x % SS_H, mc = threadIdx.x / SS_H;
+    double q[SS_T];
 #pragma unroll
-          for (int m = 0; m < 3; m++) q[m] = fma(sm.d[r2][cc][m], wk, q[m]);
-        }
-      }
+    for (int o = 0; o < SS_T; o++) q[o] = 0.0;
 #pragma unroll
-      for (int m = 0; m < 3; m++) sm.v[rr][cc][m] = q[m];
-    }
-    __syncthreads();
-    if (inside) {
-      double f[3] = {0.0, 0.0, 0.0};
-      for (int k = -5; k <= 5; k++) {
-        const int cc = c + 5 + k, gxx = x0 + cc;
-        if (gxx < 0 || gxx >= w) continue;
-        const double wk = win.w[k + 5];
+    for (int ii = 0; ii < SS_H; ii++) {
+      const double a = sm.in[mc / 3][mc % 3][ii][c];
 #pragma unroll
-        for (int m = 0; m < 3; m++) f[m] = fma(sm.v[r][cc][m], wk, f[m]);
-      }
-      const int64_t i = 3 * p + ch;
-      const double x = ih[i], y = gt[i];
-      const double dd = x - y;
-      const double gl1 = (dd > 0 ? 1.0 : (dd < 0 ? -1.0 : 0.0)) / (double)n;
-      const double gss = (f[0] + 2 * x * f[1] + y * f[2]) / (double)n;
-      g_ih[i] = (float)(scale * ((1.0 - lam) * gl1 + lam * (-0.5 * gss)));
-      if (g_im) {
-        const double dm = cov ? (double)im[i] - y : 0.0;
-        sq += dm * dm;
-        g_im[i] = (float)(scale * ((tex_active && ncov > 0) ? tex_w * ((2.0 / ncov) * mk * dm) : 0.0));
+      for (int o = 0; o < SS_T; o++) {
+        const int k = ii - o;
+        if (k >= 0 && k <= 10) q[o] = fma(a, win.w[k], q[o]);
       }
     }
-    __syncthreads();
+#pragma unroll
+    for (int o = 0; o < SS_T; o++) sm.v[mc][o][c] = q[o];
   }
-  if (inside && g_t) {
+  __syncthreads();
+  // W pass: item = (row, map x channel, half row of 8 outputs)
+  for (int it = threadIdx.x; it < SS_T * 9 * 2; it += blockDim.x) {
+    const int r = it % SS_T, rest = it / SS_T;
+    const int mc = rest % 9, c0 = (rest / 9) * 8;
+    double u[8];
+#pragma unroll
+    for (int o = 0; o < 8; o++) u[o] = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < 18; ii++) {
+      const double a = sm.v[mc][r][c0 + ii];
+#pragma unroll
+      for (int o = 0; o < 8; o++) {
+        const int k = ii - o;
+        if (k >= 0 && k <= 10) u[o] = fma(a, win.w[k], u[o]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 8; o++) sm.f[mc][r][c0 + o] = u[o];
+  }
+  __syncthreads();
+  if (!pin) return;
+  const double ncov = acc[1];
+  const double mk = (tex_active && cov) ? mask_val((double)pt, mask_k, variant) : 0.0;
+  double sq = 0.0;
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++) {
+    const int64_t i = 3 * p + ch;
+    const double x = px_[ch], y = py_[ch];
+    const double dd = x - y;
+    const double gl1 = (dd > 0 ? 1.0 : (dd < 0 ? -1.0 : 0.0)) / (double)n;
+    const double gss = (sm.f[ch][r][c] + 2 * x * sm.f[3 + ch][r][c] + y * sm.f[6 + ch][r][c]) / (double)n;
+    g_ih[i] = (float)(scale * ((1.0 - lam) * gl1 + lam * (-0.5 * gss)));
+    if (g_im) {
+      const double dm = cov ? (double)pim[ch] - y : 0.0;
+      sq += dm * dm;
+      g_im[i] = (float)(scale * ((tex_active && ncov > 0) ? tex_w * ((2.0 / ncov) * mk * dm) : 0.0));
+    }
+  }
+  if (g_t) {
     double gtv = 0.0;
-    if (tex_active && cov && ncov > 0) gtv = tex_w * (mask_der((double)t[p], mask_k, variant) * sq / ncov);
+    if (tex_active && cov && ncov > 0) gtv = tex_w * (mask_der((double)pt, mask_k, variant) * sq / ncov);
     g_t[p] = (float)(scale * gtv);
   }
 }
@@ -430,7 +385,7 @@ extern "C" int hgs_transmittance_mask(const float* t, int64_t n, double k, int32
 
 extern "C" size_t hgs_loss_scratch_bytes(int32_t height, int32_t width) {
   const size_t n = (size_t)height * width * 3;
-  return hgs::align_up(8 * 5 * n, 256) * 2 + hgs::align_up(8 * 3 * n, 256) + 256;
+  return hgs::align_up(4 * 3 * n, 256) + 256;
 }
 
 extern "C" int hgs_composite_loss(const float* i_gt, const float* i_h, const float* i_m, const int32_t* triangle_id,
@@ -450,24 +405,21 @@ extern "C" int hgs_composite_loss(const float* i_gt, const float* i_h, const flo
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t npix = (int64_t)height * width, n = npix * 3;
   unsigned char* base = (unsigned char*)scratch;
-  double* mapsA = (double*)base;  // 5 x n
-  base += align_up(8 * 5 * n, 256);
-  double* mapsB = (double*)base;  // 5 x n
-  base += align_up(8 * 5 * n, 256);
-  double* dmaps = (double*)base;  // 3 x n
-  base += align_up(8 * 3 * n, 256);
+  float* dmaps = (float*)base;  // 3 x n SSIM derivative maps
+  base += align_up(4 * 3 * n, 256);
   double* acc = (double*)base;  // 8 doubles
   LossWin win;
   for (int k = 0; k < 11; k++) win.w[k] = window11_host[k];
   cudaMemsetAsync(acc, 0, 8 * sizeof(double), st);
   static bool attr = false;
   if (!attr) {
+    cudaFuncSetAttribute(ssim_fwd_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SsimFwdSmem));
     cudaFuncSetAttribute(ssim_bwd_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SsimBwdSmem));
     attr = true;
   }
   const dim3 tg((width + SS_T - 1) / SS_T, (height + SS_T - 1) / SS_T);
-  ssim_fwd_tile_kernel<<<tg, 256, 0, st>>>(i_gt, i_h, i_m, triangle_id, t, height, width, win, mask_k,
-                                                             mask_variant, texture_active, dmaps, acc);
+  ssim_fwd_tile_kernel<<<tg, 256, sizeof(SsimFwdSmem), st>>>(i_gt, i_h, i_m, triangle_id, t, height, width, win,
+                                                             mask_k, mask_variant, texture_active, dmaps, acc);
   HGS_CHECK_LAUNCH();
   loss_scalars_kernel<<<1, 1, 0, st>>>(acc, n, lam_dssim, texture_active, texture_weight, triangle_id != nullptr,
                                        scalars);
@@ -476,7 +428,5 @@ extern "C" int hgs_composite_loss(const float* i_gt, const float* i_h, const flo
                                                              acc, lam_dssim, texture_active, texture_weight, mask_k,
                                                              mask_variant, grad_scale, grad_ih, grad_im, grad_t);
   HGS_CHECK_LAUNCH();
-  (void)mapsA;
-  (void)mapsB;
   return HGS_OK;
 }
