@@ -506,9 +506,15 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
 // accumulation) zeros for the invisible ones, then the visible ones -- a
 // few percent of them for a training view -- compacted in shared memory
 // so every thread runs the long fp64 chain on a visible Gaussian.
+#ifndef HGS_PB_ROWS
+#define HGS_PB_ROWS 8
+#endif
+#ifndef HGS_PB_MINB
+#define HGS_PB_MINB 4
+#endif
 constexpr int PB_THREADS = 128;
-constexpr int PB_SPAN = 32 * PB_THREADS;
-__global__ void __launch_bounds__(PB_THREADS) project_backward_kernel(const hgs_camera* __restrict__ cam_ptr,
+constexpr int PB_SPAN = HGS_PB_ROWS * PB_THREADS;
+__global__ void __launch_bounds__(PB_THREADS, HGS_PB_MINB) project_backward_kernel(const hgs_camera* __restrict__ cam_ptr,
                                                                       hgs_gaussians gs,
                                                                       const int32_t* __restrict__ count,
                                                                       const double* __restrict__ screen,
