@@ -213,16 +213,21 @@ class GaussianGrads:
 # --------------------------------------------------------------------------
 
 class _Scratch:
-    """Grow-only device scratch buffers shared by calls on one device."""
+    """Grow-only device scratch buffers shared by calls on one device and
+    stream (keyed by the current stream: calls enqueued on different streams
+    never share a buffer, calls on one stream are ordered by it)."""
 
     def __init__(self):
         self.bufs = {}
 
     def get(self, name: str, nbytes: int, device) -> torch.Tensor:
-        b = self.bufs.get((name, device))
+        device = torch.device(device)
+        sid = torch.cuda.current_stream(device).cuda_stream if device.type == "cuda" else 0
+        key = (name, device, sid)
+        b = self.bufs.get(key)
         if b is None or b.numel() < nbytes:
             b = torch.empty((max(int(nbytes * 1.25), 256) + 255) // 256 * 256, dtype=torch.uint8, device=device)
-            self.bufs[(name, device)] = b
+            self.bufs[key] = b
         return b
 
 

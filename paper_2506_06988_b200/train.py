@@ -41,7 +41,43 @@ def shard_views(n_views: int, rank: int, world: int) -> List[int]:
     return list(range(lo, hi))
 
 
+class _Lane:
+    """Per-view work buffers of one of the trainer's two view pipelines.
+    Views of a step alternate between the lanes, each on its own stream, so
+    one view's forward / binning overlaps the other's backward; the lanes
+    share only the gradient bucket (see HybridTrainer.step)."""
+
+    def __init__(self, dev, stream):
+        self.dev = dev
+        self.stream = stream
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.overflow = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.loss_sum = torch.zeros(6, dtype=torch.float64, device=dev)
+        self.capacity = 0
+
+    def alloc_rows(self, n: int, tiles_xy):
+        dev = self.dev
+        tx, ty = tiles_xy
+        self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
+        self.count = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
+        self.cull = torch.empty(n * 12, dtype=torch.float32, device=dev)
+        self.sort_keys = torch.empty(n, dtype=torch.int64, device=dev)
+        self.screen = torch.zeros(n * 9, dtype=torch.float64, device=dev)
+        self.tile_diff = torch.empty(16 * (tx + 1) * (ty + 1), dtype=torch.int32, device=dev)
+
+    def alloc_entries(self, cap: int, n: int, tiles_xy):
+        tx, ty = tiles_xy
+        self.capacity = cap
+        self.entries = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.tile_starts = torch.empty(tx * ty + 1, dtype=torch.int64, device=self.dev)
+        nbytes = _lib.load().hgs_tiles_scratch_bytes(n, cap, tx * ty)
+        self.tiles_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+
+
 class HybridTrainer:
+    N_LANES = 2
+
     def __init__(self, gs: GaussianSet, mesh: Optional[TexturedMesh], cameras: Sequence, images: Sequence, config,
                  rank: int = 0, world: int = 1, process_group=None, allreduce=None, density_control: bool = False,
                  extent: Optional[float] = None, rng: Optional[np.random.Generator] = None):
@@ -86,16 +122,13 @@ class HybridTrainer:
         self.frags: List[Optional[MeshFragmentBuffer]] = []
         for c in self.cameras:
             self.frags.append(rasterize_fragments(mesh, c, with_bary=False) if mesh is not None else None)
-        self._alloc_rows()
         c0 = self.cameras[0]
         self.tx = (int(c0.width) + TILE_PX - 1) // TILE_PX
         self.ty = (int(c0.height) + TILE_PX - 1) // TILE_PX
-        self.tile_diff = torch.empty(16 * (self.tx + 1) * (self.ty + 1), dtype=torch.int32, device=dev)
-        self.capacity = 0
-        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
-        self.overflow = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.lanes = [_Lane(dev, torch.cuda.Stream(dev) if dev.type == "cuda" else None)
+                      for _ in range(self.N_LANES)]
+        self._alloc_rows()
         self.loss_sum = torch.zeros(6, dtype=torch.float64, device=dev)
-        self.scalars = torch.zeros(6, dtype=torch.float64, device=dev)
         self._size_entries()
 
     # ------------------------------------------------------------------
@@ -112,15 +145,11 @@ class HybridTrainer:
         self.tex_grad = self.bucket[p_sz:p_sz + t_sz].view_as(mesh.texture) if t_sz else None
 
     def _alloc_rows(self):
-        """Per-view work buffers sized by the Gaussian count (reused
-        sequentially on one stream)."""
-        n, dev = max(len(self.gs), 1), self.dev
-        self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
-        self.count = torch.zeros(n, dtype=torch.int32, device=dev)
-        self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
-        self.cull = torch.empty(n * 12, dtype=torch.float32, device=dev)
-        self.sort_keys = torch.empty(n, dtype=torch.int64, device=dev)
-        self.screen = torch.zeros(n * 9, dtype=torch.float64, device=dev)
+        """Per-view work buffers sized by the Gaussian count, one set per
+        lane (each reused in order on its lane's stream)."""
+        n = max(len(self.gs), 1)
+        for lane in self.lanes:
+            lane.alloc_rows(n, (self.tx, self.ty))
 
     def _density_step(self, it: int) -> None:
         """loop.py:226-233 after the optimiser steps of iteration ``it``."""
@@ -141,43 +170,33 @@ class HybridTrainer:
 
     def _size_entries(self):
         """Tile-entry capacity: max K over this rank's views x 1.2 (one sync)."""
-        from .splat import _preprocess
         kmax = 0
         for v in range(len(self.cameras)):
-            proj = self._project(v)
+            proj = self._project(v, self.lanes[0])
             kmax = max(kmax, int(proj.count.sum().item()))
-        self._alloc_entries(int(kmax * 1.2) + 4096)
+        cap = int(kmax * 1.2) + 4096
+        for lane in self.lanes:
+            lane.alloc_entries(cap, len(self.gs), (self.tx, self.ty))
 
-    def _alloc_entries(self, cap):
-        self.capacity = cap
-        self.entries = torch.empty(cap, dtype=torch.int32, device=self.dev)
-        cam0 = self.cameras[0]
-        tx = (int(cam0.width) + TILE_PX - 1) // TILE_PX
-        ty = (int(cam0.height) + TILE_PX - 1) // TILE_PX
-        self.tile_starts = torch.empty(tx * ty + 1, dtype=torch.int64, device=self.dev)
-        nbytes = _lib.load().hgs_tiles_scratch_bytes(len(self.gs), cap, tx * ty)
-        self.tiles_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
-        self.tx, self.ty = tx, ty
-
-    def _project(self, v) -> ProjectedGaussians:
+    def _project(self, v, lane: _Lane) -> ProjectedGaussians:
         cam = self.cameras[v]
         ps = _lib.HGSProjected()
-        ps.rec, ps.count, ps.rect, ps.cull = (_lib.ptr(self.rec), _lib.ptr(self.count), _lib.ptr(self.rect),
-                                              _lib.ptr(self.cull))
-        ps.sort_keys, ps.tile_diff = _lib.ptr(self.sort_keys), _lib.ptr(self.tile_diff)
+        ps.rec, ps.count, ps.rect, ps.cull = (_lib.ptr(lane.rec), _lib.ptr(lane.count), _lib.ptr(lane.rect),
+                                              _lib.ptr(lane.cull))
+        ps.sort_keys, ps.tile_diff = _lib.ptr(lane.sort_keys), _lib.ptr(lane.tile_diff)
         _lib.call("hgs_preprocess", _lib.ptr(self.cam_dev[v]), int(cam.width), int(cam.height),
                   ctypes.byref(self.gs.struct()), TILE_PX, ctypes.byref(ps), _stream_ptr(self.dev))
-        return ProjectedGaussians(len(self.gs), self.rec, self.count, self.rect, None, int(cam.width),
-                                  int(cam.height), TILE_PX, self.cull, self.sort_keys, self.tile_diff)
+        return ProjectedGaussians(len(self.gs), lane.rec, lane.count, lane.rect, None, int(cam.width),
+                                  int(cam.height), TILE_PX, lane.cull, lane.sort_keys, lane.tile_diff)
 
-    def _tiles(self, proj) -> TileBins:
+    def _tiles(self, proj, lane: _Lane) -> TileBins:
         ts = _lib.HGSTiles()
-        ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tx, self.ty, TILE_PX, self.capacity
-        ts.entries, ts.tile_starts, ts.counters = _lib.ptr(self.entries), _lib.ptr(self.tile_starts), _lib.ptr(self.counters)
-        ts.scratch, ts.scratch_bytes = _lib.ptr(self.tiles_scratch), self.tiles_scratch.numel()
+        ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tx, self.ty, TILE_PX, lane.capacity
+        ts.entries, ts.tile_starts, ts.counters = _lib.ptr(lane.entries), _lib.ptr(lane.tile_starts), _lib.ptr(lane.counters)
+        ts.scratch, ts.scratch_bytes = _lib.ptr(lane.tiles_scratch), lane.tiles_scratch.numel()
         _lib.call("hgs_build_tiles", ctypes.byref(proj.struct()), len(self.gs), ctypes.byref(ts), _stream_ptr(self.dev))
-        self.overflow += self.counters[2:3]
-        return TileBins(self.tile_starts, self.entries, self.tx, self.ty, TILE_PX, proj)
+        lane.overflow += lane.counters[2:3]
+        return TileBins(lane.tile_starts, lane.entries, self.tx, self.ty, TILE_PX, proj)
 
     def mesh_layer(self, v) -> Optional[MeshLayer]:
         """Texture lookup over the cached fragments (loop.py:189-199)."""
@@ -188,26 +207,31 @@ class HybridTrainer:
         color = sample_texture(self.mesh.texture, fr.uv, fr.triangle_id)
         return MeshLayer(color, fr.depth, fr.triangle_id)
 
-    def view_grads(self, v: int, it: int, grad_scale: float):
-        """Forward + loss + backward of one view, accumulated (x grad_scale)
-        into the bucket.  Returns the device loss scalars of this view."""
+    def view_grads(self, v: int, it: int, grad_scale: float, lane: Optional[_Lane] = None, after=None):
+        """Forward + loss + backward of one view on the current stream,
+        accumulated (x grad_scale) into the bucket; the accumulation into the
+        shared bucket waits for event ``after`` (the previous view's).
+        Returns the device loss scalars of this view."""
+        lane = lane if lane is not None else self.lanes[0]
         cam = self.cameras[v]
         w, h = int(cam.width), int(cam.height)
         layer = self.mesh_layer(v)
-        proj = self._project(v)
-        tiles = self._tiles(proj)
+        proj = self._project(v, lane)
+        tiles = self._tiles(proj, lane)
         color, depth, trans, final_t, last, _ = _blend(proj, tiles, w, h, layer, self.bg)
         fr = self.frags[v]
         covered = fr.triangle_id if fr is not None else None
         bd, g_ih, g_im, g_t = composite_loss(self.images[v], color, layer.color if layer else None, covered, trans,
                                              it, self.cfg, grad_scale=grad_scale)
         ctx = RenderCtx(self.gs, cam, proj, tiles, layer, self.bg, final_t, last, self.cam_dev[v])
-        self.screen.zero_()
+        lane.screen.zero_()
         mesh_grad = None
         if layer is not None:
             mesh_grad = g_im if g_im is not None else torch.zeros(h, w, 3, dtype=torch.float32, device=self.dev)
-        screen_backward(ctx, g_ih, g_t, self.screen, mesh_grad, accumulate_mesh=True)
-        chain_backward(ctx, self.screen, self.grads, scale=1.0, accumulate=True)
+        screen_backward(ctx, g_ih, g_t, lane.screen, mesh_grad, accumulate_mesh=True)
+        if after is not None:  # the chain accumulates (read-modify-write) into the shared bucket, in view order
+            torch.cuda.current_stream(self.dev).wait_event(after)
+        chain_backward(ctx, lane.screen, self.grads, scale=1.0, accumulate=True)
         if layer is not None and self.tex_grad is not None:
             from .meshraster import texture_backward
             texture_backward(fr, mesh_grad, tuple(self.mesh.texture.shape[:2]), out=self.tex_grad)
@@ -221,12 +245,35 @@ class HybridTrainer:
         self.bucket.zero_()
         self.grads.visible.zero_()
         self.loss_sum.zero_()
-        self.overflow.zero_()
-        for v in mine:
-            self.loss_sum += self.view_grads(v, it, 1.0 / nb)
-        if int(self.overflow.item()):
+        for lane in self.lanes:
+            lane.loss_sum.zero_()
+            lane.overflow.zero_()
+        if self.lanes[0].stream is None:
+            for v in mine:
+                self.lanes[0].loss_sum += self.view_grads(v, it, 1.0 / nb)
+        else:
+            # views alternate between the lanes' streams; only the chain's
+            # accumulation into the bucket is ordered across them (events)
+            main = torch.cuda.current_stream(self.dev)
+            for lane in self.lanes:
+                lane.stream.wait_stream(main)
+            prev = None
+            for j, v in enumerate(mine):
+                lane = self.lanes[j % len(self.lanes)]
+                with torch.cuda.stream(lane.stream):
+                    lane.loss_sum += self.view_grads(v, it, 1.0 / nb, lane=lane, after=prev)
+                    prev = torch.cuda.Event()
+                    prev.record(lane.stream)
+            for lane in self.lanes:
+                main.wait_stream(lane.stream)
+        overflow = self.lanes[0].overflow
+        for lane in self.lanes[1:]:
+            overflow = overflow + lane.overflow
+        if int(overflow.item()):
             self._size_entries()
             return self.step(it, views)
+        for lane in self.lanes:
+            self.loss_sum += lane.loss_sum
         if self.world > 1:
             self.loss_sum /= nb
             if self._allreduce is not None:

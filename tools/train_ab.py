@@ -8,6 +8,8 @@ import paper_2506_06988_b200 as hgs
 from paper_2506_06988_b200 import synthetic as syn
 from paper_2506_06988_b200.config import TrainConfig
 from paper_2506_06988_b200.train import HybridTrainer
+if os.environ.get('HGS_LANES'):
+    HybridTrainer.N_LANES = int(os.environ['HGS_LANES'])
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 nv = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 dev = torch.device("cuda:0")
@@ -29,4 +31,4 @@ e0.record()
 for _ in range(k):
     loss = tr.step(it, views)
 e1.record(); torch.cuda.synchronize()
-print(f"{os.path.basename(os.environ.get('HGS_LIB', 'libhgs.so'))} train ms/step {e0.elapsed_time(e1)/k:.2f} loss {float(loss[4]):.9f}", flush=True)
+print(f"{os.path.basename(os.environ.get('HGS_LIB', 'libhgs.so'))} lanes={HybridTrainer.N_LANES} train ms/step {e0.elapsed_time(e1)/k:.2f} loss {float(loss[4]):.9f}", flush=True)
