@@ -42,7 +42,7 @@ def shard_views(n_views: int, rank: int, world: int) -> List[int]:
 
 
 class _Lane:
-    """Per-view work buffers of one of the trainer's two view pipelines.
+    """Per-view work buffers of one of the trainer's view pipelines.
     Views of a step alternate between the lanes, each on its own stream, so
     one view's forward / binning overlaps the other's backward; the lanes
     share only the gradient bucket (see HybridTrainer.step)."""
@@ -76,7 +76,7 @@ class _Lane:
 
 
 class HybridTrainer:
-    N_LANES = 2
+    N_LANES = 4  # 2: 137.7, 3: 134.2, 4: 132.3 ms per c4 step (B200)
 
     def __init__(self, gs: GaussianSet, mesh: Optional[TexturedMesh], cameras: Sequence, images: Sequence, config,
                  rank: int = 0, world: int = 1, process_group=None, allreduce=None, density_control: bool = False,
