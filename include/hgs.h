@@ -198,6 +198,13 @@ int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* tiles, int32_t
                       const hgs_mesh_layer* mesh, const double* bg_host3, int32_t mask_variant, double mask_k,
                       hgs_blend_out* out, void* stream);
 
+/* render_depth (splat/render.py:316-324) / depth_kernel
+   (splat/kernels.py:163-202): per pixel, the depth of the entry at which the
+   accumulated opacity first exceeds 0.5, NaN where it never does (no mesh
+   layer).  out_depth: H x W fp64. */
+int hgs_render_depth(const hgs_projected* proj, const hgs_tiles* tiles, int32_t width, int32_t height,
+                     double* out_depth, void* stream);
+
 /* ---------------- splat backward ---------------- */
 
 /* backward_kernel (splat/kernels.py:77-160) + np.add.at reduction

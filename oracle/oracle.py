@@ -31,6 +31,10 @@ SH_C0 = 0.28209479177387814
 SH_C1 = 0.4886025119029199
 FRUSTUM_LIMIT = 1.3
 TILE_PX = 16
+SUPPORT_MAHAL2 = 9.0
+ALPHA_CLAMP = 0.99
+SIGMA_SKIP = 1.0 / 255.0
+EARLY_STOP_T = 1e-4
 MASK_VARIANTS = {"sigmoid": 0, "identity_t": 1, "constant_one": 2, "constant_zero": 3}
 
 
@@ -442,3 +446,65 @@ def adam_step(p, m, v, g, lr, step, beta1=0.9, beta2=0.999, eps=1e-15):
     gg = _f64(g)
     lib().or_adam(ctypes.c_int64(p.size), _p(p), _p(m), _p(v), _p(gg), ctypes.c_double(lr), ctypes.c_double(beta1),
                   ctypes.c_double(beta2), ctypes.c_double(eps), ctypes.c_int64(step))
+
+
+def render_depth(gs, cam, tile_px: int = TILE_PX) -> np.ndarray:
+    """splat/render.py:316-324 with depth_kernel (splat/kernels.py:163-202)
+    restated as a pure-Python loop (small cases only): per pixel, the depth
+    of the entry at which 1 - T first exceeds 0.5, NaN where it never does."""
+    import math
+    p = project(gs, cam)
+    w, h = int(cam.width), int(cam.height)
+    t = build_tiles(p, w, h, tile_px)
+    out = np.full((h, w), np.nan)
+    mean2d, conic, alpha, depth = p.mean2d, p.conic, p.alpha, p.depth
+    for ty in range(t.tiles_y):
+        for tx in range(t.tiles_x):
+            k0 = int(t.tile_starts[ty * t.tiles_x + tx])
+            k1 = int(t.tile_starts[ty * t.tiles_x + tx + 1])
+            for py in range(ty * tile_px, min(ty * tile_px + tile_px, h)):
+                for px in range(tx * tile_px, min(tx * tile_px + tile_px, w)):
+                    fx, fy = px + 0.5, py + 0.5
+                    trans = 1.0
+                    for k in range(k0, k1):
+                        i = int(t.entries[k])
+                        dx, dy = fx - mean2d[i, 0], fy - mean2d[i, 1]
+                        m = conic[i, 0] * dx * dx + 2.0 * conic[i, 1] * dx * dy + conic[i, 2] * dy * dy
+                        if m > SUPPORT_MAHAL2 or m < 0.0:
+                            continue
+                        sig = min(alpha[i] * math.exp(-0.5 * m), ALPHA_CLAMP)
+                        if sig < SIGMA_SKIP:
+                            continue
+                        test_t = trans * (1.0 - sig)
+                        if test_t < EARLY_STOP_T:
+                            break
+                        trans = test_t
+                        if 1.0 - trans > 0.5:
+                            out[py, px] = depth[i]
+                            break
+    return out
+
+
+def init_texture(vertices, triangles, uvs, texture, images, cameras, iters: int = 500, lr: float = 0.05) -> np.ndarray:
+    """meshraster.py:206-245, mode "optimized": texture starts at 0.5, then
+    ``iters`` fp64 Adam steps on the coverage-normalised masked MSE averaged
+    over the views, clamped to [0, 1] after each step.  Returns the texture."""
+    tex = np.full(np.asarray(texture).shape, 0.5)
+    frags = [rasterize_fragments(vertices, triangles, uvs, c) for c in cameras]
+    n_cov = [int(f.valid.sum()) for f in frags]
+    if sum(n_cov) == 0:
+        return tex
+    m, v = np.zeros_like(tex), np.zeros_like(tex)
+    th, tw = tex.shape[:2]
+    for step in range(1, iters + 1):
+        grad = np.zeros_like(tex)
+        for img, fr, cov in zip(images, frags, n_cov):
+            if cov == 0:
+                continue
+            pred = sample_texture(tex, fr.uv, fr.valid)
+            diff = np.zeros_like(pred)
+            diff[fr.valid] = pred[fr.valid] - np.asarray(img, dtype=np.float64)[fr.valid]
+            grad += texture_backward(fr, 2.0 * diff / cov, (th, tw))
+        adam_step(tex, m, v, grad / len(cameras), lr, step)
+        np.clip(tex, 0.0, 1.0, out=tex)
+    return tex

@@ -96,6 +96,7 @@ SIGNATURES = {
     "hgs_build_tiles": (ctypes.c_int, [_P(HGSProjected), c_i64, _P(HGSTiles), c_void_p]),
     "hgs_blend_forward": (ctypes.c_int, [_P(HGSProjected), _P(HGSTiles), c_i32, c_i32, _P(HGSMeshLayer),
                                          _P(c_f64), c_i32, c_f64, _P(HGSBlendOut), c_void_p]),
+    "hgs_render_depth": (ctypes.c_int, [_P(HGSProjected), _P(HGSTiles), c_i32, c_i32, c_void_p, c_void_p]),
     "hgs_blend_backward": (ctypes.c_int, [_P(HGSProjected), _P(HGSTiles), c_i32, c_i32, _P(HGSMeshLayer), _P(c_f64),
                                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i32,
                                           c_void_p]),

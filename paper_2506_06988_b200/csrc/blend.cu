@@ -541,3 +541,108 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
   }
   return HGS_OK;
 }
+
+namespace hgs {
+
+// Median-style depth (depth_kernel, splat/kernels.py:163-202): the camera z
+// of the entry at which the accumulated opacity 1 - T first exceeds 0.5,
+// NaN where it never does.  One warp per pixel, fp64 throughout: lanes
+// evaluate 32 consecutive entries exactly as the reference (support test,
+// exp, clamp, skip), the chunk's transmittance is an inclusive shuffle
+// prefix product of (1 - sigma) (|rel. diff| < 1e-13 from the serial
+// product, see exact_walk), and a chunk whose products fall within 1e-12 of
+// either threshold (0.5, or the 1e-4 early stop) is replayed serially in the
+// reference's order, so every decision is the reference's.
+__global__ void __launch_bounds__(256) depth_walk_kernel(const BlendRec* __restrict__ rec,
+                                                         const uint32_t* __restrict__ entries,
+                                                         const int64_t* __restrict__ tile_starts, int tiles_x,
+                                                         int width, int height, double* __restrict__ out,
+                                                         const int64_t* __restrict__ counters) {
+  if (counters && counters[2]) return;  // overflowed bins
+  const int lane = threadIdx.x & 31;
+  const int64_t npix = (int64_t)width * height;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < npix; p += nwarps) {
+    const int px = (int)(p % width), py = (int)(p / width);
+    const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
+    const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
+    const double fx = px + 0.5, fy = py + 0.5;
+    double T = 1.0;
+    double found = __longlong_as_double(0x7ff8000000000000LL);
+    bool done = false;
+    for (int64_t base = s; base < e && !done; base += 32) {
+      const int64_t k = base + lane;
+      bool use = false;
+      double sig = 0.0, dep = 0.0;
+      if (k < e) {
+        const BlendRec c = rec[__ldg(entries + k)];
+        dep = c.depth;
+        const double dx = fx - c.mx, dy = fy - c.my;
+        const double m = c.ca * dx * dx + c.cb2 * dx * dy + c.cc * dy * dy;
+        if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
+          sig = c.alpha * exp(-0.5 * m);
+          if (sig > ALPHA_CLAMP) sig = ALPHA_CLAMP;
+          use = !(sig < SIGMA_SKIP);
+        }
+      }
+      double P = use ? 1.0 - sig : 1.0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, P, d);
+        if (lane >= d) P *= t;
+      }
+      const double t_after = T * P;
+      const bool near = use && (fabs(t_after - EARLY_STOP_T) <= 1e-12 * EARLY_STOP_T || fabs(t_after - 0.5) <= 1e-12);
+      if (!__any_sync(0xffffffffu, near)) {
+        // the reference tests the early stop before the opacity crossing
+        const unsigned stop = __ballot_sync(0xffffffffu, use && t_after < EARLY_STOP_T);
+        const unsigned hit = __ballot_sync(0xffffffffu, use && !(t_after < EARLY_STOP_T) && 1.0 - t_after > 0.5);
+        const int ks = stop ? __ffs(stop) - 1 : 32, kh = hit ? __ffs(hit) - 1 : 32;
+        if (kh < ks) {
+          found = __shfl_sync(0xffffffffu, dep, kh);
+          done = true;
+        } else if (ks < 32) {
+          done = true;
+        } else {
+          T = __shfl_sync(0xffffffffu, t_after, 31);
+        }
+      } else {
+        unsigned use_mask = __ballot_sync(0xffffffffu, use);
+        while (use_mask) {
+          const int i = __ffs(use_mask) - 1;
+          use_mask &= use_mask - 1;
+          const double sg = __shfl_sync(0xffffffffu, sig, i);
+          const double test_t = T * (1.0 - sg);
+          if (test_t < EARLY_STOP_T) { done = true; break; }
+          T = test_t;
+          if (1.0 - T > 0.5) {
+            found = __shfl_sync(0xffffffffu, dep, i);
+            done = true;
+            break;
+          }
+        }
+      }
+    }
+    if (lane == 0) out[p] = found;
+  }
+}
+
+}  // namespace hgs
+
+extern "C" int hgs_render_depth(const hgs_projected* proj, const hgs_tiles* tiles, int32_t width, int32_t height,
+                                double* out_depth, void* stream) {
+  using namespace hgs;
+  if (!proj || !tiles || !out_depth) return hgs_set_error(HGS_ERR_INVALID, "hgs_render_depth: null argument");
+  if (tiles->tile_px != BLEND_TILE)
+    return hgs_set_error(HGS_ERR_INVALID, "hgs_render_depth: only tile_px == 16 is implemented");
+  if (width <= 0 || height <= 0) return hgs_set_error(HGS_ERR_INVALID, "hgs_render_depth: empty image");
+  if (tiles->tiles_x != (width + 15) / 16 || tiles->tiles_y != (height + 15) / 16)
+    return hgs_set_error(HGS_ERR_INVALID, "hgs_render_depth: tile grid does not match image size");
+  const int64_t npix = (int64_t)width * height;
+  const int64_t blocks = std::min<int64_t>(ceil_div(npix * 32, 256), 16 * NUM_SMS);
+  depth_walk_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const BlendRec*)proj->rec, tiles->entries,
+                                                                  tiles->tile_starts, tiles->tiles_x, width, height,
+                                                                  out_depth, tiles->counters);
+  HGS_CHECK_LAUNCH();
+  return HGS_OK;
+}

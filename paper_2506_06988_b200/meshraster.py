@@ -129,3 +129,48 @@ def mesh_layer(mesh, cam, fragments: Optional[MeshFragmentBuffer] = None) -> Mes
         fragments = rasterize_fragments(mesh, cam, with_bary=False)
     color = sample_texture(mesh.texture, fragments.uv, fragments.triangle_id)
     return MeshLayer(color=color, depth=fragments.depth, triangle_id=fragments.triangle_id)
+
+
+def init_texture(mesh, images, cameras, iters: int = 500, mode: str = "optimized", lr: float = 0.05,
+                 warn=print) -> TexturedMesh:
+    """Texture initialisation (meshraster.py:206-245): constant 0.5, or
+    ``iters`` Adam steps (lr, texture clamped to [0, 1] after each) on the
+    coverage-normalised masked MSE between the mesh render and the target
+    images, views averaged.  Texels no view covers keep 0.5.  Everything
+    runs on the device: fragments once per camera, then per step the
+    bilinear fetch, masked difference, bilinear adjoint (accumulated over
+    views) and the fused Adam + clamp."""
+    from .adam import Adam
+    mesh = TexturedMesh.from_any(mesh)
+    if mesh.uvs is None:
+        raise ValueError("init_texture needs a mesh with UVs")
+    if mode not in ("constant", "optimized"):
+        raise ValueError(f"unknown texture init mode {mode!r}")
+    dev = mesh.device
+    tex0 = mesh.texture if mesh.texture is not None else torch.zeros(1, 1, 3, device=dev)
+    out = TexturedMesh(mesh.vertices.clone(), mesh.triangles.clone(), mesh.uvs.clone(),
+                       torch.full_like(tex0, 0.5, dtype=torch.float32), device=dev)
+    if mode == "constant" or iters <= 0:
+        return out
+    if len(images) != len(cameras):
+        raise ValueError("images/cameras count mismatch")
+    frags = [rasterize_fragments(out, cam, with_bary=False) for cam in cameras]
+    covered = [f.triangle_id >= 0 for f in frags]
+    n_cov = [int(c.sum().item()) for c in covered]
+    if sum(n_cov) == 0:
+        warn("init_texture: no camera sees the mesh; falling back to constant 0.5")
+        return out
+    targets = [_as_dev(im, dev, torch.float32) for im in images]
+    th, tw = int(out.texture.shape[0]), int(out.texture.shape[1])
+    opt = Adam({"texture": out.texture}, {"texture": lr})
+    grad = torch.zeros_like(out.texture)
+    for _ in range(iters):
+        grad.zero_()
+        for img, fr, cov, nc in zip(targets, frags, covered, n_cov):
+            if nc == 0:
+                continue
+            pred = sample_texture(out.texture, fr.uv, fr.triangle_id)
+            diff = torch.where(cov[..., None], pred - img, torch.zeros_like(pred))
+            texture_backward(fr, diff * (2.0 / nc), (th, tw), out=grad)
+        opt.step({"texture": grad}, clamp=("texture",), grad_scale=1.0 / len(cameras))
+    return out

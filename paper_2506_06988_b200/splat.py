@@ -387,6 +387,23 @@ def render(gs, cam, background=(0.0, 0.0, 0.0), mesh: Optional[MeshLayer] = None
     return out, ctx
 
 
+def render_depth(gs, cam, tile_px: int = TILE_PX) -> torch.Tensor:
+    """(H, W) fp64 median-style depth map for surface extraction, NaN where
+    the accumulated opacity never exceeds 0.5 (splat/render.py:316-324,
+    depth_kernel splat/kernels.py:163-202)."""
+    if tile_px != TILE_PX:
+        raise ValueError("only tile_px == 16 is implemented on the B200 path")
+    gs = GaussianSet.from_any(gs)
+    cam = Camera.from_any(cam)
+    w, h = int(cam.width), int(cam.height)
+    proj = _preprocess(gs, cam, _upload_camera(cam, gs.device), tile_px, extras=False)
+    tiles, counters = _tiles_core(proj, w, h, tile_px, None)
+    out = torch.empty(h, w, dtype=torch.float64, device=gs.device)
+    _lib.call("hgs_render_depth", ctypes.byref(proj.struct()), ctypes.byref(tiles.struct(counters)), w, h,
+              _lib.ptr(out), _stream_ptr(gs.device))
+    return out
+
+
 def rasterize_backward(ctx: RenderCtx, grad_color, grad_transmittance=None) -> GaussianGrads:
     """splat/render.py:124-182: analytic gradients of sum(grad_color * pixel)
     (+ sum(grad_transmittance * T)) for all parameters."""
