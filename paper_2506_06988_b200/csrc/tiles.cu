@@ -755,6 +755,11 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs 
 // the 16 warps take contiguous parts of the ordered list, count per tile
 // (pass 1: byte-packed warp reductions), take their per-tile start from the
 // warp prefix, then write (pass 2: one ballot per tile keeps the list order).
+__device__ __forceinline__ ushort4 unpack_rect(uint2 r) {
+  return make_ushort4((unsigned short)(r.x & 0xFFFFu), (unsigned short)(r.x >> 16), (unsigned short)(r.y & 0xFFFFu),
+                      (unsigned short)(r.y >> 16));
+}
+
 template <int S>
 struct FineMask;
 template <>
@@ -807,18 +812,19 @@ __global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
   uint32_t cnt[NT];
 #pragma unroll
   for (int q = 0; q < NT; q++) cnt[q] = 0;
-  ushort4 rq[FINE_DEPTH];
+  // loads from a clamped index (no select on the loaded value, which would
+  // wait for it at once); validity is applied where the rectangle is used
+  const uint32_t klast = w1 > w0 ? w1 - 1 : 0u;
+  const uint2* __restrict__ crect2 = reinterpret_cast<const uint2*>(crect);
+  uint2 rq[FINE_DEPTH];  // raw 64-bit rectangles: fields are unpacked only where used
 #pragma unroll
-  for (int d = 0; d < FINE_DEPTH; d++) {
-    const uint32_t k = w0 + d * 32 + lane;
-    rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
-  }
+  for (int d = 0; d < FINE_DEPTH; d++) rq[d] = __ldg(crect2 + min(w0 + d * 32 + lane, klast));
   for (uint32_t k0 = w0; k0 < w1; k0 += 32 * FINE_DEPTH) {
 #pragma unroll
     for (int d = 0; d < FINE_DEPTH; d++) {
-      const typename M::T msk = M::of(rq[d], sx0, sy0);
-      const uint32_t k = k0 + (d + FINE_DEPTH) * 32 + lane;
-      rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
+      const bool valid = k0 + d * 32 + lane < w1;
+      const typename M::T msk = valid ? M::of(unpack_rect(rq[d]), sx0, sy0) : (typename M::T)0;
+      rq[d] = __ldg(crect2 + min(k0 + (d + FINE_DEPTH) * 32 + lane, klast));
 #pragma unroll
       for (int j = 0; j < NT / 4; j++) {
         const uint32_t packed = __reduce_add_sync(0xffffffffu, (M::nibble(msk, j) * 0x00204081u) & 0x01010101u);
@@ -846,18 +852,19 @@ __global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
   uint32_t gq[FINE_DEPTH];
 #pragma unroll
   for (int d = 0; d < FINE_DEPTH; d++) {
-    const uint32_t k = w0 + d * 32 + lane;
-    rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
-    gq[d] = k < w1 ? __ldg(crow + k) : 0u;
+    const uint32_t k = min(w0 + d * 32 + lane, klast);
+    rq[d] = __ldg(crect2 + k);
+    gq[d] = __ldg(crow + k);
   }
   for (uint32_t k0 = w0; k0 < w1; k0 += 32 * FINE_DEPTH) {
 #pragma unroll
     for (int d = 0; d < FINE_DEPTH; d++) {
-      const typename M::T msk = M::of(rq[d], sx0, sy0);
+      const bool valid = k0 + d * 32 + lane < w1;
+      const typename M::T msk = valid ? M::of(unpack_rect(rq[d]), sx0, sy0) : (typename M::T)0;
       const uint32_t g = gq[d];
-      const uint32_t k = k0 + (d + FINE_DEPTH) * 32 + lane;
-      rq[d] = k < w1 ? __ldg(crect + k) : make_ushort4(1, 0, 1, 0);
-      gq[d] = k < w1 ? __ldg(crow + k) : 0u;
+      const uint32_t k = min(k0 + (d + FINE_DEPTH) * 32 + lane, klast);
+      rq[d] = __ldg(crect2 + k);
+      gq[d] = __ldg(crow + k);
 #pragma unroll
       for (int q = 0; q < NT; q++) {
         const bool hit = M::bit(msk, q);

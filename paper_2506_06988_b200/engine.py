@@ -44,7 +44,13 @@ class HybridRenderer:
         n = max(len(gs), 1)
         h, w = self.height, self.width
         self.cam_dev = torch.zeros(CAMERA_BYTES, dtype=torch.uint8, device=dev)
-        self.cam_host = torch.zeros(CAMERA_BYTES, dtype=torch.uint8).pin_memory()
+        # pinned camera staging ring: a buffer is rewritten only after its
+        # previous async H2D has executed (event), so frames can be enqueued
+        # back to back without a host sync
+        self._cam_ring = [torch.zeros(CAMERA_BYTES, dtype=torch.uint8).pin_memory() for _ in range(4)]
+        self._cam_ev = [None] * len(self._cam_ring)
+        self._cam_k = 0
+        self.cam_host = self._cam_ring[0]
         self.rec = torch.empty(n * REC_BYTES, dtype=torch.uint8, device=dev)
         self.count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.rect = torch.zeros(n * 4, dtype=torch.int16, device=dev)
@@ -87,8 +93,47 @@ class HybridRenderer:
         """H2D of the 200-byte camera struct from pinned memory (async)."""
         s = camera_struct(cam)
         raw = np.frombuffer(bytes(s), dtype=np.uint8)
+        k = self._cam_k
+        self._cam_k = (k + 1) % len(self._cam_ring)
+        if self._cam_ev[k] is not None:
+            self._cam_ev[k].synchronize()  # its previous upload has been consumed
+        self.cam_host = self._cam_ring[k]
         self.cam_host.numpy()[:len(raw)] = raw
         self.cam_dev.copy_(self.cam_host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        self._cam_ev[k] = ev
+
+    def render_to_host(self, cam, out_host: torch.Tensor) -> torch.cuda.Event:
+        """Serving path: camera H2D, one replay of the frame graph, a device
+        snapshot of the colour image and its D2H into ``out_host`` (pinned,
+        H x W x 3 fp32) on a copy stream, so the transfer overlaps the next
+        frame.  Snapshots are double-buffered.  Returns the event that marks
+        the copy complete (the caller must not reuse ``out_host`` before)."""
+        if self.graph is None:
+            self.capture()
+        if getattr(self, "_copy", None) is None:
+            self._copy = torch.cuda.Stream(self.dev)
+            self._snap = [torch.empty_like(self.color) for _ in range(2)]
+            self._snap_ev = [None, None]
+            self._snap_k = 0
+        k = self._snap_k
+        self._snap_k ^= 1
+        main = torch.cuda.current_stream(self.dev)
+        if self._snap_ev[k] is not None:
+            main.wait_event(self._snap_ev[k])  # the previous D2H from this snapshot is done
+        self.set_camera(cam)
+        self.graph.replay()
+        self._snap[k].copy_(self.color, non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        self._copy.wait_event(ready)
+        with torch.cuda.stream(self._copy):
+            out_host.copy_(self._snap[k], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self._copy)
+        self._snap_ev[k] = done
+        return done
 
     def _structs(self):
         ps = _lib.HGSProjected()
