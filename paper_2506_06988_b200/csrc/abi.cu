@@ -1,9 +1,11 @@
 // Library-level entry points of libhgs.so: error reporting and device query.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
 
+#include <algorithm>
 #include <atomic>
 
 namespace {
@@ -12,6 +14,31 @@ std::atomic<long long> g_launches{0};
 }
 
 void hgs_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace hgs {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HGS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+__global__ void zero_words_kernel(uint32_t* a, int64_t na, uint32_t* b, int64_t nb) {
+  pdl_enter();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += stride) {
+    if (i < na) a[i] = 0u;
+    else b[i - na] = 0u;
+  }
+}
+
+cudaError_t zero_pdl(cudaStream_t st, void* a, size_t abytes, void* b, size_t bbytes) {
+  const int64_t na = (int64_t)(abytes / 4), nb = b ? (int64_t)(bbytes / 4) : 0;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((na + nb + 255) / 256, 4 * NUM_SMS));
+  return launch_pdl(zero_words_kernel, dim3((unsigned)blocks), dim3(256), 0, st, (uint32_t*)a, na, (uint32_t*)b, nb);
+}
+}  // namespace hgs
 
 extern "C" int64_t hgs_kernel_launches(void) { return g_launches.load(); }
 

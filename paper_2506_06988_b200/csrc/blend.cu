@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
     const int64_t* __restrict__ counters) {
+  pdl_enter();
   if (counters && counters[2]) return;  // entry buffer overflowed: bins are invalid, the caller re-renders
   extern __shared__ __align__(128) unsigned char fast_smem_raw[];
   FastSmem& sm = *reinterpret_cast<FastSmem*>(fast_smem_raw);
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
     const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
     int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
     double mask_k, hgs_blend_out out, const int32_t* __restrict__ fixup, const int64_t* __restrict__ counters) {
+  pdl_enter();
   if (counters && counters[2]) return;  // overflowed bins (see blend_fast_kernel)
   const int64_t count = fixup ? fixup[0] : (int64_t)width * height;
   const int lane = threadIdx.x & 31;
@@ -507,7 +509,8 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
   const int n_tiles = tiles->tiles_x * tiles->tiles_y;
   const int64_t npix = (int64_t)width * height;
   if (out->fixup && proj->cull) {
-    cudaMemsetAsync(out->fixup, 0, sizeof(int32_t), st);
+    zero_pdl(st, out->fixup, sizeof(int32_t));
+    HGS_CHECK_LAUNCH();
     const size_t smem = sizeof(FastSmem);
     static bool attr = false;
     if (!attr) {
@@ -518,22 +521,22 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
       attr = true;
     }
     if (out->stats)
-      blend_fast_kernel<true><<<n_tiles, FAST_THREADS, smem, st>>>(
+      launch_pdl(blend_fast_kernel<true>, dim3(n_tiles), dim3(FAST_THREADS), smem, st, 
           (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
           width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
     else
-      blend_fast_kernel<false><<<n_tiles, FAST_THREADS, smem, st>>>(
+      launch_pdl(blend_fast_kernel<false>, dim3(n_tiles), dim3(FAST_THREADS), smem, st, 
           (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
           width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
     HGS_CHECK_LAUNCH();
     // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)
-    blend_exact_kernel<<<2 * NUM_SMS, 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,
+    launch_pdl(blend_exact_kernel, dim3(2 * NUM_SMS), dim3(256), 0, st, (const BlendRec*)proj->rec, tiles->entries,
                                                     tiles->tile_starts, tiles->tiles_x, width, height, ml,
                                                     bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
                                                     mask_k, *out, out->fixup, tiles->counters);
     HGS_CHECK_LAUNCH();
   } else {
-    blend_exact_kernel<<<ceil_div(npix * 32, 256), 256, 0, st>>>((const BlendRec*)proj->rec, tiles->entries,
+    launch_pdl(blend_exact_kernel, dim3(ceil_div(npix * 32, 256)), dim3(256), 0, st, (const BlendRec*)proj->rec, tiles->entries,
                                                             tiles->tile_starts, tiles->tiles_x, width, height, ml,
                                                             bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
                                                             mask_k, *out, nullptr, tiles->counters);

@@ -69,6 +69,39 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Programmatic dependent launch (PDL).  A kernel launched with launch_pdl()
+// may be scheduled while the previous kernel on its stream drains; it calls
+// pdl_enter() first thing: griddepcontrol.wait blocks until the previous
+// grid has completed and its writes are visible (a no-op for a normal
+// launch), then launch_dependents lets the next PDL kernel's CTAs be
+// scheduled into SM slots this grid frees (its CTAs have all started by
+// then, so they cannot be starved).  HGS_PDL=0 in the environment turns the
+// attribute off (plain stream order).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+// Zeroes up to two word ranges, as a PDL kernel (a memset node would break
+// the programmatic chain).
+__global__ void zero_words_kernel(uint32_t* a, int64_t na, uint32_t* b, int64_t nb);
+cudaError_t zero_pdl(cudaStream_t st, void* a, size_t abytes, void* b = nullptr, size_t bbytes = 0);
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace hgs
 
 // Every kernel launch is followed by HGS_CHECK_LAUNCH(): it surfaces launch

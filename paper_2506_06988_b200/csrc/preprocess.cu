@@ -38,6 +38,7 @@ __device__ __forceinline__ void quat_to_rot(double q0, double q1, double q2, dou
 
 __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __restrict__ cam_ptr, hgs_gaussians gs,
                                                          int tile_px, int tiles_x, int tiles_y, hgs_projected out) {
+  pdl_enter();  // releases the binning chain's PDL launches early
   __shared__ CamConst cs;
   if (threadIdx.x == 0) load_cam(cam_ptr, cs);
   __syncthreads();

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
                                                                 const uint32_t* __restrict__ hist, uint32_t* status,
                                                                 int nparts_cap, uint32_t* part_ctr, int write_keys,
                                                                 const uint32_t* __restrict__ poff = nullptr) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RadixSmem<K, IPT>& sm = *reinterpret_cast<RadixSmem<K, IPT>*>(smem_raw);
   constexpr int TILE = RS_THREADS * IPT;

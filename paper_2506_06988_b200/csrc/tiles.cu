@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
                                                                uint64_t* dkeys, uint32_t* dvals, uint64_t* status,
                                                                uint32_t* part_ctr, int64_t* counters,
                                                                unsigned long long* minmax) {
+  pdl_enter();
   __shared__ int s_part;
   unsigned long long nmin = 0, kmax = 0;  // max of ~key (== ~min key) and max key over visible rows
   const int nparts = (int)((n + SCAN_TILE - 1) / SCAN_TILE);
@@ -97,6 +98,7 @@ __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
 __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __restrict__ keys, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax,
                                                           uint32_t* __restrict__ k32, uint32_t* __restrict__ hist) {
+  pdl_enter();
   constexpr int NP = DEPTH_KEY_BITS / 8;
   __shared__ uint32_t sh_h[NP][256];
   for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) (&sh_h[0][0])[i] = 0;
@@ -124,6 +126,7 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
 __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ rows,
                                                           const BlendRec* __restrict__ rec, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax) {
+  pdl_enter();
   const int64_t m = counters[0];
   if (depth_shift(minmax) == 0) return;  // keys were exact
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __rest
 __global__ void __launch_bounds__(1024) tile_counts_kernel(const int* __restrict__ diff, int tiles_x, int tiles_y,
                                                            int64_t capacity, int64_t* tile_starts, int64_t* counters,
                                                            uint32_t* hist) {
+  pdl_enter();
   extern __shared__ int g[];  // (tiles_x + 1) x (tiles_y + 1)
   __shared__ uint32_t sh[2][RADIX];
   __shared__ int64_t s_chunk[1024];
@@ -430,6 +434,7 @@ __global__ void __launch_bounds__(256) coarse_prep_sum_kernel(const uint32_t* __
                                                               const ushort4* __restrict__ rect, const int64_t* counters,
                                                               int ss, ushort4* __restrict__ rsort,
                                                               uint32_t* __restrict__ bsum) {
+  pdl_enter();
   __shared__ uint32_t s_w[8];
   const int64_t m = counters[0];
   const int64_t b0 = (int64_t)blockIdx.x * PREP_ROWS;
@@ -457,6 +462,7 @@ __global__ void __launch_bounds__(256) coarse_prep_sum_kernel(const uint32_t* __
 // prep 2 (one CTA): exclusive scan of the block sums; pair total -> *npairs
 __global__ void __launch_bounds__(1024) coarse_prep_scan_kernel(const int64_t* counters, uint32_t* __restrict__ bsum,
                                                                 uint32_t* __restrict__ npairs) {
+  pdl_enter();
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
   const int64_t m = counters[0];
@@ -503,6 +509,7 @@ __global__ void __launch_bounds__(256) coarse_prep_offsets_kernel(const ushort4*
                                                                   const uint32_t* __restrict__ npairs,
                                                                   uint32_t* __restrict__ pair_off,
                                                                   uint32_t* __restrict__ wstart) {
+  pdl_enter();
   __shared__ uint32_t s_w[8];
   const int64_t m = counters[0];
   const int64_t b0 = (int64_t)blockIdx.x * PREP_ROWS;
@@ -606,6 +613,7 @@ struct CoarseArgs {
 __global__ void __launch_bounds__(BIN_THREADS) coarse_count_kernel(CoarseArgs a, uint32_t* __restrict__ mat,
                                                                    uint32_t* __restrict__ wmat,
                                                                    uint32_t* __restrict__ hist) {
+  pdl_enter();
   __shared__ uint32_t cnt[BIN_WARPS][BIN_MAX_SUPER];
   const int64_t m = a.counters[0];
   if (a.counters[1] > a.capacity) return;  // overflow: flagged in counters[2]
@@ -643,6 +651,7 @@ __global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __res
                                                            int64_t capacity, const uint32_t* __restrict__ npairs,
                                                            int ns, uint32_t* __restrict__ cstart,
                                                            uint32_t* __restrict__ slot) {
+  pdl_enter();
   __shared__ uint32_t s_sum[32][33];
   __shared__ uint32_t s_start[32];
   if (counters[1] > capacity) return;
@@ -701,6 +710,7 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs 
                                                                      const uint32_t* __restrict__ wmat,
                                                                      uint32_t* __restrict__ crow,
                                                                      ushort4* __restrict__ crect_out) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char sc_raw[];
   ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(sc_raw);
   const int64_t m = a.counters[0];
@@ -796,6 +806,7 @@ __global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
     const uint32_t* __restrict__ crow, const ushort4* __restrict__ crect, const uint32_t* __restrict__ cstart,
     const int64_t* __restrict__ tile_starts, const int64_t* counters, int64_t capacity, int tiles_x, int tiles_y,
     int sx, uint32_t* __restrict__ entries) {
+  pdl_enter();
   constexpr int NT = S * S;
   using M = FineMask<S>;
   constexpr int FINE_WARPS = fine_warps(S);
@@ -1021,7 +1032,7 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
                                                                                  (int)tile, pcnt);
       HGS_CHECK_LAUNCH();
     }
-    radix_pass_kernel<K, IPT><<<g, RS_THREADS, smem, st>>>(kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
+    launch_pdl(radix_pass_kernel<K, IPT>, dim3(g), dim3(RS_THREADS), smem, st, kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
                                                       hist + RADIX * p, status + (size_t)p * parts * RADIX, (int)parts,
                                                       part_ctr + p, (!last || last_keys) ? 1 : 0, pcnt);
     HGS_CHECK_LAUNCH();
@@ -1064,14 +1075,14 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   cudaStream_t st = (cudaStream_t)stream;
   TilesScratch s;
   carve(n, tiles->capacity, tx, ty, (unsigned char*)tiles->scratch, &s);
-  cudaMemsetAsync(s.control_begin, 0, s.control_bytes, st);
-  cudaMemsetAsync(tiles->counters, 0, 4 * sizeof(int64_t), st);
+  zero_pdl(st, s.control_begin, s.control_bytes, tiles->counters, 4 * sizeof(int64_t));
+  HGS_CHECK_LAUNCH();
   // 1. order-preserving compaction of the visible rows' depth keys
   static int scan_grid_cap = 0;
   if (scan_grid_cap == 0) scan_grid_cap = persistent_grid((const void*)compact_kernel, SCAN_THREADS, 0);
   const int scan_grid = (int)tmax<int64_t>(1, tmin<int64_t>(scan_grid_cap, (n + SCAN_TILE - 1) / SCAN_TILE));
   if (n > 0) {
-    compact_kernel<<<scan_grid, SCAN_THREADS, 0, st>>>(proj->sort_keys, n, s.dk[0], s.dv[0], s.scan_status,
+    launch_pdl(compact_kernel, dim3(scan_grid), dim3(SCAN_THREADS), 0, st, proj->sort_keys, n, s.dk[0], s.dv[0], s.scan_status,
                                                        s.part_ctr + 20, tiles->counters,
                                                        reinterpret_cast<unsigned long long*>(s.part_ctr + 24));
     HGS_CHECK_LAUNCH();
@@ -1084,7 +1095,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     cudaFuncSetAttribute(tile_counts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     tc_attr = true;
   }
-  tile_counts_kernel<<<1, 1024, grid_smem, st>>>(proj->tile_diff, tx, ty, tiles->capacity, tiles->tile_starts,
+  launch_pdl(tile_counts_kernel, dim3(1), dim3(1024), grid_smem, st, proj->tile_diff, tx, ty, tiles->capacity, tiles->tile_starts,
                                                  tiles->counters, s.hist + 8 * RADIX);
   HGS_CHECK_LAUNCH();
   if (n == 0) return HGS_OK;
@@ -1093,7 +1104,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
   uint32_t* k32b = k32a + (n > 0 ? n : 1);
   unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
-  depth_remap_kernel<<<4 * sm_count(), 256, 0, st>>>(s.dk[0], tiles->counters, minmax, k32a, s.hist);
+  launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, s.dk[0], tiles->counters, minmax, k32a, s.hist);
   HGS_CHECK_LAUNCH();
   uint32_t* k32res = nullptr;
   uint32_t* rows = nullptr;  // visible rows in (depth, row) order
@@ -1101,7 +1112,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                                    DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr, st,
                                    &k32res, true, &rows);
   if (rc) return rc;
-  depth_fixup_kernel<<<4 * sm_count(), 256, 0, st>>>(k32res, rows, (const BlendRec*)proj->rec, tiles->counters,
+  launch_pdl(depth_fixup_kernel, dim3(4 * sm_count()), dim3(256), 0, st, k32res, rows, (const BlendRec*)proj->rec, tiles->counters,
                                                      minmax);
   HGS_CHECK_LAUNCH();
   const int ss = super_shift(tx, ty);
@@ -1109,12 +1120,12 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     // 4. two-level rect binning straight into the final (tile, depth, row) order
     const int sx = (tx + (1 << ss) - 1) >> ss, sy = (ty + (1 << ss) - 1) >> ss, n_super = sx * sy;
     const int pblk = (int)((n + PREP_ROWS - 1) / PREP_ROWS);  // upper bound: kernels read m on the device
-    coarse_prep_sum_kernel<<<pblk, 256, 0, st>>>(rows, (const ushort4*)proj->rect, tiles->counters, ss, s.rsort,
+    launch_pdl(coarse_prep_sum_kernel, dim3(pblk), dim3(256), 0, st, rows, (const ushort4*)proj->rect, tiles->counters, ss, s.rsort,
                                                  s.bsum);
     HGS_CHECK_LAUNCH();
-    coarse_prep_scan_kernel<<<1, 1024, 0, st>>>(tiles->counters, s.bsum, s.npairs);
+    launch_pdl(coarse_prep_scan_kernel, dim3(1), dim3(1024), 0, st, tiles->counters, s.bsum, s.npairs);
     HGS_CHECK_LAUNCH();
-    coarse_prep_offsets_kernel<<<pblk, 256, 0, st>>>(s.rsort, tiles->counters, ss, s.bsum, s.npairs, s.pair_off,
+    launch_pdl(coarse_prep_offsets_kernel, dim3(pblk), dim3(256), 0, st, s.rsort, tiles->counters, ss, s.bsum, s.npairs, s.pair_off,
                                                      s.wstart);
     HGS_CHECK_LAUNCH();
     CoarseArgs ca{rows, s.rsort, s.pair_off, s.wstart, s.npairs, tiles->counters, tiles->capacity, ss, sx, n_super};
@@ -1124,20 +1135,20 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
       cudaFuncSetAttribute(coarse_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
       sgrid = persistent_grid((const void*)coarse_scatter_kernel, BIN_THREADS, sizeof(ScatterSmem));
     }
-    coarse_count_kernel<<<cgrid, BIN_THREADS, 0, st>>>(ca, s.bin_mat, s.bin_wmat, s.chist);
+    launch_pdl(coarse_count_kernel, dim3(cgrid), dim3(BIN_THREADS), 0, st, ca, s.bin_mat, s.bin_wmat, s.chist);
     HGS_CHECK_LAUNCH();
-    coarse_scan_kernel<<<(n_super + 31) / 32, 1024, 0, st>>>(s.bin_mat, s.chist, tiles->counters, tiles->capacity,
+    launch_pdl(coarse_scan_kernel, dim3((n_super + 31) / 32), dim3(1024), 0, st, s.bin_mat, s.chist, tiles->counters, tiles->capacity,
                                                              s.npairs, n_super, s.cstart, s.bin_slot);
     HGS_CHECK_LAUNCH();
-    coarse_scatter_kernel<<<sgrid, BIN_THREADS, sizeof(ScatterSmem), st>>>(ca, s.bin_mat, s.bin_slot, s.bin_wmat,
+    launch_pdl(coarse_scatter_kernel, dim3(sgrid), dim3(BIN_THREADS), sizeof(ScatterSmem), st, ca, s.bin_mat, s.bin_slot, s.bin_wmat,
                                                                           s.crow, s.crect);
     HGS_CHECK_LAUNCH();
     if (ss == 2)
-      fine_bin_kernel<4><<<n_super, fine_warps(4) * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
+      launch_pdl(fine_bin_kernel<4>, dim3(n_super), dim3(fine_warps(4) * 32), 0, st, s.crow, s.crect, s.cstart, tiles->tile_starts,
                                                               tiles->counters, tiles->capacity, tx, ty, sx,
                                                               tiles->entries);
     else if (ss == 3)
-      fine_bin_kernel<8><<<n_super, fine_warps(8) * 32, 0, st>>>(s.crow, s.crect, s.cstart, tiles->tile_starts,
+      launch_pdl(fine_bin_kernel<8>, dim3(n_super), dim3(fine_warps(8) * 32), 0, st, s.crow, s.crect, s.cstart, tiles->tile_starts,
                                                               tiles->counters, tiles->capacity, tx, ty, sx,
                                                               tiles->entries);
     else
