@@ -30,7 +30,10 @@ constexpr uint64_t SCAN_FLAG_INC = 2ull << 62;
 constexpr uint64_t SCAN_VALUE_MASK = (1ull << 62) - 1;
 
 constexpr uint32_t SPIN_LIMIT = 1u << 24;
-constexpr int LB_WINDOW = 16;  // predecessors read per look-back round trip
+#ifndef HGS_LB_WINDOW
+#define HGS_LB_WINDOW 16
+#endif
+constexpr int LB_WINDOW = HGS_LB_WINDOW;  // predecessors read per look-back round trip
 constexpr uint32_t RS_FLAG_AGG = 1u << 30;
 constexpr uint32_t RS_FLAG_INC = 2u << 30;
 constexpr uint32_t RS_VALUE_MASK = (1u << 30) - 1;
