@@ -194,7 +194,12 @@ __device__ __forceinline__ void bw_pixel_step(BwPix& q, const StageEntry& E, int
   }
   if (!ok) return;
   const float4 col = E.f.col;  // alpha, r, g, b
-  const float inv = __frcp_rn(1.0f - sg);  // one reciprocal for the five divisions of kernels.py:135,142-146
+  // one reciprocal for the five divisions of kernels.py:135,142-146; 1 - sigma
+  // is in [0.01, 1) (no special cases): SFU estimate + one Newton step (~1 ulp,
+  // 3 instructions instead of the IEEE-rn sequence)
+  const float om = 1.0f - sg;
+  float inv = rcp_approx(om);
+  inv = fmaf(inv, fmaf(-om, inv, 1.0f), inv);
   const float t_before = q.t_after * inv;
   const float w = sg * t_before;
   v[6] = fmaf(q.gr, w, v[6]);

@@ -69,6 +69,14 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// SFU reciprocal estimate (rcp.approx.ftz: ~1 ulp); callers either refine it
+// or correct an integer quotient derived from it
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Programmatic dependent launch (PDL).  A kernel launched with launch_pdl()
 // may be scheduled while the previous kernel on its stream drains; it calls
 // pdl_enter() first thing: griddepcontrol.wait blocks until the previous

@@ -86,11 +86,6 @@ __device__ __forceinline__ bool ellipse_meets_box(float4 con, float4 box, float 
   return mn <= fmaf(mcut, 1.002f, 0.01f);
 }
 
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
 
 // ---- fast-path numerics -------------------------------------------------
 // exp2 argument u = m * log2(e)/2 (fp64), narrowed to fp32 round-to-nearest.

@@ -276,8 +276,8 @@ constexpr uint32_t EMIT_BIG = 256;
 
 __device__ __forceinline__ void emit_entry(uint32_t o, uint32_t local, uint32_t x0, uint32_t y0, uint32_t rw,
                                            uint32_t g, int tiles_x, uint16_t* tkeys, uint32_t* tvals) {
-  // local / rw with a float reciprocal (exact after one correction: local < 2^24, rw < 2^16)
-  uint32_t q = (uint32_t)((float)local * __frcp_rn((float)rw));
+  // local / rw with a float reciprocal estimate (exact after one correction: local < 2^21, rw < 2^16)
+  uint32_t q = (uint32_t)((float)local * rcp_approx((float)rw));
   int32_t rr = (int32_t)(local - q * rw);
   if (rr < 0) { q--; rr += rw; } else if (rr >= (int32_t)rw) { q++; rr -= rw; }
   tkeys[o] = (uint16_t)((y0 + q) * (uint32_t)tiles_x + x0 + (uint32_t)rr);
@@ -285,7 +285,7 @@ __device__ __forceinline__ void emit_entry(uint32_t o, uint32_t local, uint32_t 
 }
 __device__ __forceinline__ void emit_entry(uint32_t o, uint32_t local, uint32_t x0, uint32_t y0, uint32_t rw,
                                            uint32_t g, int tiles_x, uint32_t* tkeys, uint32_t* tvals) {
-  uint32_t q = (uint32_t)((float)local * __frcp_rn((float)rw));
+  uint32_t q = (uint32_t)((float)local * rcp_approx((float)rw));
   int32_t rr = (int32_t)(local - q * rw);
   if (rr < 0) { q--; rr += rw; } else if (rr >= (int32_t)rw) { q++; rr -= rw; }
   tkeys[o] = (y0 + q) * (uint32_t)tiles_x + x0 + (uint32_t)rr;
@@ -406,7 +406,7 @@ __host__ __device__ inline int super_shift(int tiles_x, int tiles_y) {
 // tile id of the l-th tile (row-major) of a rectangle of width rw in a grid
 // of width gx
 __device__ __forceinline__ uint32_t rect_tile(uint32_t l, ushort4 rc, uint32_t rw, int gx) {
-  uint32_t q = (uint32_t)((float)l * __frcp_rn((float)rw));  // exact after one correction (l < 2^24)
+  uint32_t q = (uint32_t)((float)l * rcp_approx((float)rw));  // exact after one correction (l < 2^21)
   int32_t rr = (int32_t)(l - q * rw);
   if (rr < 0) { q--; rr += rw; } else if (rr >= (int32_t)rw) { q++; rr -= rw; }
   return (rc.z + q) * (uint32_t)gx + rc.x + (uint32_t)rr;
