@@ -362,7 +362,8 @@ struct ChainCam {
 
 __device__ __forceinline__ void quat_rot(const double* q, double* Rq, double* qn, double& nrm) {
   nrm = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
-  const double w = q[0] / nrm, x = q[1] / nrm, y = q[2] / nrm, z = q[3] / nrm;
+  const double rn = 1.0 / nrm;  // gradients only: one reciprocal for the four quotients (<= 1 ulp each)
+  const double w = q[0] * rn, x = q[1] * rn, y = q[2] * rn, z = q[3] * rn;
   qn[0] = w; qn[1] = x; qn[2] = y; qn[3] = z;
   Rq[0] = 1.0 - 2.0 * (y * y + z * z);
   Rq[1] = 2.0 * (x * y - w * z);
@@ -416,7 +417,8 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
     const double d0 = c0 - cc.center[0], d1 = c1 - cc.center[1], d2 = c2 - cc.center[2];
     const double dist = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
     const double den = fmax(dist, 1e-12);
-    const double x = d0 / den, y = d1 / den, z = d2 / den;
+    const double rden = 1.0 / den;
+    const double x = d0 * rden, y = d1 * rden, z = d2 * rden;
     const float* rr = gs.colors_rest + 9 * i;
     for (int ch = 0; ch < 3; ch++)
       pre[ch] = pre[ch] + SH_C1 * ((-y * (double)rr[ch] + z * (double)rr[3 + ch]) - x * (double)rr[6 + ch]);
@@ -432,7 +434,8 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
     const double gd[3] = {-SH_C1 * s2, -SH_C1 * s0, SH_C1 * s1};
     const double dd = (gd[0] * x + gd[1] * y) + gd[2] * z;
     const double dv[3] = {x, y, z};
-    for (int j = 0; j < 3; j++) gc[j] += (gd[j] - dv[j] * dd) / dist;
+    const double rdist = 1.0 / dist;
+    for (int j = 0; j < 3; j++) gc[j] += (gd[j] - dv[j] * dd) * rdist;
   } else {
     for (int ch = 0; ch < 3; ch++) gpre[ch] = pg[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
   }
@@ -441,10 +444,11 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
   double t[3];
   for (int j = 0; j < 3; j++) t[j] = dot3(c0, c1, c2, Rw[j * 3], Rw[j * 3 + 1], Rw[j * 3 + 2]) + cc.T[j];
   const double tz = t[2];
-  const double rx_raw = t[0] / tz, ry_raw = t[1] / tz;
+  const double rtz = 1.0 / tz;  // the chain only produces gradients: reciprocal products, <= 1-2 ulp
+  const double rx_raw = t[0] * rtz, ry_raw = t[1] * rtz;
   const double rx = clampd(rx_raw, -cc.limx, cc.limx), ry = clampd(ry_raw, -cc.limy, cc.limy);
   const double in_x = fabs(rx_raw) < cc.limx ? 1.0 : 0.0, in_y = fabs(ry_raw) < cc.limy ? 1.0 : 0.0;
-  const double J[6] = {fx / tz, 0.0, -fx * rx / tz, 0.0, fy / tz, -fy * ry / tz};
+  const double J[6] = {fx * rtz, 0.0, -fx * rx * rtz, 0.0, fy * rtz, -fy * ry * rtz};
   double q[4], Rq[9], qn[4], nrm;
   for (int k = 0; k < 4; k++) q[k] = gs.rotations[4 * i + k];
   quat_rot(q, Rq, qn, nrm);
@@ -477,10 +481,10 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
       gJ[j * 3 + k] = (gA[j * 3] * Rw[k * 3] + gA[j * 3 + 1] * Rw[k * 3 + 1]) + gA[j * 3 + 2] * Rw[k * 3 + 2];
   // mean2d and J(t) (render.py:255-271)
   double gt[3] = {0.0, 0.0, 0.0};
-  gt[0] += gm0 * fx / tz;
-  gt[1] += gm1 * fy / tz;
-  gt[2] += -(gm0 * fx * rx_raw + gm1 * fy * ry_raw) / tz;
-  const double inv_tz2 = 1.0 / (tz * tz);
+  gt[0] += gm0 * fx * rtz;
+  gt[1] += gm1 * fy * rtz;
+  gt[2] += -(gm0 * fx * rx_raw + gm1 * fy * ry_raw) * rtz;
+  const double inv_tz2 = rtz * rtz;
   gt[0] += gJ[2] * (-fx * in_x * inv_tz2);
   gt[1] += gJ[5] * (-fy * in_y * inv_tz2);
   gt[2] += ((gJ[0] * (-fx * inv_tz2) + gJ[4] * (-fy * inv_tz2)) + gJ[2] * fx * (in_x * rx_raw + rx) * inv_tz2) +
@@ -514,7 +518,8 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
     gqn[k] = acc;
   }
   const double dq = ((gqn[0] * qn[0] + gqn[1] * qn[1]) + gqn[2] * qn[2]) + gqn[3] * qn[3];
-  for (int k = 0; k < 4; k++) put(out.rotations, 4 * i + k, (gqn[k] - qn[k] * dq) / nrm, o_r[k]);
+  const double rnrm = 1.0 / nrm;
+  for (int k = 0; k < 4; k++) put(out.rotations, 4 * i + k, (gqn[k] - qn[k] * dq) * rnrm, o_r[k]);
   if (out.densify_norm) {
     const double sx = gm0 * (cc.W / 2.0), sy = gm1 * (cc.H / 2.0);
     put(out.densify_norm, i, sqrt(sx * sx + sy * sy) / (double)scale, o_dn);
