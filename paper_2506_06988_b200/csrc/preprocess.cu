@@ -47,12 +47,15 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
   const CamConst& c = cs;
 
   const double c0 = gs.centers[3 * i], c1 = gs.centers[3 * i + 1], c2 = gs.centers[3 * i + 2];
+  // every per-Gaussian load is issued early so their latencies overlap
+  const float lg = gs.logits[i];
+  const float ls0 = gs.log_scales[3 * i], ls1 = gs.log_scales[3 * i + 1], ls2 = gs.log_scales[3 * i + 2];
   double t[3];
 #pragma unroll
   for (int j = 0; j < 3; j++) t[j] = dot3(c0, c1, c2, c.R[j * 3], c.R[j * 3 + 1], c.R[j * 3 + 2]) + c.T[j];
   const double depth = t[2];
   bool ok = (depth > c.near_) && (depth < c.far_);
-  const double alpha = 1.0 / (1.0 + exp(-(double)gs.logits[i]));
+  const double alpha = 1.0 / (1.0 + exp(-(double)lg));
   ok = ok && (alpha >= SIGMA_SKIP);
   if (!ok) {
     // culled before projection (near/far/opacity, project.py:80-83): no
@@ -63,6 +66,9 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
     if (out.cull) reinterpret_cast<CullRec*>(out.cull)[i].box = make_float4(0.f, 0.f, -1.0f, -1.0f);
     return;
   }
+  const float q0 = gs.rotations[4 * i], q1 = gs.rotations[4 * i + 1], q2 = gs.rotations[4 * i + 2],
+              q3 = gs.rotations[4 * i + 3];
+  const float dc0 = gs.colors_dc[3 * i], dc1 = gs.colors_dc[3 * i + 1], dc2 = gs.colors_dc[3 * i + 2];
   const double tz = ok ? depth : 1.0;
   const double mx = c.fx * t[0] / tz + c.cx;
   const double my = c.fy * t[1] / tz + c.cy;
@@ -72,8 +78,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
     // 3 sqrt(|J|_F^2 max(s)^2 + 0.3); a Gaussian whose box with that bound
     // misses the screen is culled by the reference too -- skip its covariance
     // (most rows of a training view fall here).
-    const double lsm = fmax(fmax((double)gs.log_scales[3 * i], (double)gs.log_scales[3 * i + 1]),
-                            (double)gs.log_scales[3 * i + 2]);
+    const double lsm = fmax(fmax((double)ls0, (double)ls1), (double)ls2);
     const double rxc = clampd(t[0] / tz, -c.limx, c.limx), ryc = clampd(t[1] / tz, -c.limy, c.limy);
     const double jf2 = (c.fx * c.fx * (1.0 + rxc * rxc) + c.fy * c.fy * (1.0 + ryc * ryc)) / (tz * tz);
     const double r_ub = 3.0 * sqrt(jf2 * exp(2.0 * lsm) + COV_FLOOR) * (1.0 + 1e-6) + 1e-6;
@@ -88,10 +93,8 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
 
   // 3D covariance: Sigma = M M^T, M = R diag(s)   (project.py:91-94)
   double Rq[9], M[9], sig[9];
-  quat_to_rot(gs.rotations[4 * i], gs.rotations[4 * i + 1], gs.rotations[4 * i + 2], gs.rotations[4 * i + 3], Rq);
-  double s[3];
-#pragma unroll
-  for (int j = 0; j < 3; j++) s[j] = exp((double)gs.log_scales[3 * i + j]);
+  quat_to_rot(q0, q1, q2, q3, Rq);
+  const double s[3] = {exp((double)ls0), exp((double)ls1), exp((double)ls2)};
 #pragma unroll
   for (int a = 0; a < 3; a++)
 #pragma unroll
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __
   // view-dependent colour (project.py:56-67)
   double pre[3];
 #pragma unroll
-  for (int ch = 0; ch < 3; ch++) pre[ch] = 0.5 + SH_C0 * (double)gs.colors_dc[3 * i + ch];
+  for (int ch = 0; ch < 3; ch++) pre[ch] = 0.5 + SH_C0 * (double)(ch == 0 ? dc0 : (ch == 1 ? dc1 : dc2));
   double vx = 0.0, vy = 0.0, vz = 0.0, dist = 0.0;
   if (gs.colors_rest != nullptr) {
     const double d0 = c0 - c.center[0], d1 = c1 - c.center[1], d2 = c2 - c.center[2];
