@@ -379,7 +379,22 @@ __device__ __forceinline__ void quat_rot(const double* q, double* Rq, double* qn
 // Chain rule of one visible Gaussian i (render.py:185-313).
 __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& gs, const double* __restrict__ screen,
                                        const hgs_gaussian_grads& out, float scale, int accumulate, int64_t i) {
-  // accumulation: every old gradient value is loaded up front (independent
+  // all per-Gaussian inputs are loaded up front (independent loads whose
+  // latencies overlap) ...
+  const double* pg = screen + 9 * i;
+  double pgv[9];
+#pragma unroll
+  for (int k = 0; k < 9; k++) pgv[k] = pg[k];
+  const float p_lg = gs.logits[i];
+  const float p_c[3] = {gs.centers[3 * i], gs.centers[3 * i + 1], gs.centers[3 * i + 2]};
+  const float p_dc[3] = {gs.colors_dc[3 * i], gs.colors_dc[3 * i + 1], gs.colors_dc[3 * i + 2]};
+  const float p_q[4] = {gs.rotations[4 * i], gs.rotations[4 * i + 1], gs.rotations[4 * i + 2], gs.rotations[4 * i + 3]};
+  const float p_ls[3] = {gs.log_scales[3 * i], gs.log_scales[3 * i + 1], gs.log_scales[3 * i + 2]};
+  float rr[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (gs.colors_rest)
+#pragma unroll
+    for (int k = 0; k < 9; k++) rr[k] = gs.colors_rest[9 * i + k];
+  // ... and for accumulation every old gradient value too (independent
   // loads, overlapping the arithmetic) instead of 24 serialised
   // read-modify-writes through possibly aliasing pointers
   float o_lg = 0.f, o_dn = 0.f, o_c[3] = {0.f, 0.f, 0.f}, o_s[3] = {0.f, 0.f, 0.f}, o_dc[3] = {0.f, 0.f, 0.f};
@@ -400,29 +415,27 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
       for (int k = 0; k < 9; k++) o_rest[k] = *(out.colors_rest + 9 * i + k);
   }
   auto put = [&](float* dst, int64_t idx, double v, float old) { dst[idx] = old + (float)(v * scale); };
-  const double* pg = screen + 9 * i;
-  const double gm0 = pg[0], gm1 = pg[1];
-  const double gcov[4] = {pg[2], pg[3], pg[3], pg[4]};
-  const double ga = pg[5];
+  const double gm0 = pgv[0], gm1 = pgv[1];
+  const double gcov[4] = {pgv[2], pgv[3], pgv[3], pgv[4]};
+  const double ga = pgv[5];
   const double fx = cc.fx, fy = cc.fy;
   const double* Rw = cc.R;
   // opacity: sigma = alpha G, alpha = sigmoid(logit)   (render.py:199-200)
-  const double alpha = 1.0 / (1.0 + exp(-(double)gs.logits[i]));
+  const double alpha = 1.0 / (1.0 + exp(-(double)p_lg));
   put(out.logits, i, ga * alpha * (1.0 - alpha), o_lg);
   // colour (render.py:202-220)
-  const double c0 = gs.centers[3 * i], c1 = gs.centers[3 * i + 1], c2 = gs.centers[3 * i + 2];
+  const double c0 = p_c[0], c1 = p_c[1], c2 = p_c[2];
   double pre[3], gpre[3], gc[3] = {0.0, 0.0, 0.0};
-  for (int ch = 0; ch < 3; ch++) pre[ch] = 0.5 + SH_C0 * (double)gs.colors_dc[3 * i + ch];
+  for (int ch = 0; ch < 3; ch++) pre[ch] = 0.5 + SH_C0 * (double)p_dc[ch];
   if (gs.colors_rest) {
     const double d0 = c0 - cc.center[0], d1 = c1 - cc.center[1], d2 = c2 - cc.center[2];
     const double dist = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
     const double den = fmax(dist, 1e-12);
     const double rden = 1.0 / den;
     const double x = d0 * rden, y = d1 * rden, z = d2 * rden;
-    const float* rr = gs.colors_rest + 9 * i;
     for (int ch = 0; ch < 3; ch++)
       pre[ch] = pre[ch] + SH_C1 * ((-y * (double)rr[ch] + z * (double)rr[3 + ch]) - x * (double)rr[6 + ch]);
-    for (int ch = 0; ch < 3; ch++) gpre[ch] = pg[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
+    for (int ch = 0; ch < 3; ch++) gpre[ch] = pgv[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
     for (int ch = 0; ch < 3; ch++) {
       put(out.colors_rest, 9 * i + 0 * 3 + ch, -SH_C1 * y * gpre[ch], o_rest[ch]);
       put(out.colors_rest, 9 * i + 1 * 3 + ch, SH_C1 * z * gpre[ch], o_rest[3 + ch]);
@@ -437,7 +450,7 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
     const double rdist = 1.0 / dist;
     for (int j = 0; j < 3; j++) gc[j] += (gd[j] - dv[j] * dd) * rdist;
   } else {
-    for (int ch = 0; ch < 3; ch++) gpre[ch] = pg[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
+    for (int ch = 0; ch < 3; ch++) gpre[ch] = pgv[6 + ch] * (pre[ch] > 0.0 ? 1.0 : 0.0);
   }
   for (int ch = 0; ch < 3; ch++) put(out.colors_dc, 3 * i + ch, SH_C0 * gpre[ch], o_dc[ch]);
   // forward intermediates (render.py:222-248)
@@ -450,10 +463,10 @@ __device__ __noinline__ void chain_one(const ChainCam& cc, const hgs_gaussians& 
   const double in_x = fabs(rx_raw) < cc.limx ? 1.0 : 0.0, in_y = fabs(ry_raw) < cc.limy ? 1.0 : 0.0;
   const double J[6] = {fx * rtz, 0.0, -fx * rx * rtz, 0.0, fy * rtz, -fy * ry * rtz};
   double q[4], Rq[9], qn[4], nrm;
-  for (int k = 0; k < 4; k++) q[k] = gs.rotations[4 * i + k];
+  for (int k = 0; k < 4; k++) q[k] = p_q[k];
   quat_rot(q, Rq, qn, nrm);
   double s[3], M[9], sig[9], A[6];
-  for (int j = 0; j < 3; j++) s[j] = exp((double)gs.log_scales[3 * i + j]);
+  for (int j = 0; j < 3; j++) s[j] = exp((double)p_ls[j]);
   for (int a = 0; a < 3; a++)
     for (int b = 0; b < 3; b++) M[a * 3 + b] = Rq[a * 3 + b] * s[b];
   for (int a = 0; a < 3; a++)
