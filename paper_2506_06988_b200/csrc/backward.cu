@@ -32,9 +32,6 @@ namespace hgs {
 #ifndef HGS_BW_MINB
 #define HGS_BW_MINB 6  // 64 registers: 6 CTAs (24 consumer warps) per SM; 4 -> 6 was -2.8 % per c4 step
 #endif
-#ifndef HGS_BW_EXP
-#define HGS_BW_EXP 0
-#endif
 constexpr int BW_BATCH = HGS_BW_BATCH;
 constexpr int BW_NSTAGE = HGS_BW_NSTAGE;
 constexpr int BW_CONSUMERS = 4;  // 8x8-pixel sub-tiles, two pixels per lane
@@ -338,16 +335,8 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
       bw_pixel_step(q1, E, lo + i, fx, fy1, v);
       const bool any = v[6] != 0.0f || v[7] != 0.0f || v[8] != 0.0f || v[5] != 0.0f || v[0] != 0.0f;
       if (!__any_sync(0xffffffffu, any)) continue;
-#if HGS_BW_EXP == 2
-      if (v[0] + v[1] + v[2] + v[3] + v[4] + v[5] + v[6] + v[7] + v[8] == 12345.0f) screen[lane] = 1.0;
-#else
       const float tot = warp_reduce9(v, lane);
-#if HGS_BW_EXP == 1
-      if (tot == 12345.0f) screen[lane] = 1.0;
-#else
       if (vidx >= 0 && tot != 0.0f) atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
-#endif
-#endif
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
