@@ -108,7 +108,12 @@ typedef struct hgs_projected {
 /* TileBins (splat/tiles.py:19-32).  entries hold ORIGINAL Gaussian rows in
    (tile, depth, row) order == np.lexsort((kept, depth, tile)) (tiles.py:65).
    counters (device, int64[4]): [0] M visible rows, [1] K entries, [2]
-   overflow flag (K > capacity; entries/tile_starts are then invalid). */
+   overflow flag (K > capacity; entries/tile_starts are then invalid).  All
+   counts stay on the device, so a frame can be enqueued (or captured into a
+   CUDA graph) without a host round trip; on overflow the binning scatter,
+   hgs_blend_forward, hgs_blend_backward and hgs_render_depth read the flag
+   and do nothing (no access past `entries`): grow the buffer to >= K and
+   re-enqueue. */
 typedef struct hgs_tiles {
   int32_t tiles_x, tiles_y, tile_px;
   int32_t reserved;
