@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
 // the full 64-bit depth key (runs are rare and short; long runs of exactly
 // equal depths are already ordered and only verified).
 __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ rows,
-                                                          const BlendRec* __restrict__ rec, const int64_t* counters,
+                                                          const uint64_t* __restrict__ sort_keys, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax) {
   pdl_enter();
   const int64_t m = counters[0];
@@ -135,7 +135,9 @@ __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __rest
     if (j + 1 >= m || k32[j + 1] != kj) continue;   // singleton
     int64_t e = j + 1;
     while (e < m && k32[e] == kj) e++;
-    auto key64 = [&](uint32_t row) { return (unsigned long long)__double_as_longlong(rec[row].depth); };
+    // full keys by row from the 8-byte sort_keys array (the fp64 depth bit
+    // pattern preprocess wrote; L2-resident) rather than the 80-byte records
+    auto key64 = [&](uint32_t row) { return (unsigned long long)__ldg(sort_keys + row); };
     bool sorted = true;
     for (int64_t t = j + 1; t < e && sorted; t++) {
       const unsigned long long a = key64(rows[t - 1]), b = key64(rows[t]);
@@ -1112,7 +1114,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                                    DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr, st,
                                    &k32res, true, &rows);
   if (rc) return rc;
-  launch_pdl(depth_fixup_kernel, dim3(4 * sm_count()), dim3(256), 0, st, k32res, rows, (const BlendRec*)proj->rec, tiles->counters,
+  launch_pdl(depth_fixup_kernel, dim3(4 * sm_count()), dim3(256), 0, st, k32res, rows, (const uint64_t*)proj->sort_keys, tiles->counters,
                                                      minmax);
   HGS_CHECK_LAUNCH();
   const int ss = super_shift(tx, ty);
