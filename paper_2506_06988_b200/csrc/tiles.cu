@@ -788,35 +788,25 @@ struct FineMask<4> {
   __device__ static bool bit(T m, int q) { return (m >> q) & 1u; }
   __device__ static uint32_t nibble(T m, int j) { return (m >> (4 * j)) & 0xFu; }
 };
-template <>
-struct FineMask<8> {
-  using T = unsigned long long;
-  __device__ static T of(ushort4 rc, int sx0, int sy0) {
-    const int lx0 = max((int)rc.x - sx0, 0), lx1 = min((int)rc.y - sx0, 7);
-    const int ly0 = max((int)rc.z - sy0, 0), ly1 = min((int)rc.w - sy0, 7);
-    if (lx0 > lx1 || ly0 > ly1) return 0ull;
-    const unsigned long long rowbits = (2ull << lx1) - (1ull << lx0);
-    const unsigned long long ymask = (ly1 == 7 ? 0ull : (1ull << (8 * (ly1 + 1)))) - (1ull << (8 * ly0));
-    return (rowbits * 0x0101010101010101ull) & ymask;
-  }
-  __device__ static bool bit(T m, int q) { return (m >> q) & 1ull; }
-  __device__ static uint32_t nibble(T m, int j) { return (uint32_t)(m >> (4 * j)) & 0xFu; }
-};
 
 template <int S>
 __global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
     const uint32_t* __restrict__ crow, const ushort4* __restrict__ crect, const uint32_t* __restrict__ cstart,
     const int64_t* __restrict__ tile_starts, const int64_t* counters, int64_t capacity, int tiles_x, int tiles_y,
-    int sx, uint32_t* __restrict__ entries) {
+    int sx, uint32_t* __restrict__ entries, int qs) {
   pdl_enter();
   constexpr int NT = S * S;
   using M = FineMask<S>;
   constexpr int FINE_WARPS = fine_warps(S);
   __shared__ uint32_t s_cnt[FINE_WARPS][NT];
   if (counters[1] > capacity) return;
-  const int s = blockIdx.x;
+  // qs > 0: the super-tiles are (S << qs)^2 tiles and 4^qs CTAs share one,
+  // each owning an S x S block of its tiles (every CTA reads the whole coarse
+  // list, writes only its own tiles' entries: no cross-CTA dependency)
+  const int s = blockIdx.x >> (2 * qs), quad = blockIdx.x & ((1 << (2 * qs)) - 1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sx0 = (s % sx) * S, sy0 = (s / sx) * S;
+  const int sx0 = (s % sx) * (S << qs) + (quad & ((1 << qs) - 1)) * S;
+  const int sy0 = (s / sx) * (S << qs) + (quad >> qs) * S;
   const uint32_t b = cstart[s], e = cstart[s + 1];
   const uint32_t per = ((e - b + FINE_WARPS - 1) / FINE_WARPS + 31) & ~31u;
   const uint32_t w0 = min(e, b + warp * per), w1 = min(e, w0 + per);
@@ -1145,14 +1135,10 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     launch_pdl(coarse_scatter_kernel, dim3(sgrid), dim3(BIN_THREADS), sizeof(ScatterSmem), st, ca, s.bin_mat, s.bin_slot, s.bin_wmat,
                                                                           s.crow, s.crect);
     HGS_CHECK_LAUNCH();
-    if (ss == 2)
-      launch_pdl(fine_bin_kernel<4>, dim3(n_super), dim3(fine_warps(4) * 32), 0, st, s.crow, s.crect, s.cstart, tiles->tile_starts,
-                                                              tiles->counters, tiles->capacity, tx, ty, sx,
-                                                              tiles->entries);
-    else if (ss == 3)
-      launch_pdl(fine_bin_kernel<8>, dim3(n_super), dim3(fine_warps(8) * 32), 0, st, s.crow, s.crect, s.cstart, tiles->tile_starts,
-                                                              tiles->counters, tiles->capacity, tx, ty, sx,
-                                                              tiles->entries);
+    if (ss == 2 || ss == 3)  // 8x8 super-tiles: four 4x4-tile CTAs each (parallelism at 1080p)
+      launch_pdl(fine_bin_kernel<4>, dim3(n_super << (2 * (ss - 2))), dim3(fine_warps(4) * 32), 0, st, s.crow,
+                 s.crect, s.cstart, tiles->tile_starts, tiles->counters, tiles->capacity, tx, ty, sx, tiles->entries,
+                 ss - 2);
     else
       return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large for binning");
     HGS_CHECK_LAUNCH();
