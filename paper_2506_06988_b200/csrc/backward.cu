@@ -3,12 +3,14 @@
 // _chain_to_parameters (splat/render.py:185-313) + densify statistic and
 // visibility (render.py:171-178).
 //
-// K5: one CTA per 16x16 tile, warp-specialised like the forward: 8 consumer
-// warps own 8x4 sub-tiles (one pixel per lane), 1 producer warp streams the
+// K5: one CTA per 16x16 tile, warp-specialised like the forward: 4 consumer
+// warps own 8x8 sub-tiles (two pixels per lane), 1 producer warp streams the
 // tile's entries NEWEST FIRST (from the largest `last` of the tile down to
-// the first entry) through a 4-stage cp.async/mbarrier ring.  Each pixel
+// the first entry) through a 3-stage x 64-entry cp.async/mbarrier ring
+// (64 registers: 6 CTAs per SM).  Each pixel
 // walks back from its last blended entry (kernels.py:120): T before an entry
-// is reconstructed by division, the suffix colour starts at T_final * (mesh
+// is reconstructed from T after it (one reciprocal of 1 - sigma: SFU
+// estimate + Newton step), the suffix colour starts at T_final * (mesh
 // colour or background), exactly as the reference.  Per-warp ellipse cull
 // as in the forward.  The per-entry 9-vector (mean2d 2, cov 3 full-matrix
 // convention, alpha, rgb 3) is reduced over the warp (reduce-scatter) and

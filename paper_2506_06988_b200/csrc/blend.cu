@@ -5,7 +5,7 @@
 // Fast path (blend_fast_kernel): one CTA per 16x16 tile, warp-specialised:
 // 8 consumer warps each own an 8x4 sub-tile (one pixel per lane), 1
 // producer warp streams the tile's depth-sorted entry list through a
-// 4-stage shared-memory ring (128 entries x 112 B per stage: 64 B of the
+// 2-stage shared-memory ring (128 entries x 112 B per stage: 64 B of the
 // fp64 blend record + the 48 B fp32 CullRec) with cp.async, completion
 // tracked by mbarriers (full: producer -> consumers, empty: consumers ->
 // producer).  Consumers never meet at a CTA barrier: each compacts every
@@ -15,8 +15,8 @@
 //
 // Numerics of the fast path (every decision equals the reference's):
 //  * the conic form m is evaluated in fp64 with FMAs and scaled to the exp2
-//    argument u = m log2(e)/2 in fp64; u is narrowed to fp32 with integer
-//    ops (no F2F).  The support test m > 9 / m < 0 is decided on u with a
+//    argument u = m log2(e)/2 in fp64; u is narrowed to fp32 (round to
+//    nearest).  The support test m > 9 / m < 0 is decided on u with a
 //    2^-20 relative guard band; inside the band (or for a conic flagged
 //    ill-conditioned by preprocess) the entry is re-evaluated exactly in the
 //    reference's operation order with fp64 exp() -- per entry, in place.
