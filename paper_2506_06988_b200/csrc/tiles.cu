@@ -391,7 +391,9 @@ constexpr int BIN_THREADS = 256;
 constexpr int BIN_WARPS = BIN_THREADS / 32;
 constexpr int BIN_PG = 1024;                 // depth-ordered rows per partition
 constexpr int BIN_SUB = BIN_PG / BIN_WARPS;  // rows per warp
-constexpr int BIN_MAX_SUPER = 256;           // super-tiles: one look-back digit per thread
+constexpr int BIN_MAX_SUPER = 512;           // super-tile capacity (two per thread in the scans);
+                                              // loops run to the frame's super-tile count
+static_assert(BIN_MAX_SUPER == 2 * BIN_THREADS, "coarse scans hold two super-tiles per thread");
 // warps per fine CTA (two CTAs per SM: the grid is one wave of super-tiles)
 __host__ __device__ constexpr int fine_warps(int S) { return S == 4 ? 16 : 8; }
 constexpr int FINE_DEPTH = 4;  // rounds of 32 list entries in flight per warp
@@ -623,23 +625,25 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_count_kernel(CoarseArgs a,
   const int nparts = (int)((P + CP_PART - 1) / CP_PART);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int part = blockIdx.x; part < nparts; part += gridDim.x) {
-    for (int i = threadIdx.x; i < BIN_WARPS * BIN_MAX_SUPER; i += BIN_THREADS) (&cnt[0][0])[i] = 0;
+#pragma unroll
+    for (int w = 0; w < BIN_WARPS; w++)
+      for (int t = threadIdx.x; t < a.ns; t += BIN_THREADS) cnt[w][t] = 0;
     __syncthreads();
     walk_pairs((uint32_t)part * BIN_WARPS + warp, P, m, a.pair_off, a.rsort, a.sorted_rows, a.wstart, a.ss, a.sx, lane,
                [&](bool valid, uint32_t sti, uint32_t, ushort4) {
                  if (valid) atomicAdd(&cnt[warp][sti], 1u);
                });
     __syncthreads();
-    if (threadIdx.x < a.ns) {  // per-warp exclusive prefix (for the scatter) and partition total
+    for (int t = threadIdx.x; t < a.ns; t += BIN_THREADS) {  // per-warp exclusive prefix (for the scatter) and total
       uint32_t acc = 0;
 #pragma unroll
       for (int w = 0; w < BIN_WARPS; w++) {
-        const uint32_t v = cnt[w][threadIdx.x];
-        wmat[((size_t)part * BIN_WARPS + w) * BIN_MAX_SUPER + threadIdx.x] = acc;
+        const uint32_t v = cnt[w][t];
+        wmat[((size_t)part * BIN_WARPS + w) * BIN_MAX_SUPER + t] = acc;
         acc += v;
       }
-      mat[(size_t)part * BIN_MAX_SUPER + threadIdx.x] = acc;
-      if (acc) atomicAdd(&hist[threadIdx.x], acc);
+      mat[(size_t)part * BIN_MAX_SUPER + t] = acc;
+      if (acc) atomicAdd(&hist[t], acc);
     }
     __syncthreads();
   }
@@ -699,13 +703,20 @@ __global__ void __launch_bounds__(1024) coarse_scan_kernel(const uint32_t* __res
 // rank) order, then written out as contiguous runs per super-tile
 // (coalesced: a random (row, super-tile) scatter would touch a fresh 32 B
 // sector per pair).
+// Dynamic shared memory: a fixed head followed by arrays sized by the
+// frame's super-tile count (nsp = ns rounded up to even), so a small grid
+// keeps the occupancy of the old fixed layout: lstart[nsp + 1] (partition-
+// local run starts), gslot[nsp] (global slot of each run), cnt[8][nsp]
+// (per-warp local positions).
 struct ScatterSmem {
   uint4 stage[CP_PART];                      // row, rect lo, rect hi, super-tile
-  uint32_t cnt[BIN_WARPS][BIN_MAX_SUPER];    // per-warp local positions
-  uint32_t lstart[BIN_MAX_SUPER + 1];        // partition-local run starts
-  uint32_t gslot[BIN_MAX_SUPER];             // global slot of each run
   uint32_t warp_tmp[8];
 };
+__host__ __device__ inline int scatter_nsp(int ns) { return (ns + 1) & ~1; }
+__host__ __device__ inline size_t scatter_smem_bytes(int ns) {
+  const int nsp = scatter_nsp(ns);
+  return sizeof(ScatterSmem) + sizeof(uint32_t) * (size_t)(nsp + 1 + nsp + BIN_WARPS * nsp);
+}
 
 __global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs a, const uint32_t* __restrict__ mat,
                                                                      const uint32_t* __restrict__ slot,
@@ -715,6 +726,10 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs 
   pdl_enter();
   extern __shared__ __align__(16) unsigned char sc_raw[];
   ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(sc_raw);
+  const int nsp = scatter_nsp(a.ns);
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(sc_raw + sizeof(ScatterSmem));
+  uint32_t* gslot = lstart + nsp + 1;
+  uint32_t* cnt = gslot + nsp;  // [warp * nsp + super-tile]
   const int64_t m = a.counters[0];
   if (a.counters[1] > a.capacity) return;
   const uint32_t P = *a.npairs;
@@ -722,39 +737,45 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int part = blockIdx.x; part < nparts; part += gridDim.x) {
     const uint32_t k = (uint32_t)part * BIN_WARPS + warp;
-    {  // partition-local run starts (exclusive scan over super-tiles; one per thread)
-      const uint32_t c = threadIdx.x < a.ns ? mat[(size_t)part * BIN_MAX_SUPER + threadIdx.x] : 0u;
+    {  // partition-local run starts (exclusive scan over super-tiles; two consecutive per thread)
+      const int t0 = 2 * threadIdx.x;
+      const size_t row = (size_t)part * BIN_MAX_SUPER;
+      const uint32_t c0 = t0 < a.ns ? mat[row + t0] : 0u, c1 = t0 + 1 < a.ns ? mat[row + t0 + 1] : 0u;
       uint32_t tot;
-      const uint32_t e = block_exclusive_scan<uint32_t>(c, sm.warp_tmp, tot);
-      sm.lstart[threadIdx.x] = e;
-      if (threadIdx.x == 0) sm.lstart[BIN_MAX_SUPER] = tot;
-      sm.gslot[threadIdx.x] = threadIdx.x < a.ns ? slot[(size_t)part * BIN_MAX_SUPER + threadIdx.x] : 0u;
+      const uint32_t e = block_exclusive_scan<uint32_t>(c0 + c1, sm.warp_tmp, tot);
+      if (t0 < nsp) {
+        lstart[t0] = e;
+        lstart[t0 + 1] = e + c0;
+        gslot[t0] = t0 < a.ns ? slot[row + t0] : 0u;
+        gslot[t0 + 1] = t0 + 1 < a.ns ? slot[row + t0 + 1] : 0u;
+      }
+      if (threadIdx.x == 0) lstart[nsp] = tot;
       __syncthreads();
     }
-    for (int i = threadIdx.x; i < BIN_WARPS * BIN_MAX_SUPER; i += BIN_THREADS) {
-      const int t = i % BIN_MAX_SUPER;
-      (&sm.cnt[0][0])[i] = t < a.ns ? sm.lstart[t] + wmat[(size_t)part * BIN_WARPS * BIN_MAX_SUPER + i] : 0u;
-    }
+#pragma unroll
+    for (int w = 0; w < BIN_WARPS; w++)
+      for (int t = threadIdx.x; t < a.ns; t += BIN_THREADS)
+        cnt[w * nsp + t] = lstart[t] + wmat[((size_t)part * BIN_WARPS + w) * BIN_MAX_SUPER + t];
     __syncthreads();
     walk_pairs(k, P, m, a.pair_off, a.rsort, a.sorted_rows, a.wstart, a.ss, a.sx, lane,
                [&](bool valid, uint32_t sti, uint32_t g, ushort4 rc) {
                  const unsigned peers = __match_any_sync(0xffffffffu, sti);
                  uint32_t cur = 0;
-                 if (valid) cur = sm.cnt[warp][sti];
+                 if (valid) cur = cnt[warp * nsp + sti];
                  __syncwarp();
                  if (valid) {
                    const uint32_t pos = cur + __popc(peers & lanemask_lt());
                    sm.stage[pos] = make_uint4(g, (uint32_t)rc.x | ((uint32_t)rc.y << 16),
                                               (uint32_t)rc.z | ((uint32_t)rc.w << 16), sti);
-                   if (lane == __ffs(peers) - 1) sm.cnt[warp][sti] = cur + __popc(peers);
+                   if (lane == __ffs(peers) - 1) cnt[warp * nsp + sti] = cur + __popc(peers);
                  }
                  __syncwarp();
                });
     __syncthreads();
-    const uint32_t n = sm.lstart[BIN_MAX_SUPER];
+    const uint32_t n = lstart[nsp];
     for (uint32_t i = threadIdx.x; i < n; i += BIN_THREADS) {
       const uint4 v = sm.stage[i];
-      const uint32_t pos = sm.gslot[v.w] + (i - sm.lstart[v.w]);
+      const uint32_t pos = gslot[v.w] + (i - lstart[v.w]);
       crow[pos] = v.x;
       crect_out[pos] = make_ushort4(v.y & 0xffffu, v.y >> 16, v.z & 0xffffu, v.z >> 16);
     }
@@ -1121,18 +1142,23 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                                                      s.wstart);
     HGS_CHECK_LAUNCH();
     CoarseArgs ca{rows, s.rsort, s.pair_off, s.wstart, s.npairs, tiles->counters, tiles->capacity, ss, sx, n_super};
-    static int cgrid = 0, sgrid = 0;
+    static int cgrid = 0, sgrid = 0, sgrid_ns = -1;
+    const size_t ssmem = scatter_smem_bytes(n_super);
     if (cgrid == 0) {
       cgrid = persistent_grid((const void*)coarse_count_kernel, BIN_THREADS, 0);
-      cudaFuncSetAttribute(coarse_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem));
-      sgrid = persistent_grid((const void*)coarse_scatter_kernel, BIN_THREADS, sizeof(ScatterSmem));
+      cudaFuncSetAttribute(coarse_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)scatter_smem_bytes(BIN_MAX_SUPER));
+    }
+    if (sgrid_ns != n_super) {  // occupancy depends on the super-tile count
+      sgrid = persistent_grid((const void*)coarse_scatter_kernel, BIN_THREADS, ssmem);
+      sgrid_ns = n_super;
     }
     launch_pdl(coarse_count_kernel, dim3(cgrid), dim3(BIN_THREADS), 0, st, ca, s.bin_mat, s.bin_wmat, s.chist);
     HGS_CHECK_LAUNCH();
     launch_pdl(coarse_scan_kernel, dim3((n_super + 31) / 32), dim3(1024), 0, st, s.bin_mat, s.chist, tiles->counters, tiles->capacity,
                                                              s.npairs, n_super, s.cstart, s.bin_slot);
     HGS_CHECK_LAUNCH();
-    launch_pdl(coarse_scatter_kernel, dim3(sgrid), dim3(BIN_THREADS), sizeof(ScatterSmem), st, ca, s.bin_mat, s.bin_slot, s.bin_wmat,
+    launch_pdl(coarse_scatter_kernel, dim3(sgrid), dim3(BIN_THREADS), ssmem, st, ca, s.bin_mat, s.bin_slot, s.bin_wmat,
                                                                           s.crow, s.crect);
     HGS_CHECK_LAUNCH();
     if (ss == 2 || ss == 3)  // 8x8 super-tiles: four 4x4-tile CTAs each (parallelism at 1080p)
