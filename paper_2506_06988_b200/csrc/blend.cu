@@ -107,7 +107,7 @@ __device__ __noinline__ float exact_entry(const StageEntry& E, double fx, double
   return sg < SIGMA_SKIP ? -1.0f : (float)sg;
 }
 
-// Exact walk of one pixel by one warp (fp64 exp()): lanes evaluate 32
+// Exact walk of one pixel by one warp (fp64 exp()): lanes evaluate
 // consecutive entries in parallel -- support test, exp, clamp, skip and
 // the mesh-depth stop exactly as kernels.py:38-51 -- then the chunk's
 // transmittance recurrence T <- T (1 - sigma) is evaluated as a shuffle
@@ -122,46 +122,84 @@ struct ExactPixel {
   double T, r, g, b, dacc;
   int64_t last;
 };
-__device__ __noinline__ ExactPixel exact_walk(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
-                                              int64_t s, int64_t e, double fx, double fy, double limit, int lane) {
+
+// The walk, two entries per lane per round (64 per warp iteration) with a
+// software pipeline (indices four rounds ahead, records two): lane L
+// evaluates entries base + 2L and base + 2L + 1, whose gathers and fp64
+// exp() overlap; T before each entry is T * (exclusive lane prefix product)
+// * (in-lane running product).  Decisions: the first mesh-
+// depth stop in entry order cuts the round; outside the 1e-12 band around the
+// early-stop threshold the first entry with T(1 - sigma) < 1e-4 ends the
+// walk; a round with a value inside the band is replayed serially in the
+// reference's order.
+__device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
+                                               int64_t s, int64_t e, double fx, double fy, double limit, int lane) {
+  constexpr int EW = 2, RW = 32 * EW;
   double T = 1.0, pr = 0.0, pg = 0.0, pb = 0.0, pd = 0.0;
   int64_t last = -1;
   bool done = false;
-  // software pipeline: entry indices four chunks ahead, records two ahead
-  // (one warp per pixel: registers are cheap, the gather latency is not)
-  uint32_t ix[4];
+  auto idx = [&](int64_t rbase, int u) -> uint32_t {
+    const int64_t k = rbase + EW * lane + u;
+    return k < e ? __ldg(entries + k) : 0u;
+  };
+  uint32_t ix[4][EW];
 #pragma unroll
-  for (int d = 0; d < 4; d++) ix[d] = (s + d * 32 + lane < e) ? __ldg(entries + s + d * 32 + lane) : 0u;
-  BlendRec r0, r1;
-  if (s + lane < e) r0 = rec[ix[0]];
-  if (s + 32 + lane < e) r1 = rec[ix[1]];
-  for (int64_t base = s; base < e && !done; base += 32) {
-    const int64_t k = base + lane;
-    const BlendRec c = r0;
-    r0 = r1;
-    if (base + 64 + lane < e) r1 = rec[ix[2]];
-    ix[0] = ix[1];
-    ix[1] = ix[2];
-    ix[2] = ix[3];
-    if (base + 128 + lane < e) ix[3] = __ldg(entries + base + 128 + lane);
-    bool stop = false, use = false;
-    double sig = 0.0;
-    if (k < e) {
-      stop = c.depth >= limit;
-      const double dx = fx - c.mx, dy = fy - c.my;
-      const double m = c.ca * dx * dx + c.cb2 * dx * dy + c.cc * dy * dy;
-      if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
-        sig = c.alpha * exp(-0.5 * m);
-        if (sig > ALPHA_CLAMP) sig = ALPHA_CLAMP;
-        use = !(sig < SIGMA_SKIP);
+  for (int d = 0; d < 4; d++)
+#pragma unroll
+    for (int u = 0; u < EW; u++) ix[d][u] = idx(s + (int64_t)d * RW, u);
+  BlendRec r0[EW], r1[EW];
+#pragma unroll
+  for (int u = 0; u < EW; u++) {
+    if (s + EW * lane + u < e) r0[u] = rec[ix[0][u]];
+    if (s + RW + EW * lane + u < e) r1[u] = rec[ix[1][u]];
+  }
+  for (int64_t base = s; base < e && !done; base += RW) {
+    BlendRec c[EW];
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      c[u] = r0[u];
+      r0[u] = r1[u];
+      if (base + 2 * RW + EW * lane + u < e) r1[u] = rec[ix[2][u]];
+      ix[0][u] = ix[1][u];
+      ix[1][u] = ix[2][u];
+      ix[2][u] = ix[3][u];
+      ix[3][u] = idx(base + 4 * RW, u);
+    }
+    double sig[EW];
+    bool use[EW];
+    int us = EW;  // first depth stop of this lane
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      const int64_t k = base + EW * lane + u;
+      use[u] = false;
+      sig[u] = 0.0;
+      if (k < e) {
+        if (c[u].depth >= limit && us == EW) us = u;
+        const double dx = fx - c[u].mx, dy = fy - c[u].my;
+        const double m = c[u].ca * dx * dx + c[u].cb2 * dx * dy + c[u].cc * dy * dy;
+        if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
+          double sg = c[u].alpha * exp(-0.5 * m);
+          if (sg > ALPHA_CLAMP) sg = ALPHA_CLAMP;
+          use[u] = !(sg < SIGMA_SKIP);
+          sig[u] = sg;
+        }
       }
     }
-    const unsigned stop_mask = __ballot_sync(0xffffffffu, stop);
-    const int first_stop = stop_mask ? __ffs(stop_mask) - 1 : 32;
-    if (lane >= first_stop) use = false;
-    if (first_stop < 32) done = true;
-    // inclusive prefix product of the (1 - sigma) factors
-    double P = use ? 1.0 - sig : 1.0;
+    const unsigned smask = __ballot_sync(0xffffffffu, us < EW);
+    const int ls = smask ? __ffs(smask) - 1 : 32;
+    const int lsu = __shfl_sync(0xffffffffu, us, ls & 31);
+#pragma unroll
+    for (int u = 0; u < EW; u++)
+      if (lane > ls || (lane == ls && u >= lsu)) use[u] = false;
+    if (ls < 32) done = true;
+    double f[EW];
+    double q = 1.0;
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      f[u] = use[u] ? 1.0 - sig[u] : 1.0;
+      q *= f[u];
+    }
+    double P = q;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const double t = __shfl_up_sync(0xffffffffu, P, d);
@@ -169,40 +207,71 @@ __device__ __noinline__ ExactPixel exact_walk(const BlendRec* __restrict__ rec, 
     }
     double Pex = __shfl_up_sync(0xffffffffu, P, 1);
     if (lane == 0) Pex = 1.0;
-    const double t_after = T * P;
-    const bool near = use && fabs(t_after - EARLY_STOP_T) <= 1e-12 * EARLY_STOP_T;
-    double w = 0.0;
+    double ta[EW];
+    double run = T * Pex;
+    bool near = false;
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      run *= f[u];
+      ta[u] = run;
+      near = near || (use[u] && fabs(run - EARLY_STOP_T) <= 1e-12 * EARLY_STOP_T);
+    }
     if (!__any_sync(0xffffffffu, near)) {
-      const unsigned smask = __ballot_sync(0xffffffffu, use && t_after < EARLY_STOP_T);
-      const int kstop = smask ? __ffs(smask) - 1 : 32;
-      const bool valid = use && lane < kstop;
-      if (valid) w = sig * (T * Pex);
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      int ue = EW;
+#pragma unroll
+      for (int u = 0; u < EW; u++)
+        if (use[u] && ta[u] < EARLY_STOP_T && ue == EW) ue = u;
+      const unsigned emask = __ballot_sync(0xffffffffu, ue < EW);
+      const int le = emask ? __ffs(emask) - 1 : 32;
+      const int leu = __shfl_sync(0xffffffffu, ue, le & 31);
+      int lastu = -1;
+      double tb = T * Pex, tl = 0.0;
+#pragma unroll
+      for (int u = 0; u < EW; u++) {
+        const bool valid = use[u] && (lane < le || (lane == le && u < leu));
+        if (valid) {
+          const double w = sig[u] * tb;
+          pr += c[u].r * w;
+          pg += c[u].g * w;
+          pb += c[u].b * w;
+          pd += c[u].depth * w;
+          lastu = u;
+          tl = ta[u];
+        }
+        tb = ta[u];
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, lastu >= 0);
       if (vmask) {
         const int lv = 31 - __clz(vmask);
-        T = __shfl_sync(0xffffffffu, t_after, lv);
-        last = base + lv;
+        T = __shfl_sync(0xffffffffu, tl, lv);
+        last = base + (int64_t)EW * lv + __shfl_sync(0xffffffffu, lastu, lv);
       }
-      if (kstop < 32) done = true;
+      if (le < 32) done = true;
     } else {
-      // serial replay of this chunk in the reference's order
-      unsigned use_mask = __ballot_sync(0xffffffffu, use);
-      while (use_mask) {
-        const int i = __ffs(use_mask) - 1;
-        use_mask &= use_mask - 1;
-        const double sg = __shfl_sync(0xffffffffu, sig, i);
-        const double test_t = T * (1.0 - sg);
-        if (test_t < EARLY_STOP_T) { done = true; break; }
-        if (lane == i) w = sg * T;
-        T = test_t;
-        last = base + i;
+      bool stop = false;
+      for (int i = 0; i < 32 && !stop; i++) {
+#pragma unroll
+        for (int u = 0; u < EW; u++) {
+          const bool ui = __shfl_sync(0xffffffffu, use[u], i);
+          if (!ui || stop) continue;
+          const double sg = __shfl_sync(0xffffffffu, sig[u], i);
+          const double test_t = T * (1.0 - sg);
+          if (test_t < EARLY_STOP_T) {
+            stop = true;
+            continue;
+          }
+          if (lane == i) {
+            const double w = sg * T;
+            pr += c[u].r * w;
+            pg += c[u].g * w;
+            pb += c[u].b * w;
+            pd += c[u].depth * w;
+          }
+          T = test_t;
+          last = base + (int64_t)EW * i + u;
+        }
       }
-    }
-    if (w != 0.0) {  // (lanes past the list end hold no record)
-      pr += c.r * w;
-      pg += c.g * w;
-      pb += c.b * w;
-      pd += c.depth * w;
+      if (stop) done = true;
     }
   }
 #pragma unroll
@@ -477,7 +546,7 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
     const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
     const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
     const double limit = mesh_here ? mesh.depth[p] : __longlong_as_double(0x7ff0000000000000LL);
-    const ExactPixel q = exact_walk(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5,
+    const ExactPixel q = exact_walk2(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5,
                                     limit, lane);
     if (lane == 0)
       write_pixel(out, mesh, mesh_here, p, q.T, q.r, q.g, q.b, q.dacc, 1.0 - q.T, q.last, bg0, bg1, bg2,
@@ -553,7 +622,7 @@ namespace hgs {
 // evaluate 32 consecutive entries exactly as the reference (support test,
 // exp, clamp, skip), the chunk's transmittance is an inclusive shuffle
 // prefix product of (1 - sigma) (|rel. diff| < 1e-13 from the serial
-// product, see exact_walk), and a chunk whose products fall within 1e-12 of
+// product, see exact_walk2), and a chunk whose products fall within 1e-12 of
 // either threshold (0.5, or the 1e-4 early stop) is replayed serially in the
 // reference's order, so every decision is the reference's.
 __global__ void __launch_bounds__(256) depth_walk_kernel(const BlendRec* __restrict__ rec,
