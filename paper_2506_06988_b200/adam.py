@@ -6,7 +6,6 @@ modes."""
 
 from __future__ import annotations
 
-import ctypes
 import math
 from typing import Dict, Iterable, Optional
 

@@ -21,8 +21,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .scene import CAMERA_BYTES, Camera, GaussianSet, TexturedMesh, camera_struct
-from .splat import (REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, TileBins, _c_f64_3, _stream_ptr,
+from .scene import CAMERA_BYTES, GaussianSet, TexturedMesh, camera_struct
+from .splat import (REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, TileBins, _c_f64_3,
                     MASK_VARIANTS)
 
 

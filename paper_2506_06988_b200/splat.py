@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .scene import (Camera, GaussianSet, RenderOutputs, camera_struct, camera_tensor, default_device)
+from .scene import (Camera, GaussianSet, RenderOutputs, camera_tensor, default_device)
 
 # splat/project.py:19-27, tiles.py:16
 COV_FLOOR = 0.3

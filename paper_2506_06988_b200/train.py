@@ -29,8 +29,7 @@ from .backward import GradBuffer, chain_backward, screen_backward
 from .losses import composite_loss
 from .meshraster import MeshFragmentBuffer, rasterize_fragments
 from .scene import Camera, GaussianSet, TexturedMesh, camera_tensor
-from .splat import (REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, RenderCtx, TileBins, _blend, _stream_ptr,
-                    SCRATCH)
+from .splat import REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, RenderCtx, TileBins, _blend, _stream_ptr
 
 
 def shard_views(n_views: int, rank: int, world: int) -> List[int]:
