@@ -54,3 +54,34 @@ def test_train_driver_matches_reference_trajectory(cuda_device, tmp_path):
     assert len(g2) == res.final["n_gaussians"]
     st = fileio.load_optimizer_state(tmp_path / "optimizer_state.bin")
     assert st["step"] == 12
+
+
+def test_trainer_lanes_match_single_stream(cuda_device):
+    """HybridTrainer's 4-lane schedule (views overlapped on streams, chain
+    accumulation ordered by events) gives the single-stream step: same loss,
+    parameters equal up to fp64-atomic ordering in the blend backward."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import synthetic as syn
+    from paper_2506_06988_b200.config import TrainConfig
+    from paper_2506_06988_b200.train import HybridTrainer
+    sc = syn.make_config("c2", seed=0)
+    rng = np.random.default_rng(3)
+    views = [syn.look_at((0.2 * k, -0.1, -0.2), (0.0, 0.0, 5.0), width=320, height=240) for k in range(6)]
+    cams = [hgs.Camera.from_any(v) for v in views]
+    images = [torch.as_tensor(rng.uniform(0, 1, (240, 320, 3)), dtype=torch.float32) for _ in cams]
+    results = []
+    for lanes in (1, 4):
+        HybridTrainer.N_LANES = lanes
+        try:
+            gs = hgs.GaussianSet.from_any(sc.gaussians)
+            mesh = hgs.TexturedMesh.from_any(sc.mesh)
+            tr = HybridTrainer(gs, mesh, cams, images, TrainConfig())
+            loss = tr.step(TrainConfig().warmup_iters + 1, list(range(len(cams))))
+            results.append((loss.cpu().numpy(), tr.gs.params.detach().cpu().numpy().copy(),
+                            mesh.texture.detach().cpu().numpy().copy()))
+        finally:
+            HybridTrainer.N_LANES = 4
+    (l1, p1, t1), (l4, p4, t4) = results
+    assert np.allclose(l1, l4, rtol=1e-9, atol=1e-12)
+    assert np.abs(p1 - p4).max() < 1e-6
+    assert np.abs(t1 - t4).max() < 1e-6
