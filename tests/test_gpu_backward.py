@@ -242,3 +242,46 @@ def test_c3_frame_and_backward_match_oracle(cuda_device):
         bound = max(1e-4, 2e-6 * np.abs(b).max())
         err = np.abs(a - b).max()
         assert err <= bound, f"{k}: max abs err {err:.3e} > {bound:.3e} (scale {np.abs(b).max():.3g})"
+
+
+def test_c2_sh1_forward_backward_match_oracle(cuda_device):
+    """c2 scale with SH degree 1 (view-dependent colour, project.py:56-67):
+    kept set, blend order, image and every gradient group incl. colors_rest
+    against the oracle."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    from paper_2506_06988_b200 import synthetic as syn
+    sc = syn.make_config("c2", seed=1, sh_degree=1)
+    assert sc.gaussians.colors_rest is not None
+    cam = sc.cameras[0]
+    g, c, m = dev_scene(sc.gaussians, cam, sc.mesh)
+    rng = np.random.default_rng(9)
+    gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
+    gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
+    color, depth, tt, octx = orc.render(sc.gaussians, cam, (0.1, 0.2, 0.3), _mesh_oracle(sc.gaussians, cam, sc.mesh))
+    og = orc.backward(octx, gc, gt)
+    layer = mr.mesh_layer(m, c)
+    out, ctx = hgs.render(g, c, background=(0.1, 0.2, 0.3), mesh=layer)
+    assert np.array_equal(ctx.last_consumed.cpu().numpy(), octx["last"])
+    assert np.abs(np_(out.color) - color).max() < 1e-5
+    assert np.abs(np_(out.transmittance) - tt).max() < 1e-5
+    gr = hgs.rasterize_backward(ctx, gc, gt)
+    for k in GROUPS + ("colors_rest",):
+        grad_close(np_(getattr(gr, k)), getattr(og, k), atol=1e-4, scale_tol=1e-4, what=k)
+
+
+@pytest.mark.parametrize("variant", ["sigmoid", "identity_t", "constant_one", "constant_zero"])
+def test_engine_mask_epilogue_matches_oracle(variant, cuda_device):
+    """The transmittance-mask epilogue fused into the blend (losses.py:79-91)
+    against the oracle's mask of the oracle's T, at c2 scale."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import synthetic as syn
+    from paper_2506_06988_b200.engine import HybridRenderer
+    sc = syn.make_config("c2", seed=0)
+    cam = sc.cameras[0]
+    g, c, m = dev_scene(sc.gaussians, cam, sc.mesh)
+    _, _, tt, _ = orc.render(sc.gaussians, cam, (0, 0, 0), _mesh_oracle(sc.gaussians, cam, sc.mesh))
+    r = HybridRenderer(g, m, c.width, c.height, mask=(variant, 20.0))
+    r.frame(c, sync_check=True)
+    ref = orc.transmittance_mask(tt, 20.0, variant)
+    assert np.abs(np_(r.mask_out) - ref).max() < 1e-5
