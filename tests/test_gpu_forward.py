@@ -329,3 +329,32 @@ def test_c4_training_view_matches_oracle(view, cuda_device):
     # ~1e-6 here (north_star tolerance: 1e-4)
     assert_close(np_(out.color), color, atol=1e-5, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+
+
+def test_pdl_launch_chain_does_not_change_results(cuda_device, tmp_path):
+    """The programmatic-dependent-launch chain (HGS_PDL, read once per
+    process) only changes scheduling: a c2 engine frame rendered in a
+    subprocess with HGS_PDL=0 equals this process's (PDL on) bit for bit."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "frame.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {repr(os.path.abspath(os.path.join(os.path.dirname(__file__), '..')))})\n"
+        "import paper_2506_06988_b200 as hgs\n"
+        "from paper_2506_06988_b200 import synthetic as syn\n"
+        "from paper_2506_06988_b200.engine import HybridRenderer\n"
+        "sc = syn.make_config('c2', seed=0)\n"
+        "g = hgs.GaussianSet.from_any(sc.gaussians); m = hgs.TexturedMesh.from_any(sc.mesh)\n"
+        "c = hgs.Camera.from_any(sc.cameras[0])\n"
+        "r = HybridRenderer(g, m, c.width, c.height); r.frame(c, sync_check=True); r.capture(); r.replay()\n"
+        "torch.cuda.synchronize()\n"
+        "np.save(sys.argv[1], np.concatenate([r.color.cpu().numpy().ravel(), r.trans.cpu().numpy().ravel()]))\n")
+    out_off = tmp_path / "off.npy"
+    out_on = tmp_path / "on.npy"
+    env = dict(os.environ, HGS_PDL="0")
+    subprocess.run([sys.executable, str(script), str(out_off)], env=env, check=True, timeout=600)
+    env_on = {k: v for k, v in os.environ.items() if k != "HGS_PDL"}
+    subprocess.run([sys.executable, str(script), str(out_on)], env=env_on, check=True, timeout=600)
+    assert np.array_equal(np.load(out_off), np.load(out_on))
