@@ -319,7 +319,7 @@ def run_ours(args):
     e2e_value = frames_total / (e2e_ms * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
             "config": {"workload": f"{args.config}: full hybrid frame (mesh raster + texture + project + tiles + blend)",
                        "gaussians": len(gs), "visible": m_vis, "tile_entries": k_entries, "triangles": mesh.n_faces,
                        "texture": list(mesh.texture.shape), "resolution": [W, H],
