@@ -320,6 +320,8 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "dtype_note": "projection, depth order, raster and every blend decision in fp64; blend weights / colour "
+                          "sums in fp32 with an error bound (exact fp64 replay where a decision is ambiguous)",
             "config": {"workload": f"{args.config}: full hybrid frame (mesh raster + texture + project + tiles + blend)",
                        "gaussians": len(gs), "visible": m_vis, "tile_entries": k_entries, "triangles": mesh.n_faces,
                        "texture": list(mesh.texture.shape), "resolution": [W, H],
