@@ -111,14 +111,13 @@ def test_init_texture_modes(cuda_device):
 
 def test_gradients_match_finite_differences(cuda_device):
     """Analytic gradients of L = sum(g . colour) + sum(g_T . T) against
-    central finite differences of the device forward, for the parameters of
-    the most visible Gaussians (reference test_gaussian_param_gradient_
-    through_full_loss / test_matches_finite_differences, independent of the
-    oracle).  Only parameters the image depends on smoothly: the DC colour
-    (linear) and the opacity logit.  The reference's gradients (which the
-    oracle tests match at c2-c5) do not differentiate through the support
-    cutoff m <= 9, the 1/255 skip or the early stop, so finite differences
-    of positions / scales in a dense scene include those jumps."""
+    finite differences of the device forward for the most visible Gaussians
+    (reference test_gaussian_param_gradient_through_full_loss /
+    test_matches_finite_differences; independent of the oracle).  The
+    reference's gradients do not differentiate through the support cutoff
+    m <= 9, the 1/255 skip or the early stop, so a parameter whose two
+    one-sided differences disagree sits next to such a jump and is skipped;
+    every smooth parameter must match, and most parameters must be smooth."""
     import paper_2506_06988_b200 as hgs
     sc = syn.small_scene(seed=13, n=120, width=64, height=48, with_mesh=False)
     cam = sc.cameras[0]
@@ -130,19 +129,21 @@ def test_gradients_match_finite_differences(cuda_device):
 
     def loss(h):
         out, _ = hgs.render(*_dev(h, cam)[:2], background=bg)
-        return float((_np(out.color).astype(np.float64) * gc).sum() + (_np(out.transmittance).astype(np.float64) * gt).sum())
+        return float((_np(out.color).astype(np.float64) * gc).sum() +
+                     (_np(out.transmittance).astype(np.float64) * gt).sum())
 
     g, c, _ = _dev(gs, cam)
     _, ctx = hgs.render(g, c, background=bg)
     gr = hgs.rasterize_backward(ctx, torch.as_tensor(gc, dtype=torch.float32, device="cuda"),
                                 torch.as_tensor(gt, dtype=torch.float32, device="cuda"))
-    # the Gaussians with the largest opacity gradient are well inside the image
+    l0 = loss(gs)
     order = np.argsort(-np.abs(_np(gr.logit_opacities)))[:4]
-    checked = 0
+    eps = 2.5e-4
+    smooth = total = 0
     for i in order:
-        for group, j in (("logit_opacities", None), ("colors_dc", 0), ("colors_dc", 1), ("colors_dc", 2)):
-            eps = 2e-3
-            vals = []
+        for group, j in (("centers", 0), ("centers", 1), ("centers", 2), ("log_scales", 0), ("log_scales", 1),
+                         ("rotations", 1), ("logit_opacities", None), ("colors_dc", 0), ("colors_dc", 2)):
+            one = []
             for sgn in (1, -1):
                 h = syn.HostGaussians(gs.centers.copy(), gs.rotations.copy(), gs.log_scales.copy(),
                                       gs.logit_opacities.copy(), gs.colors_dc.copy(), None)
@@ -151,9 +152,12 @@ def test_gradients_match_finite_differences(cuda_device):
                     arr[i] += sgn * eps
                 else:
                     arr[i, j] += sgn * eps
-                vals.append(loss(h))
-            fd = (vals[0] - vals[1]) / (2 * eps)
+                one.append(sgn * (loss(h) - l0) / eps)
+            total += 1
+            if abs(one[0] - one[1]) > 0.05 * max(1.0, abs(one[0]), abs(one[1])):
+                continue  # a blend decision changes within +-eps: no derivative there
+            smooth += 1
+            fd = 0.5 * (one[0] + one[1])
             an = float(_np(getattr(gr, group))[i] if j is None else _np(getattr(gr, group))[i, j])
             assert abs(an - fd) <= 2e-2 * max(1.0, abs(fd)), f"{group}[{i},{j}]: analytic {an:.5g} vs fd {fd:.5g}"
-            checked += 1
-    assert checked == 16
+    assert smooth >= 0.75 * total, f"only {smooth} of {total} parameters smooth"
