@@ -161,3 +161,58 @@ def test_gradients_match_finite_differences(cuda_device):
             an = float(_np(getattr(gr, group))[i] if j is None else _np(getattr(gr, group))[i, j])
             assert abs(an - fd) <= 2e-2 * max(1.0, abs(fd)), f"{group}[{i},{j}]: analytic {an:.5g} vs fd {fd:.5g}"
     assert smooth >= 0.75 * total, f"only {smooth} of {total} parameters smooth"
+
+
+def test_composite_loss_gradients_match_finite_differences(cuda_device):
+    """d(total loss)/d(rendered pixel), d/d(mesh colour) and d/d(T) from
+    composite_loss against finite differences of its own scalar (L1 +
+    D-SSIM + masked texture term, losses.py:139-174; reference
+    test_gradient_matches_fd / test_gradients_match_fd)."""
+    from paper_2506_06988_b200 import losses
+
+    class Cfg:
+        dssim_weight = 0.2
+        zero_dssim_after_densify = False
+        densify_until_iter = 1500
+        warmup_iters = 300
+        texture_weight = 0.5
+        mask_sharpness = 20.0
+        mask_variant = "sigmoid"
+
+    rng = np.random.default_rng(7)
+    h, w = 40, 48
+    gt = rng.uniform(0, 1, (h, w, 3))
+    ih = np.clip(gt + rng.normal(0, 0.2, gt.shape), 0, 1)
+    im = np.clip(gt + rng.normal(0, 0.2, gt.shape), 0, 1)
+    tri = np.where(rng.uniform(size=(h, w)) < 0.7, 1, -1).astype(np.int32)
+    tt = rng.uniform(0.05, 0.95, (h, w))
+    it = Cfg.warmup_iters + 1
+    dev = lambda a, dt=torch.float32: torch.as_tensor(a, dtype=dt, device="cuda")  # noqa: E731
+
+    def total(a, b, t):
+        bd, *_ = losses.composite_loss(dev(gt), dev(a), dev(b), dev(tri, torch.int32), dev(t), it, Cfg)
+        return bd.total
+
+    bd, g_ih, g_im, g_t = losses.composite_loss(dev(gt), dev(ih), dev(im), dev(tri, torch.int32), dev(tt), it, Cfg)
+    g_ih, g_im, g_t = _np(g_ih), _np(g_im), _np(g_t)
+    eps = 1e-3
+    picks = [(5, 7, 0), (20, 30, 1), (33, 3, 2), (12, 40, 1)]
+    for y, x, ch in picks:
+        if abs(ih[y, x, ch] - gt[y, x, ch]) < 10 * eps:
+            continue  # L1 kink
+        a1, a2 = ih.copy(), ih.copy()
+        a1[y, x, ch] += eps
+        a2[y, x, ch] -= eps
+        fd = (total(a1, im, tt) - total(a2, im, tt)) / (2 * eps)
+        assert abs(fd - g_ih[y, x, ch]) <= 1e-2 * abs(fd) + 1e-9, ("ih", y, x, ch, fd, g_ih[y, x, ch])
+        if tri[y, x] >= 0:
+            b1, b2 = im.copy(), im.copy()
+            b1[y, x, ch] += eps
+            b2[y, x, ch] -= eps
+            fd = (total(ih, b1, tt) - total(ih, b2, tt)) / (2 * eps)
+            assert abs(fd - g_im[y, x, ch]) <= 1e-2 * abs(fd) + 1e-9, ("im", y, x, ch, fd, g_im[y, x, ch])
+            t1, t2 = tt.copy(), tt.copy()
+            t1[y, x] += eps
+            t2[y, x] -= eps
+            fd = (total(ih, im, t1) - total(ih, im, t2)) / (2 * eps)
+            assert abs(fd - g_t[y, x]) <= 1e-2 * abs(fd) + 1e-9, ("t", y, x, fd, g_t[y, x])
