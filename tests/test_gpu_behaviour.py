@@ -216,3 +216,24 @@ def test_composite_loss_gradients_match_finite_differences(cuda_device):
             t2[y, x] -= eps
             fd = (total(ih, im, t1) - total(ih, im, t2)) / (2 * eps)
             assert abs(fd - g_t[y, x]) <= 1e-2 * abs(fd) + 1e-9, ("t", y, x, fd, g_t[y, x])
+
+
+def test_texture_backward_is_the_adjoint_of_sampling(cuda_device):
+    """sample_texture is linear in the texture, so texture_backward must be
+    its exact adjoint: <tb(G), D> == <G, sample(D)> for any D, G
+    (meshraster.py:158-184; reference test_texel_center_receives_full_gradient
+    / test_matches_finite_differences)."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    rng = np.random.default_rng(8)
+    cam = syn.look_at((0.1, 0.0, 0.0), (0.0, 0.2, 5.0), width=96, height=72)
+    mesh = syn.wall_mesh(rng, cam, 300, 32, depth=4.0)
+    m = hgs.TexturedMesh.from_any(mesh)
+    c = hgs.Camera.from_any(cam)
+    fr = mr.rasterize_fragments(m, c)
+    d = torch.as_tensor(rng.normal(size=(32, 32, 3)), dtype=torch.float32, device="cuda")
+    gimg = torch.as_tensor(rng.normal(size=(72, 96, 3)), dtype=torch.float32, device="cuda")
+    lhs = float((mr.texture_backward(fr, gimg, (32, 32)).double() * d.double()).sum())
+    rhs = float((gimg.double() * mr.sample_texture(d, fr.uv, fr.triangle_id).double()).sum())
+    assert abs(lhs - rhs) <= 1e-4 * max(1.0, abs(rhs))
+    assert bool((fr.triangle_id >= 0).any())
