@@ -1,25 +1,32 @@
 // K2 tile binning: build_tiles (gsmesh/splat/tiles.py:35-69).
 //
 // The reference orders tile entries with np.lexsort((kept, depth, tile))
-// (tiles.py:65).  Here:
-//   1. compact the visible rows (count > 0) in row order (chained scan) and
-//      add each row's tile rectangle into a 2D difference grid
-//   2. per-tile entry counts = 2D prefix sums of that grid; their exclusive
-//      scan is the CSR tile_starts (and K); the tile-key digit histograms
-//      follow from the counts                                    (1 CTA)
-//   3. sort the visible rows by the fp64 depth bit pattern, stably
-//      (8 LSD passes) -> rows in (depth, row) order
-//   4. bin_kernel (tile grids up to BIN_MAX_TILES): partitions of the
-//      depth-ordered rows; per partition and warp, per-tile entry counts of
-//      the rows' rectangles (shared memory); a decoupled look-back per tile
-//      across partitions gives each partition's offset inside every tile's
-//      list; then every entry is ranked in (depth, row) order inside its
-//      tile (warp match on the tile id) and written straight to its final
-//      slot -> (tile, depth, row) order == the reference's lexsort, exactly,
-//      with no entry-level sort at all.
+// (tiles.py:65).  Here, with every count kept on the device (one CUDA-graph
+// capturable chain of PDL launches):
+//   1. compact the visible rows (count > 0) in row order (chained scan),
+//      with the min / max of their depth keys; preprocess has already added
+//      each row's tile rectangle into 16 privatised 2D difference grids
+//   2. tile_counts: per-tile entry counts = 2D prefix sums of those grids;
+//      their exclusive scan is the CSR tile_starts, K and the overflow flag
+//                                                                 (1 CTA)
+//   3. depth order: the fp64 depth bit patterns (positive doubles order like
+//      their bits) are remapped to 24-bit keys over [min, max] (digit
+//      histograms in the same pass), sorted stably by 3 onesweep LSD passes
+//      (sort.cuh), and every run of equal truncated keys is re-ordered by the
+//      full 64-bit key -> visible rows in (depth, row) order, exactly
+//   4. two-level rectangle binning (tile grids of up to 512 4x4 super-tiles,
+//      i.e. 1080p; larger grids use 8x8 super-tiles split into four 4x4
+//      fine CTAs): the depth-ordered rows are flattened into (row,
+//      super-tile) pairs, partitioned evenly over warps; count / scan /
+//      scatter build each super-tile's coarse list in depth order (staged in
+//      shared memory for coalesced writes); fine_bin_kernel expands every
+//      coarse entry into its tiles of the super-tile (16-bit masks, ballots
+//      in order) straight into the final (tile, depth, row) order == the
+//      reference's lexsort, with no entry-level sort at all
 //   Larger tile grids: exclusive scan of the rows' tile counts in depth
 //      order, emission of (tile id, row) pairs, stable LSD sort by tile id.
-// Positive doubles order like their IEEE bit patterns, so step 2 is exact.
+// On overflow (K > capacity) the scatter / fine kernels and every consumer
+// of the bins skip their work; the caller grows the buffer and re-runs.
 #include "sort.cuh"
 
 namespace hgs {
