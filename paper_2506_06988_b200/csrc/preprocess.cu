@@ -1,8 +1,12 @@
 // K1 preprocess: project (gsmesh/splat/project.py:70-140), evaluate_colors
 // (:56-67) and the per-row tile rectangle / count of build_tiles
 // (splat/tiles.py:45-50).  One thread per Gaussian, fp64 arithmetic in the
-// reference's operation order; reads 56 B (+36 B SH1) of fp32 parameters and
-// writes the 80 B blend record + 8 B rectangle + 4 B count per row.
+// reference's operation order; reads 56 B (+36 B SH1) of fp32 parameters
+// (every load issued up front) and writes the 80 B blend record, the 48 B
+// fp32 cull record, the 8 B rectangle, the 4 B count and the 8 B depth key
+// per row, and adds the rectangle into a 2D tile difference grid.  Rows
+// culled before projection (near / far / opacity) or by a conservative
+// screen bound on the reference's radius exit before the covariance.
 #include "common.cuh"
 
 namespace hgs {

@@ -3,7 +3,8 @@
 // decoupled look-back and dynamic partition assignment so that every count
 // can stay on the device (no host round trip between stages).
 //
-// Radix pass: 256 threads x 16 items = 4096 keys per partition.  Ranking is
+// Radix pass: 256 threads x IPT items per partition (the depth sort uses
+// IPT = 8: 2048 keys, 3 passes over 24-bit keys).  Ranking is
 // warp-level multisplit (__match_any_sync) with per-warp digit counters in
 // shared memory, which preserves input order inside a partition (stability);
 // partitions are ordered by their dynamically assigned id, and the look-back
