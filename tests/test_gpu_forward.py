@@ -188,11 +188,12 @@ def test_depth_order_exact_under_key_truncation(cuda_device):
     assert np.array_equal(np_(dt.entries), t_ref.entries)
 
 
-@pytest.mark.parametrize("wh,n", [((1920, 1080), 60_000), ((1200, 680), 3_000)])
+@pytest.mark.parametrize("wh,n", [((3840, 2160), 120_000), ((1920, 1080), 60_000), ((1200, 680), 3_000)])
 def test_large_grid_bins_and_blend_match_oracle(wh, n, cuda_device):
-    """Tile grids of c5 (120 x 68 tiles: 8 x 8 super-tiles) and c3 (4 x 4),
-    with near-camera Gaussians spanning the whole screen (the depth order
-    puts them first): tile bins bit-exact, colours / T within 1e-6."""
+    """Tile grids of 4K (240 x 135 tiles: 8 x 8 super-tiles, four 4 x 4 fine
+    CTAs each), c5 (120 x 68 tiles: 510 4 x 4 super-tiles) and c3, with
+    near-camera Gaussians spanning the whole screen (the depth order puts
+    them first): tile bins bit-exact, colours / T within 1e-5."""
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import synthetic as syn
     rng = np.random.default_rng(11)
