@@ -173,32 +173,68 @@ __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __rest
 // Per-tile counts from the difference grid (2D inclusive prefix sums, in
 // shared memory), the CSR starts (exclusive scan), K, the overflow flag, and
 // the digit histograms of the tile keys for the LSD passes.  One CTA.
-__global__ void __launch_bounds__(1024) tile_counts_kernel(const int* __restrict__ diff, int tiles_x, int tiles_y,
+// Grids too large for shared memory (> 200 KB of cells: beyond ~51k tiles)
+// are summed into the first difference-grid copy in global memory and
+// prefixed there (each thread walks a row / column 32 cells at a time, the
+// loads in flight together); preprocess re-zeroes the grids every frame.
+__global__ void __launch_bounds__(1024) tile_counts_kernel(int* __restrict__ diff, int tiles_x, int tiles_y,
                                                            int64_t capacity, int64_t* tile_starts, int64_t* counters,
-                                                           uint32_t* hist) {
+                                                           uint32_t* hist, int in_global) {
   pdl_enter();
-  extern __shared__ int g[];  // (tiles_x + 1) x (tiles_y + 1)
-  __shared__ uint32_t sh[2][RADIX];
+  extern __shared__ int g_smem[];  // (tiles_x + 1) x (tiles_y + 1)
+  int* g = in_global ? diff : g_smem;
+  __shared__ uint32_t sh[3][RADIX];
   __shared__ int64_t s_chunk[1024];
   const int gw = tiles_x + 1;
   const int cells = gw * (tiles_y + 1);
   const int n_tiles = tiles_x * tiles_y;
-  for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < 3 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
   for (int c = threadIdx.x; c < cells; c += blockDim.x) {
     int v = 0;
 #pragma unroll
     for (int k = 0; k < TILE_DIFF_COPIES; k++) v += diff[(size_t)k * cells + c];
-    g[c] = v;
+    g[c] = v;  // (global path: copy 0 in place -- each cell is read and written by one thread)
   }
   __syncthreads();
-  for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along x
-    int run = 0;
-    for (int x = 0; x < tiles_x; x++) { run += g[y * gw + x]; g[y * gw + x] = run; }
-  }
-  __syncthreads();
-  for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along y
-    int run = 0;
-    for (int y = 0; y < tiles_y; y++) { run += g[y * gw + x]; g[y * gw + x] = run; }
+  if (!in_global) {
+    for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along x
+      int run = 0;
+      for (int x = 0; x < tiles_x; x++) { run += g[y * gw + x]; g[y * gw + x] = run; }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along y
+      int run = 0;
+      for (int y = 0; y < tiles_y; y++) { run += g[y * gw + x]; g[y * gw + x] = run; }
+    }
+  } else {
+    for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along x, 32 cells per round
+      int run = 0;
+      int* row = g + (size_t)y * gw;
+      for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+        int v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) v[i] = x0 + i < tiles_x ? row[x0 + i] : 0;
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+          run += v[i];
+          if (x0 + i < tiles_x) row[x0 + i] = run;
+        }
+      }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along y
+      int run = 0;
+      for (int y0 = 0; y0 < tiles_y; y0 += 32) {
+        int v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) v[i] = y0 + i < tiles_y ? g[(size_t)(y0 + i) * gw + x] : 0;
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+          run += v[i];
+          if (y0 + i < tiles_y) g[(size_t)(y0 + i) * gw + x] = run;
+        }
+      }
+    }
   }
   __syncthreads();
   const int per = (n_tiles + blockDim.x - 1) / blockDim.x;
@@ -210,6 +246,7 @@ __global__ void __launch_bounds__(1024) tile_counts_kernel(const int* __restrict
     if (c) {
       atomicAdd(&sh[0][t & 255], (uint32_t)c);
       atomicAdd(&sh[1][(t >> 8) & 255], (uint32_t)c);
+      atomicAdd(&sh[2][(t >> 16) & 255], (uint32_t)c);
     }
   }
   // block-wide exclusive scan of the chunk sums
@@ -243,7 +280,7 @@ __global__ void __launch_bounds__(1024) tile_counts_kernel(const int* __restrict
     tile_starts[t] = run;
     run += g[(t / tiles_x) * gw + t % tiles_x];
   }
-  for (int i = threadIdx.x; i < 2 * RADIX; i += blockDim.x) hist[i] = (&sh[0][0])[i];
+  for (int i = threadIdx.x; i < 3 * RADIX; i += blockDim.x) hist[i] = (&sh[0][0])[i];
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) offsets_kernel(const int32_t* __restrict__ count,
@@ -918,7 +955,7 @@ struct TilesScratch {
   uint32_t* tv0;
   uint32_t* tv1;
   // zeroed control block
-  uint32_t* rs_status;    // 8 depth passes x parts_n x 256, then 2 tile passes x parts_k x 256
+  uint32_t* rs_status;    // 8 depth passes x parts_n x 256, then 3 tile passes x parts_k x 256
   uint64_t* scan_status;  // 2 x (parts_n + 1)
   uint32_t* hist;         // 10 x 256
   uint32_t* part_ctr;     // 32
@@ -982,9 +1019,9 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.cstart = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(BIN_MAX_SUPER + 1)) : nullptr;
   const size_t ctl0 = off;
   t.control_begin = base ? base + ctl0 : nullptr;
-  t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 2 * parts_k));
+  t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 3 * parts_k));
   t.scan_status = (uint64_t*)take(sizeof(uint64_t) * (size_t)(2 * (parts_n + 1)));
-  t.hist = (uint32_t*)take(sizeof(uint32_t) * 10 * RADIX);
+  t.hist = (uint32_t*)take(sizeof(uint32_t) * 11 * RADIX);
   t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);  // [24..27]: depth key min/max (u64 x 2)
   t.diff = (int*)take(sizeof(int) * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1));
   t.chist = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER) : nullptr;
@@ -1108,15 +1145,16 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     HGS_CHECK_LAUNCH();
   }
   // 2. per-tile counts -> tile_starts, K, overflow, tile-key histograms
-  const size_t grid_smem = sizeof(int) * (size_t)(tx + 1) * (size_t)(ty + 1);
-  if (grid_smem > 200 * 1024) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large");
+  const size_t grid_bytes = sizeof(int) * (size_t)(tx + 1) * (size_t)(ty + 1);
+  const int tc_global = grid_bytes > 200 * 1024 ? 1 : 0;  // prefix sums in global memory for huge grids
+  const size_t grid_smem = tc_global ? 0 : grid_bytes;
   static bool tc_attr = false;
   if (!tc_attr) {
     cudaFuncSetAttribute(tile_counts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     tc_attr = true;
   }
   launch_pdl(tile_counts_kernel, dim3(1), dim3(1024), grid_smem, st, proj->tile_diff, tx, ty, tiles->capacity, tiles->tile_starts,
-                                                 tiles->counters, s.hist + 8 * RADIX);
+                                                 tiles->counters, s.hist + 8 * RADIX, tc_global);
   HGS_CHECK_LAUNCH();
   if (n == 0) return HGS_OK;
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
@@ -1187,7 +1225,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   while ((1 << bits) < n_tiles) bits++;
   const int tpasses = (bits + 7) / 8;
   uint32_t* rs_tile_status = s.rs_status + (size_t)8 * s.parts_n * RADIX;
-  if (tpasses > 2) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: more than 65536 tiles");
+  if (tpasses > 3) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: more than 2^24 tiles");
   if (n_tiles > 65535) {
     emit_kernel<uint32_t><<<4 * sm_count(), 256, 0, st>>>(rows, s.offsets, (const ushort4*)proj->rect,
                                                           tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],

@@ -188,10 +188,13 @@ def test_depth_order_exact_under_key_truncation(cuda_device):
     assert np.array_equal(np_(dt.entries), t_ref.entries)
 
 
-@pytest.mark.parametrize("wh,n", [((3840, 2160), 120_000), ((1920, 1080), 60_000), ((1200, 680), 3_000)])
+@pytest.mark.parametrize("wh,n", [((7680, 4320), 60_000), ((5120, 2880), 60_000), ((3840, 2160), 120_000),
+                                  ((1920, 1080), 60_000), ((1200, 680), 3_000)])
 def test_large_grid_bins_and_blend_match_oracle(wh, n, cuda_device):
-    """Tile grids of 4K (240 x 135 tiles: 8 x 8 super-tiles, four 4 x 4 fine
-    CTAs each), c5 (120 x 68 tiles: 510 4 x 4 super-tiles) and c3, with
+    """Tile grids beyond the binner (8K: 129600 tiles, 32-bit tile keys; 5K:
+    57600 tiles, 16-bit keys -- emission + stable LSD sort by tile id), 4K
+    (240 x 135 tiles: 8 x 8 super-tiles, four 4 x 4 fine CTAs each), c5
+    (120 x 68 tiles: 510 4 x 4 super-tiles) and c3, with
     near-camera Gaussians spanning the whole screen (the depth order puts
     them first): tile bins bit-exact, colours / T within 1e-5."""
     import paper_2506_06988_b200 as hgs
