@@ -89,6 +89,11 @@ class HybridTrainer:
         dev = gs.device
         self.dev = dev
         self.cameras = [Camera.from_any(c) for c in cameras]
+        if len({(int(c.width), int(c.height)) for c in self.cameras}) > 1:
+            raise ValueError("HybridTrainer needs one image size for all views (its per-lane buffers are sized once); "
+                             "loop.train handles mixed resolutions")
+        if len(images) != len(self.cameras):
+            raise ValueError(f"{len(self.cameras)} cameras but {len(images)} images")
         self.cam_dev = [camera_tensor(c, dev) for c in self.cameras]
         self.images = [im if isinstance(im, torch.Tensor) else torch.as_tensor(np.asarray(im, dtype=np.float32))
                        for im in images]
