@@ -113,3 +113,50 @@ def composite_loss(i_gt, i_h, i_m, covered, t, iteration: int, config, grad_scal
               MASK_VARIANTS[config.mask_variant], _WIN, float(grad_scale), _lib.ptr(grad_ih), _lib.ptr(grad_im),
               _lib.ptr(grad_t), _lib.ptr(scalars), _lib.ptr(scratch), scratch.numel(), _stream_ptr(dev))
     return LossBreakdown(scalars), grad_ih, grad_im, grad_t
+
+
+# ---- the reference's individual loss terms (losses.py:41-116), each a
+# configuration of the fused composite kernel (same arithmetic) -------------
+
+class _TermConfig:
+    def __init__(self, lam=0.0, texture_weight=0.0, k=20.0, variant="sigmoid"):
+        self.dssim_weight = lam
+        self.zero_dssim_after_densify = False
+        self.warmup_iters = 0
+        self.densify_until_iter = 2  # iteration 1 is inside the texture window
+        self.texture_weight = texture_weight
+        self.mask_sharpness = k
+        self.mask_variant = variant
+
+
+def l1_loss(pred, target):
+    """losses.py:41-44 -> (mean |pred - target|, sign(pred - target) / size)."""
+    bd, g, _, _ = composite_loss(target, pred, None, None, _zeros_t(pred), 1, _TermConfig(lam=0.0))
+    return bd.l1, g
+
+
+def dssim(pred, target):
+    """losses.py:73-76 -> ((1 - SSIM) / 2, its gradient w.r.t. pred)."""
+    bd, g, _, _ = composite_loss(target, pred, None, None, _zeros_t(pred), 1, _TermConfig(lam=1.0))
+    return bd.dssim, g
+
+
+def ssim(pred, target):
+    """losses.py:47-70 -> (mean SSIM, its gradient w.r.t. pred): 11-tap
+    sigma 1.5 zero-padded separable window, fp64."""
+    v, g = dssim(pred, target)
+    return 1.0 - 2.0 * v, g * -2.0
+
+
+def texture_loss(i_gt, i_m, covered, t, k: float = 20.0, variant: str = "sigmoid"):
+    """losses.py:103-116 -> (L_t, grad w.r.t. I_m, grad w.r.t. T); uncovered
+    pixels contribute nothing, the mean is over covered pixels."""
+    bd, _, g_im, g_t = composite_loss(i_gt, i_gt, i_m, covered, t, 1,
+                                      _TermConfig(texture_weight=1.0, k=k, variant=variant))
+    return bd.l_t, g_im, g_t
+
+
+def _zeros_t(img):
+    shp = tuple(img.shape[:2])
+    dev = img.device if isinstance(img, torch.Tensor) and img.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    return torch.zeros(shp, dtype=torch.float32, device=dev)

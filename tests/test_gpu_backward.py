@@ -379,3 +379,34 @@ def test_c4_composite_loss_matches_oracle(cuda_device):
     for a, b, nm in ((gih, ogih, "grad_ih"), (gim, ogim, "grad_im"), (gt, ogt, "grad_t")):
         scale = np.abs(b).max()
         assert np.abs(np_(a) - b).max() <= 1e-3 * scale, nm
+
+
+@pytest.mark.parametrize("variant", ["sigmoid", "identity_t"])
+def test_individual_loss_terms_match_oracle(variant, cuda_device):
+    """l1_loss, ssim, dssim and texture_loss (losses.py:41-116), the
+    reference's public loss terms, against the oracle: values at 1e-9
+    relative, gradients at 1e-3 of their scale; no coverage -> zero."""
+    from paper_2506_06988_b200 import losses
+    rng = np.random.default_rng(12)
+    h, w = 57, 83  # not a multiple of the 16-px SSIM tile
+    gt = rng.uniform(0, 1, (h, w, 3)).astype(np.float32).astype(np.float64)
+    pr = np.clip(gt + rng.normal(0, 0.15, gt.shape), 0, 1).astype(np.float32).astype(np.float64)
+    im = np.clip(gt + rng.normal(0, 0.15, gt.shape), 0, 1).astype(np.float32).astype(np.float64)
+    cov = rng.uniform(size=(h, w)) < 0.6
+    t = rng.uniform(0, 1, (h, w)).astype(np.float32).astype(np.float64)
+
+    def close_grad(a, b, nm):
+        assert np.abs(np_(a) - b).max() <= 1e-3 * np.abs(b).max() + 1e-12, nm
+
+    for fn in ("l1_loss", "ssim", "dssim"):
+        v, g = getattr(losses, fn)(pr, gt)
+        ov, og = getattr(orc, fn)(pr, gt)
+        assert abs(v - ov) <= 1e-9 * max(1.0, abs(ov)), fn
+        close_grad(g, og, fn)
+    v, gim, gt_ = losses.texture_loss(gt, im, cov, t, 20.0, variant)
+    ov, ogim, ogt = orc.texture_loss(gt, im, cov, t, 20.0, variant)
+    assert abs(v - ov) <= 1e-9 * max(1.0, abs(ov))
+    close_grad(gim, ogim, "texture grad_im")
+    close_grad(gt_, ogt, "texture grad_t")
+    v, gim, gt_ = losses.texture_loss(gt, im, np.zeros((h, w), dtype=bool), t, 20.0, variant)
+    assert v == 0.0 and float(gim.abs().max()) == 0.0 and float(gt_.abs().max()) == 0.0
