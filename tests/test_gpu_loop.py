@@ -85,3 +85,70 @@ def test_trainer_lanes_match_single_stream(cuda_device):
     assert np.allclose(l1, l4, rtol=1e-9, atol=1e-12)
     assert np.abs(p1 - p4).max() < 1e-6
     assert np.abs(t1 - t4).max() < 1e-6
+
+
+def test_trainer_two_rank_protocol_on_one_gpu(cuda_device):
+    """HybridTrainer's data-parallel step with world=2, the two ranks as host
+    threads on one GPU joined through the trainer's all-reduce hook (a host
+    barrier + sum -- no kernel waits on another): both replicas end
+    bit-identical and equal the single-process step over the whole batch up
+    to fp32 summation order."""
+    import threading
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import synthetic as syn
+    from paper_2506_06988_b200.config import TrainConfig
+    from paper_2506_06988_b200.train import HybridTrainer
+    sc = syn.make_config("c2", seed=0)
+    rng = np.random.default_rng(5)
+    views = [syn.look_at((0.15 * k, -0.1, -0.2), (0.0, 0.0, 5.0), width=320, height=240) for k in range(6)]
+    cams = [hgs.Camera.from_any(v) for v in views]
+    images = [torch.as_tensor(rng.uniform(0, 1, (240, 320, 3)), dtype=torch.float32) for _ in cams]
+    it = TrainConfig().warmup_iters + 1
+
+    def make(rank, world, hook=None):
+        gs = hgs.GaussianSet.from_any(sc.gaussians)
+        mesh = hgs.TexturedMesh.from_any(sc.mesh)
+        return HybridTrainer(gs, mesh, cams, images, TrainConfig(), rank=rank, world=world, allreduce=hook)
+
+    single = make(0, 1)
+    single.step(it, list(range(len(cams))))
+    ref_p = single.gs.params.detach().cpu().numpy()
+
+    barrier = threading.Barrier(2)
+    shared = {}
+
+    def hook_for(rank):
+        def hook(t):
+            shared.setdefault(t.numel(), {})[rank] = t.clone()
+            barrier.wait()
+            parts = shared[t.numel()]
+            total = parts[0] + parts[1]
+            t.copy_(total)
+            torch.cuda.synchronize()
+            barrier.wait()
+            if rank == 0:
+                shared.pop(t.numel(), None)
+            barrier.wait()
+        return hook
+
+    trainers = [make(r, 2, hook_for(r)) for r in range(2)]
+    errors = []
+
+    def run(r):
+        try:
+            trainers[r].step(it, list(range(len(cams))))
+            torch.cuda.synchronize()
+        except Exception as e:  # surfaced below
+            errors.append(e)
+            barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=600)
+    assert not errors, errors
+    p0 = trainers[0].gs.params.detach().cpu().numpy()
+    p1 = trainers[1].gs.params.detach().cpu().numpy()
+    assert np.array_equal(p0, p1)
+    assert np.abs(p0 - ref_p).max() < 1e-6
