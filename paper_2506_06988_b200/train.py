@@ -236,6 +236,9 @@ class HybridTrainer:
         if after is not None:  # the chain accumulates (read-modify-write) into the shared bucket, in view order
             torch.cuda.current_stream(self.dev).wait_event(after)
         chain_backward(ctx, lane.screen, self.grads, scale=1.0, accumulate=True)
+        if lane.stream is not None:  # the next view's chain may start once this one is done
+            lane.chain_done = torch.cuda.Event()
+            lane.chain_done.record(torch.cuda.current_stream(self.dev))
         if layer is not None and self.tex_grad is not None:
             from .meshraster import texture_backward
             texture_backward(fr, mesh_grad, tuple(self.mesh.texture.shape[:2]), out=self.tex_grad)
@@ -266,8 +269,7 @@ class HybridTrainer:
                 lane = self.lanes[j % len(self.lanes)]
                 with torch.cuda.stream(lane.stream):
                     lane.loss_sum += self.view_grads(v, it, 1.0 / nb, lane=lane, after=prev)
-                    prev = torch.cuda.Event()
-                    prev.record(lane.stream)
+                    prev = lane.chain_done
             for lane in self.lanes:
                 main.wait_stream(lane.stream)
         overflow = self.lanes[0].overflow
