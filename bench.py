@@ -157,10 +157,11 @@ def run_reference(args):
     sc = syn.make_config(args.config, seed=0)
     cores = len(os.sched_getaffinity(0))
     # warm-up steps (untimed), then K timed steps; each step is one frame
-    cpu_frames(sc, max_frames=1, threads=cores)  # untimed warm-up frame (page-in, thread pool)
+    n_warm = min(args.warmup, 3)
+    cpu_frames(sc, max_frames=n_warm, threads=cores)  # untimed warm-up frames (page-in, thread pool)
     fps, frames, dt, th = cpu_frames(sc, max_seconds=args.ref_seconds, max_frames=args.steps, threads=cores)
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 / fps, "higher_is_better": True, "scaling": "weak",
+            "warmup": n_warm, "ms_per_step": 1000.0 / fps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: full hybrid frame (mesh raster + texture + project + tiles + blend)",
                        "gaussians": len(sc.gaussians), "triangles": int(sc.mesh.n_faces),
