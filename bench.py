@@ -99,6 +99,28 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+# one pixel-Gaussian evaluation = ~14 FP32 operations
+# (conic form, exp2 argument, alpha, the T / colour recurrence) + 1 ex2
+FP32_OPS_PER_EVAL = 14.0
+
+
+def compute_peaks():
+    """FP32 / MUFU / FP64 / SMEM / issue peaks microbenchmarked on a B200 of
+    this pool (tools/ubench_peaks.cu -> profiles/r02_ubench.json); falls
+    back to the nominal figures (148 SMs x 128 FP32 lanes, 16 ex2 / SM / clk
+    at 1965 MHz) when the file is absent."""
+    p = os.path.join(ROOT, "profiles", "r02_ubench.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"fp32": d["fp32_fma"]["rate"], "ex2": d["mufu_ex2"]["rate"], "fp64": d["fp64_fma"]["rate"],
+                "smem": d["smem_lds128"]["rate"], "issue": d["issue_int"]["rate"],
+                "kind": "measured (tools/ubench_peaks.cu, profiles/r02_ubench.json)"}
+    f = 1.965e9
+    return {"fp32": 148 * 128 * f, "ex2": 148 * 16 * f, "fp64": 148 * 64 * f, "smem": 148 * 128 * f,
+            "issue": 148 * 4 * f, "kind": "nominal (no profiles/r02_ubench.json)"}
+
+
 def cpu_frames(scene, max_seconds=15.0, max_frames=5, threads=0):
     """Oracle (CPU restatement of the reference path) full hybrid frames on
     the host cores; returns (fps, frames, seconds, threads)."""
@@ -156,9 +178,9 @@ def run_reference(args):
     from paper_2506_06988_b200 import synthetic as syn
     sc = syn.make_config(args.config, seed=0)
     cores = len(os.sched_getaffinity(0))
-    # warm-up steps (untimed), then K timed steps; each step is one frame
-    n_warm = min(args.warmup, 3)
-    cpu_frames(sc, max_frames=n_warm, threads=cores)  # untimed warm-up frames (page-in, thread pool)
+    # W warm-up steps (untimed), then K timed steps; each step is one frame
+    n_warm = args.warmup
+    cpu_frames(sc, max_seconds=1e9, max_frames=n_warm, threads=cores)  # untimed warm-up frames (page-in, thread pool)
     fps, frames, dt, th = cpu_frames(sc, max_seconds=args.ref_seconds, max_frames=args.steps, threads=cores)
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": n_warm, "ms_per_step": 1000.0 / fps, "higher_is_better": True, "scaling": "weak",
@@ -171,6 +193,32 @@ def run_reference(args):
                                        f"(time-capped at {args.ref_seconds:.0f} s; oracle/gsmesh_oracle.c, OpenMP)"},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def e2e_dropin(sc, gs_dev, mesh_dev, cam, stream, flush, steps):
+    """Drop-in e2e: ``render(host_gaussians, cam, mesh=layer)`` per frame,
+    host numpy in (the reference's fp64 GaussianSet arrays), colour / depth
+    / T out as host numpy.  Returns (ms over ``steps`` frames, steps)."""
+    import torch
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    layer = mr.mesh_layer(mesh_dev, cam)  # precomputed, as bench_fps does (metrics.py:47-56)
+    host = sc.gaussians
+    outs = None
+    for _ in range(2):  # warm (allocator, scratch)
+        out, _ctx = hgs.render(host, cam, background=(0.0, 0.0, 0.0), mesh=layer)
+        outs = (out.color.cpu().numpy(), out.depth.cpu().numpy(), out.transmittance.cpu().numpy())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        flush.fill_(i & 0xff)
+        out, _ctx = hgs.render(host, cam, background=(0.0, 0.0, 0.0), mesh=layer)
+        outs = (out.color.cpu().numpy(), out.depth.cpu().numpy(), out.transmittance.cpu().numpy())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    assert outs[0].shape == (cam.height, cam.width, 3) and outs[2].shape == (cam.height, cam.width)
+    return float(e0.elapsed_time(e1)), steps
 
 
 def run_ours(args):
@@ -223,14 +271,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
     # e2e: the serving loop through the engine API (HybridRenderer.render_to_host):
-    # per frame the camera H2D, the graph replay, a device snapshot of the
-    # colour image and its D2H into pinned host memory on a copy stream
-    # (double-buffered: frame i's transfer overlaps frame i+1's render).
-    # Timed as ONE region from the first frame's start to the last image's
-    # arrival on the host; the L2 flush between frames stays inside it.
-    host_imgs = [torch.empty(H, W, 3, dtype=torch.float32).pin_memory() for _ in range(2)]
+    # per frame the camera H2D, the graph replay, device snapshots of the
+    # reference's RenderOutputs images (colour, depth, transmittance) and
+    # their D2H into pinned host memory on a copy stream (double-buffered:
+    # frame i's transfer overlaps frame i+1's render).  Timed as ONE region
+    # from the first frame's start to the last image's arrival on the host;
+    # the L2 flush between frames stays inside it.
+    host_imgs = [(torch.empty(H, W, 3, dtype=torch.float32).pin_memory(),
+                  torch.empty(H, W, dtype=torch.float32).pin_memory(),
+                  torch.empty(H, W, dtype=torch.float32).pin_memory()) for _ in range(2)]
     for i in range(2):  # warm the copy stream / snapshots
-        r.render_to_host(cam, host_imgs[i])
+        r.render_to_host(cam, *host_imgs[i])
     torch.cuda.synchronize()
     e2e_0, e2e_1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pending = [None, None]
@@ -238,20 +289,27 @@ def run_ours(args):
     for i in range(args.steps):
         flush.fill_(i & 0xff)
         if pending[i & 1] is not None:
-            pending[i & 1].synchronize()  # host buffer free again (its copy landed)
-        pending[i & 1] = r.render_to_host(cam, host_imgs[i & 1])
+            pending[i & 1].synchronize()  # host buffers free again (their copies landed)
+        pending[i & 1] = r.render_to_host(cam, *host_imgs[i & 1])
     for ev_ in pending:
         if ev_ is not None:
             stream.wait_event(ev_)
     e2e_1.record(stream)
     torch.cuda.synchronize()
-    clk = clocks.stop()
     e2e_ms = float(e2e_0.elapsed_time(e2e_1))
-    assert torch.equal(host_imgs[(args.steps - 1) & 1], r.color.cpu()), "e2e image differs from the device frame"
-    t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    last_host = host_imgs[(args.steps - 1) & 1]
+    assert torch.equal(last_host[0], r.color.cpu()), "e2e image differs from the device frame"
+    assert torch.equal(last_host[2], r.trans.cpu()), "e2e transmittance differs from the device frame"
+    # e2e through the drop-in call: render(gs, cam, mesh=layer) with the
+    # Gaussians as the reference holds them (host numpy fp64 arrays, uploaded
+    # every call), the mesh layer precomputed as in the reference's bench_fps
+    # (metrics.py:47-56), and colour / depth / T brought back as host arrays
+    dropin_ms, dropin_steps = e2e_dropin(sc, gs, mesh, cam, stream, flush, max(3, min(args.steps, 20)))
+    clk = clocks.stop()
+    t = torch.tensor([ms, e2e_ms, dropin_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, e2e_ms = float(t[0]), float(t[1])
+    ms, e2e_ms, dropin_ms = float(t[0]), float(t[1]), float(t[2])
     _, _, ovf = r.check()
     assert not ovf, "tile-entry capacity overflow during the timed region"
     # the reference's own bench_fps boundary (metrics.py:44-64): project +
@@ -302,15 +360,22 @@ def run_ours(args):
     tiles_ms /= reps
     walked, blended = (int(x) for x in r.stats.cpu())
     npix = W * H
-    # algorithmic HBM floor of one blend launch (our record
-    # sizes): the K entry indices once (4 B), each visible Gaussian's 80 B
-    # record + 32 B cull record once (the gathers are L2-resident), per pixel
-    # mesh colour 12 + depth 8 + id 4 B in, colour 12 + depth 4 + T 4 B out
+    # K4 is rated against its compute bound: evaluations/s
+    # vs min(FP32 rate / 14 ops, ex2 rate), peaks microbenchmarked on the box
+    pk = compute_peaks()
+    eval_rate = walked / (blend_ms * 1e-3)
+    eval_peak = min(pk["fp32"] / FP32_OPS_PER_EVAL, pk["ex2"])
+    # secondary: the algorithmic HBM floor of one blend launch (§8(d) K4, our
+    # record sizes): the K entry indices once (4 B), each visible Gaussian's
+    # 80 B record + 32 B cull record once (the gathers are L2-resident), per
+    # pixel mesh colour 12 + depth 8 + id 4 B in, colour 12 + depth 4 + T 4 out
     blend_bytes = k_entries * 4 + m_vis * (80 + 32) + npix * (12 + 8 + 4 + 12 + 4 + 4)
     peak, peak_kind = measured_peaks()
     achieved = blend_bytes / (blend_ms * 1e-3) / 1e9
     prof = {}
-    pp = os.path.join(ROOT, "profiles", "r01_blend_ncu.json")
+    pp = os.path.join(ROOT, "profiles", "r02_blend_ncu.json")
+    if not os.path.exists(pp):
+        pp = os.path.join(ROOT, "profiles", "r01_blend_ncu.json")
     if os.path.exists(pp):
         with open(pp) as f:
             prof = json.load(f)
@@ -329,20 +394,33 @@ def run_ours(args):
                        "l2": "flushed between frames (256 MB write)", "parallelism": f"replicas x{world}",
                        "evaluations_walked_per_px": walked / npix, "blended_per_px": blended / npix},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 200,
-                    "d2h_bytes_per_step": int(H * W * 3 * 4),
+                    "d2h_bytes_per_step": int(H * W * 5 * 4),
                     "note": "scene resident; serving loop HybridRenderer.render_to_host: per frame camera H2D (pinned) + "
-                            "graph replay + colour snapshot + D2H on a copy stream overlapping the next frame; one "
-                            "timed region over all frames, L2 flush between frames included"},
+                            "graph replay + colour / depth / transmittance snapshots + their D2H on a copy stream "
+                            "overlapping the next frame; one timed region over all frames, L2 flush between frames "
+                            "included"},
+            "e2e_dropin": {"value": dropin_steps * world / (dropin_ms * 1e-3), "unit": UNIT,
+                           "h2d_bytes_per_step": int(len(gs) * 14 * 8 + 200),
+                           "d2h_bytes_per_step": int(H * W * 5 * 4), "steps": dropin_steps,
+                           "note": "the reference's drop-in call per frame: render(gs, cam, mesh=layer) with the "
+                                   "Gaussians as host numpy fp64 arrays (uploaded every call), mesh layer precomputed "
+                                   "(bench_fps boundary, metrics.py:47-56), colour / depth / T copied back to host "
+                                   "numpy; render() keeps the backward state (fp64 final T)"},
             "gpu_launches": int(launches_per_frame * args.steps * 2),
             "clocks": clk,
-            "roofline": {"kernel": "blend_fast_kernel (K4)", "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": prof.get("dram_bytes"),
-                         "algorithmic_bytes": blend_bytes, "peak_kind": peak_kind, "kernel_ms": blend_ms,
+            "roofline": {"kernel": "blend_fast_kernel (K4)", "bound": "fp32_issue", "achieved": eval_rate,
+                         "peak": eval_peak, "unit": "evaluations/s", "frac": eval_rate / eval_peak,
+                         "traffic": prof.get("dram_bytes"), "kernel_ms": blend_ms,
+                         "evaluations_per_launch": walked,
+                         "peak_basis": f"min(FP32 FMA rate / {FP32_OPS_PER_EVAL:g} ops, MUFU ex2 rate) = "
+                                       f"min({pk['fp32']:.3e} / {FP32_OPS_PER_EVAL:g}, {pk['ex2']:.3e})",
+                         "peak_kind": pk["kind"],
                          "issue_active": prof.get("issue_active"), "fp64_pipe_active": prof.get("fp64_pipe_active"),
-                         "note": "K4 is instruction-issue bound, not HBM bound (the staged records are L2-resident): "
-                                 "frac is far below 1 by construction; issue_active (ncu, "
-                                 "profiles/r01_blend_ncu.json) and compute_rate.blend_evaluations_per_s are the "
-                                 "relevant figures"},
+                         "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                                 "algorithmic_bytes": blend_bytes, "peak_kind": peak_kind},
+                         "note": "K4 is compute (instruction-issue) bound; the staged records are L2-resident, so its "
+                                 "HBM figure (hbm) is far below 1 by construction. achieved = pixel-Gaussian "
+                                 "evaluations walked (counted in-kernel) / the kernel's CUDA-event time"},
             "compute_rate": {"blend_evaluations_per_s": walked / (blend_ms * 1e-3),
                              "tiles_stage_ms": tiles_ms, "blend_ms": blend_ms},
             "gs_frame": {"value": 1000.0 / gs_ms, "unit": UNIT, "ms_per_step": gs_ms,
@@ -425,6 +503,21 @@ def run_train(args, rank, world, local, dev):
                     "all_reduce(SUM) of one flat grad bucket (N>1), fused Adam (Gaussians + texture)"}
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _spawned_rank(local_rank: int, args, port: int) -> None:
+    """Entry of one rank started by ``bench.py --gpus N`` itself (no
+    torchrun): the torchrun environment, then the normal per-rank path."""
+    os.environ.update({"RANK": str(local_rank), "LOCAL_RANK": str(local_rank), "WORLD_SIZE": str(args.gpus),
+                       "LOCAL_WORLD_SIZE": str(args.gpus), "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    run_ours(args)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -442,8 +535,20 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    launched = "WORLD_SIZE" in os.environ
+    if launched and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        ap.error(f"--gpus {args.gpus} but the launcher started WORLD_SIZE={os.environ['WORLD_SIZE']} ranks")
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args)  # rank 0 only (the CPU path has no ranks); other ranks exit 0
+    elif args.gpus > 1 and not launched:
+        # one process per GPU, started here (the driver may also use torchrun)
+        import torch
+        import torch.multiprocessing as mp
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but only {torch.cuda.device_count()} CUDA devices are visible")
+        mp.spawn(_spawned_rank, args=(args, _free_port()), nprocs=args.gpus, join=True)
     else:
         run_ours(args)
 

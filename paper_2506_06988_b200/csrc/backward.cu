@@ -7,20 +7,24 @@
 // warps own 8x8 sub-tiles (two pixels per lane), 1 producer warp streams the
 // tile's entries NEWEST FIRST (from the largest `last` of the tile down to
 // the first entry) through a 3-stage x 64-entry cp.async/mbarrier ring
-// (64 registers: 6 CTAs per SM).  Each pixel
-// walks back from its last blended entry (kernels.py:120): T before an entry
-// is reconstructed from T after it (one reciprocal of 1 - sigma: SFU
-// estimate + Newton step), the suffix colour starts at T_final * (mesh
-// colour or background), exactly as the reference.  Per-warp ellipse cull
-// as in the forward.  The per-entry 9-vector (mean2d 2, cov 3 full-matrix
-// convention, alpha, rgb 3) is reduced over the warp (reduce-scatter) and
-// added to the per-Gaussian fp64 accumulator with one atomic per component
-// per warp.
+// (5 CTAs per SM).  Each pixel walks back from its last blended entry
+// (kernels.py:120): T before an entry is reconstructed from T after it (one
+// reciprocal of 1 - sigma), starting from the forward's fp64 final T; the
+// suffix colours enter only through one scalar Q (see BwPix).  Per-warp
+// ellipse cull as in the forward.  The per-entry 9-vector (mean2d 2, cov 3
+// full-matrix convention, alpha, rgb 3) is reduced over the warp
+// (reduce-scatter) and added to the per-Gaussian fp64 accumulator with one
+// atomic per component per warp.
 //
 // Numerics: the per-entry decisions (support m <= 9, skip sigma < 1/255,
 // clamp at 0.99) are the reference's: fp64 conic form, fp32 sigma from the
 // SFU with guard bands (stage.cuh), and an exact fp64 re-evaluation of the
-// entry inside a band.  The gradient arithmetic is fp32.
+// entry inside a band.  The gradient arithmetic runs in fp64 (sigma from the
+// fp64 exp2, T / Q recurrence, s_i, mean2d and cov products; alpha and colour
+// products in fp32): the reverse recurrence compounds every error of sigma
+// and T over the walk, and the centre gradients (|g| ~ 4e2 at c3) must hold
+// 1e-4 absolute -- fp32 arithmetic left 2.6e-4, this design 3.9e-5
+// (tools/diag_bw_variants.py).
 #include "stage.cuh"
 
 namespace hgs {
@@ -32,7 +36,7 @@ namespace hgs {
 #define HGS_BW_NSTAGE 3
 #endif
 #ifndef HGS_BW_MINB
-#define HGS_BW_MINB 6  // 64 registers: 6 CTAs (24 consumer warps) per SM; 4 -> 6 was -2.8 % per c4 step
+#define HGS_BW_MINB 5  // fp64 walk state: 5 CTAs (81 regs) 170.6 vs 4 CTAs 174.6 ms per c4 step
 #endif
 constexpr int BW_BATCH = HGS_BW_BATCH;
 constexpr int BW_NSTAGE = HGS_BW_NSTAGE;
@@ -46,44 +50,46 @@ struct BwSmem {
   unsigned long long full[BW_NSTAGE];
   unsigned long long empty[BW_NSTAGE];
   unsigned char list[BW_CONSUMERS][BW_BATCH];
+  double exp2tab[16];
   int max_last;
 };
 
 // Sum 9 per-lane values over the warp (reduce-scatter, 12 shuffles): lane L
 // ends with the total of value index reduce9_index(L) (-1: none).
-__device__ __forceinline__ float warp_reduce9(float v[9], int lane) {
+template <typename R>
+__device__ __forceinline__ R warp_reduce9(R v[9], int lane) {
   // offset 16: lower lanes keep 0..4, upper keep 5..8
   const bool u16 = lane & 16;
 #pragma unroll
   for (int i = 0; i < 5; i++) {
-    const float hi = i < 4 ? v[5 + i] : 0.0f;
-    const float send = u16 ? v[i] : hi;
-    const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+    const R hi = i < 4 ? v[5 + i] : (R)0;
+    const R send = u16 ? v[i] : hi;
+    const R recv = __shfl_xor_sync(0xffffffffu, send, 16);
     v[i] = (u16 ? hi : v[i]) + recv;
   }
   // now 5 values (upper lanes: 4 + a zero); offset 8: keep 0..2 / 3..4
   const bool u8 = lane & 8;
 #pragma unroll
   for (int i = 0; i < 3; i++) {
-    const float hi = i < 2 ? v[3 + i] : 0.0f;
-    const float send = u8 ? v[i] : hi;
-    const float recv = __shfl_xor_sync(0xffffffffu, send, 8);
+    const R hi = i < 2 ? v[3 + i] : (R)0;
+    const R send = u8 ? v[i] : hi;
+    const R recv = __shfl_xor_sync(0xffffffffu, send, 8);
     v[i] = (u8 ? hi : v[i]) + recv;
   }
   // 3 values; offset 4: keep 0..1 / 2
   const bool u4 = lane & 4;
 #pragma unroll
   for (int i = 0; i < 2; i++) {
-    const float hi = i < 1 ? v[2] : 0.0f;
-    const float send = u4 ? v[i] : hi;
-    const float recv = __shfl_xor_sync(0xffffffffu, send, 4);
+    const R hi = i < 1 ? v[2] : (R)0;
+    const R send = u4 ? v[i] : hi;
+    const R recv = __shfl_xor_sync(0xffffffffu, send, 4);
     v[i] = (u4 ? hi : v[i]) + recv;
   }
   // 2 values; offset 2: keep 0 / 1
   {
     const bool u2 = lane & 2;
-    const float send = u2 ? v[0] : v[1];
-    const float recv = __shfl_xor_sync(0xffffffffu, send, 2);
+    const R send = u2 ? v[0] : v[1];
+    const R recv = __shfl_xor_sync(0xffffffffu, send, 2);
     v[0] = (u2 ? v[1] : v[0]) + recv;
   }
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
@@ -101,14 +107,14 @@ __device__ __forceinline__ int reduce9_index(int lane) {
 }
 
 struct BwExact {
-  float sig, gauss;
+  double sig, gauss;
   bool clamped;
 };
 // Exact per-entry evaluation in the reference's operation order
 // (kernels.py:126-133): sigma (or -1: no contribution), the Gaussian value
 // and whether sigma was clamped.
 __device__ __noinline__ BwExact bw_exact_entry(const StageEntry& E, double fx, double fy) {
-  BwExact r{-1.0f, 0.0f, false};
+  BwExact r{-1.0, 0.0, false};
   const double dx = fx - E.a.x, dy = fy - E.a.y;
   const double m = E.b.x * dx * dx + E.b.y * dx * dy + E.c.x * dy * dy;
   if (m > SUPPORT_MAHAL2 || m < 0.0) return r;
@@ -117,15 +123,25 @@ __device__ __noinline__ BwExact bw_exact_entry(const StageEntry& E, double fx, d
   r.clamped = sg > ALPHA_CLAMP;
   if (r.clamped) sg = ALPHA_CLAMP;
   if (sg < SIGMA_SKIP) return r;
-  r.gauss = (float)g;
-  r.sig = (float)sg;
+  r.gauss = g;
+  r.sig = sg;
   return r;
 }
 
-// Per-pixel reverse-walk state (fp32).
+// Per-pixel reverse-walk state.  The three suffix colours acc_c of
+// kernels.py:111-160 only ever enter the gradient through
+// Q = sum_c g_c acc_c + g_T T_final (s_i = (g.c_i T_after - Q) / (1 - sigma)
+// and Q += (g.c_i) w_i), so the walk carries that one scalar.  fp64: T after
+// the current entry and Q (T before an entry is T after it / (1 - sigma), an
+// error in either compounds over the walk, and s_i is a difference of nearly
+// equal terms); the upstream gradients are given in fp32.
+#ifndef HGS_BW_V64
+#define HGS_BW_V64 5  // leading 9-vector components accumulated in fp64 (mean2d 2, cov 3)
+#endif
 struct BwPix {
   int last;
-  float gr, gg, gb, gtp, t_fin, t_after, acc_r, acc_g, acc_b;
+  float gr, gg, gb;
+  double t_after, q;
 };
 
 __device__ __forceinline__ void bw_pixel_init(BwPix& q, bool inside, int64_t p, int64_t s, const hgs_mesh_layer& mesh,
@@ -134,19 +150,19 @@ __device__ __forceinline__ void bw_pixel_init(BwPix& q, bool inside, int64_t p, 
                                               const float* __restrict__ grad_color, const float* __restrict__ grad_t,
                                               float* __restrict__ mesh_grad, int accumulate_mesh) {
   q.last = -1;
-  q.gr = q.gg = q.gb = q.gtp = 0.f;
-  q.t_fin = q.t_after = 1.f;
-  q.acc_r = q.acc_g = q.acc_b = 0.f;
+  q.gr = q.gg = q.gb = 0.f;
+  q.t_after = 1.0;
+  q.q = 0.0;
   if (!inside) return;
   q.last = last_idx[p];
   q.gr = grad_color[3 * p];
   q.gg = grad_color[3 * p + 1];
   q.gb = grad_color[3 * p + 2];
-  q.gtp = grad_t ? grad_t[p] : 0.f;
-  q.t_fin = (float)final_t[p];
+  const double gtp = grad_t ? (double)grad_t[p] : 0.0;
+  const double t_fin = final_t[p];
   const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
   if (mesh_grad) {  // d pixel / d mesh colour = T * valid (render.py:180-181)
-    const float f = mesh_here ? q.t_fin : 0.f;
+    const float f = mesh_here ? (float)t_fin : 0.f;
     float* mg = mesh_grad + 3 * p;
     if (accumulate_mesh) {
       mg[0] += q.gr * f; mg[1] += q.gg * f; mg[2] += q.gb * f;
@@ -155,76 +171,84 @@ __device__ __forceinline__ void bw_pixel_init(BwPix& q, bool inside, int64_t p, 
     }
   }
   // suffix colour starts at T_final * (mesh colour or background) (kernels.py:111-119)
-  q.t_after = q.t_fin;
+  double c0 = bg0, c1 = bg1, c2 = bg2;
   if (mesh_here) {
-    q.acc_r = q.t_fin * mesh.color[3 * p];
-    q.acc_g = q.t_fin * mesh.color[3 * p + 1];
-    q.acc_b = q.t_fin * mesh.color[3 * p + 2];
-  } else {
-    q.acc_r = q.t_fin * (float)bg0;
-    q.acc_g = q.t_fin * (float)bg1;
-    q.acc_b = q.t_fin * (float)bg2;
+    c0 = mesh.color[3 * p];
+    c1 = mesh.color[3 * p + 1];
+    c2 = mesh.color[3 * p + 2];
   }
+  q.t_after = t_fin;
+  q.q = t_fin * (((double)q.gr * c0 + (double)q.gg * c1) + (double)q.gb * c2 + gtp);
   if (q.last >= 0) q.last -= (int)s;  // relative to the tile start
 }
 
 // One reverse step of kernels.py:120-160 for one pixel and entry E (relative
-// index rel): decisions, then the pixel's 9-vector added into v.
-__device__ __forceinline__ void bw_pixel_step(BwPix& q, const StageEntry& E, int rel, double fx, double fy, float v[9]) {
+// index rel): the reference's decisions (fp32 fast test + exact fp64
+// re-evaluation inside the guard bands), then the gradient arithmetic --
+// sigma from the fp64 exp2 (stage.cuh), the T / Q recurrence and s_i in
+// fp64, the 9-vector products in fp64 for the first HGS_BW_V64 components
+// (mean2d, cov: they reach the centre gradients through the focal / depth
+// chain) and fp32 for the rest (alpha, colour).
+__device__ __forceinline__ void bw_pixel_step(BwPix& q, const StageEntry& E, int rel, double fx, double fy,
+                                              const double* __restrict__ tab, double vd[5], float vf[4]) {
   const bool act = q.last >= 0 && rel <= q.last;
   if (!act) return;  // entry after this pixel's last blended one
-  // fast evaluation: fp64 conic form, fp32 sigma
   const double dx = fx - E.a.x, dy = fy - E.a.y;
   const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
-  const float uu = __double2float_rn(m * U_SCALE);
+  const double u = m * U_SCALE;
+  const float uu = __double2float_rn(u);
   const float a32 = E.f.col.x;
-  float gauss = ex2_neg(uu);
-  const float sraw = fabsf(a32) * gauss;
+  const float sraw = fabsf(a32) * ex2_neg(uu);
   bool clamped = sraw > CLAMP_F;
-  float sg = fminf(sraw, CLAMP_F);
-  bool ok = act && uu < U9_LO && sg >= SKIP_F;
-  const float key = fminf(amb_key(uu, sg, a32), fabsf(fmaf(sraw, CLAMP_BAND_INV, -CLAMP_F * CLAMP_BAND_INV)));
-  if (act && key <= 1.0f) {  // rare: decide in the reference's order
+  bool ok = uu < U9_LO && fminf(sraw, CLAMP_F) >= SKIP_F;
+  const float key = fminf(amb_key(uu, fminf(sraw, CLAMP_F), a32),
+                          fabsf(fmaf(sraw, CLAMP_BAND_INV, -CLAMP_F * CLAMP_BAND_INV)));
+  double sg, gauss;
+  if (key <= 1.0f) {  // rare: decide (and evaluate) in the reference's order
     const BwExact x = bw_exact_entry(E, fx, fy);
-    ok = x.sig >= 0.0f;
+    ok = x.sig >= 0.0;
     sg = x.sig;
     gauss = x.gauss;
     clamped = x.clamped;
+  } else {
+    gauss = exp2_neg64(u, uu, tab);
+    sg = clamped ? ALPHA_CLAMP : E.d.x * gauss;
   }
   if (!ok) return;
-  const float4 col = E.f.col;  // alpha, r, g, b
-  // one reciprocal for the five divisions of kernels.py:135,142-146; 1 - sigma
-  // is in [0.01, 1) (no special cases): SFU estimate + one Newton step (~1 ulp,
-  // 3 instructions instead of the IEEE-rn sequence)
-  const float om = 1.0f - sg;
-  float inv = rcp_approx(om);
-  inv = fmaf(inv, fmaf(-om, inv, 1.0f), inv);
-  const float t_before = q.t_after * inv;
-  const float w = sg * t_before;
-  v[6] = fmaf(q.gr, w, v[6]);
-  v[7] = fmaf(q.gg, w, v[7]);
-  v[8] = fmaf(q.gb, w, v[8]);
-  float s_i = (q.gr * (col.y * t_before - q.acc_r * inv) + q.gg * (col.z * t_before - q.acc_g * inv)) +
-              q.gb * (col.w * t_before - q.acc_b * inv);
-  s_i = fmaf(q.gtp, -q.t_fin * inv, s_i);
-  if (!clamped) {
-    const float4 con = E.f.con;  // conic xx, xy, yy
-    const float dxf = (float)dx, dyf = (float)dy;
-    const float qd_x = fmaf(con.x, dxf, con.y * dyf);
-    const float qd_y = fmaf(con.y, dxf, con.z * dyf);
-    const float common = s_i * sg;
-    const float hc = 0.5f * common;
-    v[0] = fmaf(common, qd_x, v[0]);
-    v[1] = fmaf(common, qd_y, v[1]);
-    v[2] = fmaf(hc * qd_x, qd_x, v[2]);
-    v[3] = fmaf(hc * qd_x, qd_y, v[3]);
-    v[4] = fmaf(hc * qd_y, qd_y, v[4]);
-    v[5] = fmaf(s_i, gauss, v[5]);
-  }
-  q.acc_r = fmaf(col.y, w, q.acc_r);
-  q.acc_g = fmaf(col.z, w, q.acc_g);
-  q.acc_b = fmaf(col.w, w, q.acc_b);
+  // g . c_i (the colour enters s_i only through it); colour r from the fp64
+  // record, g / b from the fp32 record
+  const double gc = fma((double)q.gr, E.d.y, fma((double)q.gg, (double)E.f.col.z, (double)q.gb * E.f.col.w));
+  // one reciprocal for the divisions of kernels.py:135,142-146
+  const double inv = rcp64(1.0 - sg);
+  const double t_before = q.t_after * inv;
+  const double w = sg * t_before;
+  const double s_i = fma(gc, t_before, -q.q * inv);
+  q.q = fma(gc, w, q.q);
   q.t_after = t_before;
+  const float w32 = (float)w;
+  vf[1] = fmaf(q.gr, w32, vf[1]);
+  vf[2] = fmaf(q.gg, w32, vf[2]);
+  vf[3] = fmaf(q.gb, w32, vf[3]);
+  if (!clamped) {
+    const double cx = E.b.x, cy = 0.5 * E.b.y, cz = E.c.x;  // conic xx, xy, yy
+    const double qd_x = fma(cx, dx, cy * dy);
+    const double qd_y = fma(cy, dx, cz * dy);
+    const double common = s_i * sg;
+    vd[0] = fma(common, qd_x, vd[0]);
+    vd[1] = fma(common, qd_y, vd[1]);
+#if HGS_BW_V64 >= 5
+    const double hc = 0.5 * common;
+    vd[2] = fma(hc * qd_x, qd_x, vd[2]);
+    vd[3] = fma(hc * qd_x, qd_y, vd[3]);
+    vd[4] = fma(hc * qd_y, qd_y, vd[4]);
+#else
+    const float hc = 0.5f * (float)common, qx = (float)qd_x, qy = (float)qd_y;
+    vd[2] = (double)fmaf(hc * qx, qx, (float)vd[2]);
+    vd[3] = (double)fmaf(hc * qx, qy, (float)vd[3]);
+    vd[4] = (double)fmaf(hc * qy, qy, (float)vd[4]);
+#endif
+    vf[0] = fmaf((float)s_i, (float)gauss, vf[0]);
+  }
 }
 
 __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel(
@@ -248,6 +272,7 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
     sm.max_last = -1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  exp2_tab_load(sm.exp2tab);
   __syncthreads();
   // consumer pixels: warp w owns the 8x8 sub-tile (w & 1, w >> 1); lane
   // (x, y) = (lane & 7, lane >> 3) holds pixels (x, y) and (x, y + 4)
@@ -330,15 +355,15 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
     for (int li = 0; li < nl; li++) {
       const int i = sm.list[warp][li];
       const StageEntry& E = sm.ent[slot][i];
-      float v[9];
-#pragma unroll
-      for (int c = 0; c < 9; c++) v[c] = 0.0f;
-      bw_pixel_step(q0, E, lo + i, fx, fy0, v);
-      bw_pixel_step(q1, E, lo + i, fx, fy1, v);
-      const bool any = v[6] != 0.0f || v[7] != 0.0f || v[8] != 0.0f || v[5] != 0.0f || v[0] != 0.0f;
+      double vd[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      float vf[4] = {0.f, 0.f, 0.f, 0.f};
+      bw_pixel_step(q0, E, lo + i, fx, fy0, sm.exp2tab, vd, vf);
+      bw_pixel_step(q1, E, lo + i, fx, fy1, sm.exp2tab, vd, vf);
+      const bool any = vf[1] != 0.f || vf[2] != 0.f || vf[3] != 0.f || vf[0] != 0.f || vd[0] != 0.0;
       if (!__any_sync(0xffffffffu, any)) continue;
-      const float tot = warp_reduce9(v, lane);
-      if (vidx >= 0 && tot != 0.0f) atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
+      double v[9] = {vd[0], vd[1], vd[2], vd[3], vd[4], (double)vf[0], (double)vf[1], (double)vf[2], (double)vf[3]};
+      const double tot = warp_reduce9(v, lane);
+      if (vidx >= 0 && tot != 0) atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);

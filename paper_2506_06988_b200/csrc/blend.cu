@@ -45,6 +45,9 @@ constexpr int BLEND_THREADS = BLEND_TILE * BLEND_TILE;
 #ifndef HGS_FAST_MINB
 #define HGS_FAST_MINB 4
 #endif
+#ifndef HGS_FAST_MINB_PREC
+#define HGS_FAST_MINB_PREC 3
+#endif
 constexpr int BATCH = HGS_FAST_BATCH;
 constexpr int NSTAGE = HGS_FAST_NSTAGE;
 constexpr int CONSUMERS = 8;
@@ -55,6 +58,7 @@ struct FastSmem {
   unsigned long long full[NSTAGE];
   unsigned long long empty[NSTAGE];
   unsigned char list[CONSUMERS][BATCH];
+  double exp2tab[16];
   int done_warps;
   int end_batch;
   unsigned long long stats[2];
@@ -72,7 +76,7 @@ __device__ __forceinline__ double mask_value(double t, double k, int variant) {
 __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_mesh_layer& mesh, bool mesh_here,
                                             int64_t p, double T, double r, double g, double b, double dacc,
                                             double acc, int64_t last, double bg0, double bg1, double bg2, int mask_variant,
-                                            double mask_k) {
+                                            double mask_k, double T_state) {
   double oc0, oc1, oc2, od;
   if (mesh_here) {
     oc0 = r + T * (double)mesh.color[3 * p];
@@ -90,21 +94,21 @@ __device__ __forceinline__ void write_pixel(const hgs_blend_out& out, const hgs_
   out.color[3 * p + 2] = (float)oc2;
   out.depth[p] = (float)od;
   out.transmittance[p] = (float)T;
-  if (out.final_t) out.final_t[p] = T;
+  if (out.final_t) out.final_t[p] = T_state;
   if (out.last) out.last[p] = (int32_t)last;
   if (out.mask) out.mask[p] = (float)mask_value(T, mask_k, mask_variant);
 }
 
 // Exact re-evaluation of one entry in the reference's operation order
-// (kernels.py:42-51): support test, fp64 exp, clamp, skip.  Returns sigma
-// (narrowed), or -1 when the entry is not blended.
-__device__ __noinline__ float exact_entry(const StageEntry& E, double fx, double fy) {
+// (kernels.py:42-51): support test, fp64 exp, clamp, skip.  Returns sigma,
+// or -1 when the entry is not blended.
+__device__ __noinline__ double exact_entry(const StageEntry& E, double fx, double fy) {
   const double dx = fx - E.a.x, dy = fy - E.a.y;
   const double m = E.b.x * dx * dx + E.b.y * dx * dy + E.c.x * dy * dy;
-  if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0f;
+  if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0;
   double sg = E.d.x * exp(-0.5 * m);
   if (sg > ALPHA_CLAMP) sg = ALPHA_CLAMP;
-  return sg < SIGMA_SKIP ? -1.0f : (float)sg;
+  return sg < SIGMA_SKIP ? -1.0 : sg;
 }
 
 // Exact walk of one pixel by one warp (fp64 exp()): lanes evaluate
@@ -284,8 +288,12 @@ __device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec,
   return ExactPixel{T, pr, pg, pb, pd, last};
 }
 
-template <bool STATS>
-__global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel(
+// PREC (the caller asked for the backward state final_t): T is also carried
+// in fp64 with sigma from the fp64 exp2 (stage.cuh) for every blended entry,
+// i.e. the reference's T recurrence to ~1e-11 relative; only final_t takes
+// it -- colour / T / depth outputs are the same fp32 values as without.
+template <bool STATS, bool PREC>
+__global__ void __launch_bounds__(FAST_THREADS, PREC ? HGS_FAST_MINB_PREC : HGS_FAST_MINB) blend_fast_kernel(
     const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
@@ -308,6 +316,7 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
     sm.stats[0] = sm.stats[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (PREC) exp2_tab_load(sm.exp2tab);
   __syncthreads();
   const int tx = tile % tiles_x, ty = tile / tiles_x;
 
@@ -361,6 +370,7 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
   bool flagged = false;
   bool warp_done = false;
   float T = 1.0f;     // transmittance
+  double T64 = 1.0;   // PREC: the reference's fp64 T
   float eT = 0.0f;    // bound on |T - T_reference| (valid while not done)
   float acc = 0.0f;   // sum of blend weights (= 1 - T_reference up to rounding)
   float r = 0.0f, g = 0.0f, bl = 0.0f, dacc = 0.0f;
@@ -397,7 +407,8 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
           int jj[2];
           jj[0] = sm.list[warp][li];
           jj[1] = has1 ? sm.list[warp][li + 1] : jj[0];
-          float sg[2];
+          float sg[2], uf[2];
+          double um[2];
           bool ok[2], dstop[2];
           float key = 2.0f;
 #pragma unroll
@@ -407,7 +418,9 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
             const float a32 = E.f.col.x;
             const double dx = fx - A.x, dy = fy - A.y;
             const double m = fma(dx, fma(B.y, dy, B.x * dx), (C.x * dy) * dy);
-            const float uu = __double2float_rn(m * U_SCALE);
+            um[u] = m * U_SCALE;
+            const float uu = __double2float_rn(um[u]);
+            uf[u] = uu;
             const float sgf = fminf(fabsf(a32) * ex2_neg(uu), CLAMP_F);
             dstop[u] = C.y >= limit;
             ok[u] = uu < U9_LO && sgf >= SKIP_F;
@@ -441,6 +454,14 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
             dacc = fmaf(d1, w1, fmaf(d0, w0, dacc));
             acc = (acc + w0) + w1;
             T = T2;
+            if (PREC) {  // no entry of the step is ambiguous: fp32 decisions are the reference's
+              double f0 = 1.0, f1 = 1.0;
+              if (s0 > 0.0f)
+                f0 = 1.0 - fmin(sm.ent[slot][jj[0]].d.x * exp2_neg64(um[0], uf[0], sm.exp2tab), ALPHA_CLAMP);
+              if (s1 > 0.0f)
+                f1 = 1.0 - fmin(sm.ent[slot][jj[1]].d.x * exp2_neg64(um[1], uf[1], sm.exp2tab), ALPHA_CLAMP);
+              T64 = (T64 * f0) * f1;
+            }
             const int bb = b * BATCH;
             last = s1 > 0.0f ? bb + jj[1] : (s0 > 0.0f ? bb + jj[0] : last);
             if (STATS && !done) {
@@ -449,16 +470,16 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
             }
             continue;
           }
+          double sx[2] = {-1.0, -1.0};  // exact sigma of re-evaluated entries
           if (__any_sync(0xffffffffu, key <= 1.0f)) {  // rare: exact per-entry re-evaluation
 #pragma unroll
             for (int u = 0; u < 2; u++) {
               const StageEntry& E = sm.ent[slot][jj[u]];
-              const double dx = fx - E.a.x, dy = fy - E.a.y;
-              const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
-              if (amb_key(__double2float_rn(m * U_SCALE), sg[u], E.f.col.x) <= 1.0f) {
-                const float x = exact_entry(E, fx, fy);
-                ok[u] = x >= 0.0f;
-                sg[u] = x;
+              if (amb_key(uf[u], sg[u], E.f.col.x) <= 1.0f) {
+                const double x = exact_entry(E, fx, fy);
+                ok[u] = x >= 0.0;
+                sg[u] = (float)x;
+                sx[u] = x;
               }
             }
           }
@@ -495,6 +516,8 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
             if (upd) {
               last = b * BATCH + jj[u];
               if (STATS) blended++;
+              if (PREC)
+                T64 *= 1.0 - (sx[u] >= 0.0 ? sx[u] : fmin(E.d.x * exp2_neg64(um[u], uf[u], sm.exp2tab), ALPHA_CLAMP));
             }
           }
           if (__all_sync(0xffffffffu, done)) break;
@@ -525,7 +548,7 @@ __global__ void __launch_bounds__(FAST_THREADS, HGS_FAST_MINB) blend_fast_kernel
     return;
   }
   write_pixel(out, mesh, mesh_here, p, T, r, g, bl, dacc, acc, last >= 0 ? s + last : -1, bg0, bg1, bg2,
-              mask_variant, mask_k);
+              mask_variant, mask_k, PREC ? T64 : (double)T);
 }
 
 // The exact walk, one warp per pixel (persistent grid-stride): over the
@@ -550,7 +573,7 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
                                     limit, lane);
     if (lane == 0)
       write_pixel(out, mesh, mesh_here, p, q.T, q.r, q.g, q.b, q.dacc, 1.0 - q.T, q.last, bg0, bg1, bg2,
-                  mask_variant, mask_k);
+                  mask_variant, mask_k, q.T);
   }
 }
 
@@ -577,26 +600,28 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
   cudaStream_t st = (cudaStream_t)stream;
   const int n_tiles = tiles->tiles_x * tiles->tiles_y;
   const int64_t npix = (int64_t)width * height;
-  if (out->fixup && proj->cull) {
+#ifndef HGS_FWD_EXACT
+#define HGS_FWD_EXACT 0
+#endif
+  if (out->fixup && proj->cull && !HGS_FWD_EXACT) {
     zero_pdl(st, out->fixup, sizeof(int32_t));
     HGS_CHECK_LAUNCH();
     const size_t smem = sizeof(FastSmem);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(blend_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(blend_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute(blend_fast_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(blend_fast_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      for (auto fn : {blend_fast_kernel<false, false>, blend_fast_kernel<true, false>, blend_fast_kernel<false, true>,
+                      blend_fast_kernel<true, true>}) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      }
       attr = true;
     }
-    if (out->stats)
-      launch_pdl(blend_fast_kernel<true>, dim3(n_tiles), dim3(FAST_THREADS), smem, st, 
-          (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
-          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
-    else
-      launch_pdl(blend_fast_kernel<false>, dim3(n_tiles), dim3(FAST_THREADS), smem, st, 
-          (const BlendRec*)proj->rec, (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x,
-          width, height, ml, bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
+    const bool prec = out->final_t != nullptr;
+    auto fn = out->stats ? (prec ? blend_fast_kernel<true, true> : blend_fast_kernel<true, false>)
+                         : (prec ? blend_fast_kernel<false, true> : blend_fast_kernel<false, false>);
+    launch_pdl(fn, dim3(n_tiles), dim3(FAST_THREADS), smem, st, (const BlendRec*)proj->rec,
+               (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x, width, height, ml,
+               bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
     HGS_CHECK_LAUNCH();
     // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)
     launch_pdl(blend_exact_kernel, dim3(2 * NUM_SMS), dim3(256), 0, st, (const BlendRec*)proj->rec, tiles->entries,

@@ -95,21 +95,34 @@ __global__ void mesh_project_kernel(const hgs_camera* __restrict__ cam, const fl
   out[i] = make_double3(cam->fx * t[0] / safe + cam->cx, cam->fy * t[1] / safe + cam->cy, t[2]);
 }
 
+__device__ __forceinline__ void cas128(unsigned long long* rec, unsigned long long cz, unsigned long long cf,
+                                       unsigned long long nz, unsigned long long nf, unsigned long long& oz,
+                                       unsigned long long& of) {
+  asm volatile(
+      "{\n\t.reg .b128 c, n, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 n, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, n;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(oz), "=l"(of)
+      : "l"(cz), "l"(cf), "l"(nz), "l"(nf), "l"(rec)
+      : "memory");
+}
+
 __device__ __forceinline__ void zrec_min(unsigned long long* rec, unsigned long long zb, unsigned long long f) {
-  // lexicographic (z bits, triangle) minimum; the CAS returns the current
-  // record, so a torn initial read only costs one more iteration
-  unsigned long long cz = rec[0], cf = rec[1];
+  // lexicographic (z bits, triangle) minimum.  The record only ever
+  // decreases, so a z word read at any time bounds the current one from
+  // above: zb > cz is a safe reject.  The two plain 64-bit loads may pair a
+  // newer z with an older triangle id, so a z tie is confirmed with an
+  // atomic read (a CAS that writes back what it expects) before rejecting;
+  // a failed CAS returns the coherent current record.
+  unsigned long long cz = *(volatile unsigned long long*)rec;
+  if (zb > cz) return;
+  unsigned long long cf = *(volatile unsigned long long*)(rec + 1);
+  if (zb == cz && f >= cf) cas128(rec, cz, cf, cz, cf, cz, cf);
   while (zb < cz || (zb == cz && f < cf)) {
     unsigned long long oz, of;
-    asm volatile(
-        "{\n\t.reg .b128 c, n, o;\n\t"
-        "mov.b128 c, {%2, %3};\n\t"
-        "mov.b128 n, {%4, %5};\n\t"
-        "atom.global.cas.b128 o, [%6], c, n;\n\t"
-        "mov.b128 {%0, %1}, o;\n\t}"
-        : "=l"(oz), "=l"(of)
-        : "l"(cz), "l"(cf), "l"(zb), "l"(f), "l"(rec)
-        : "memory");
+    cas128(rec, cz, cf, zb, f, oz, of);
     if (oz == cz && of == cf) return;
     cz = oz;
     cf = of;

@@ -119,4 +119,55 @@ __device__ __forceinline__ float ex2_neg(float u) {
   return e;
 }
 
+// ---- fp64 sigma for the training state ---------------------------------
+// The backward reconstructs T before every entry from the final T of the
+// forward, so the final T and the per-entry sigma it is built from must be
+// accurate far beyond fp32 for the gradients to hold the 1e-4 absolute
+// contract at |g| ~ 4e2 (measured: fp32 T / sigma leave 2.6e-4 at c3).
+// 2^-u in fp64, u >= 0: u = k/16 + r with k = floor(16 uu) from the fp32
+// argument (r in [-2^-20, 1/16)), 2^-r by a degree-5 Taylor polynomial
+// (|r ln2| < 0.0434: truncation < 1e-11 relative), 2^(-k/16) = table[k & 15]
+// x 2^-(k >> 4) (exact power of two).  The 16-entry table lives in shared
+// memory (128 B: one entry per bank pair, conflict-free).
+__constant__ double c_exp2_tab[16] = {1.0,
+                                      0.9576032806985737,
+                                      0.9170040432046712,
+                                      0.8781260801866497,
+                                      0.8408964152537145,
+                                      0.8052451659746271,
+                                      0.7711054127039704,
+                                      0.7384130729697497,
+                                      0.7071067811865476,
+                                      0.6771277734684463,
+                                      0.6484197773255048,
+                                      0.620928906036742,
+                                      0.5946035575013605,
+                                      0.5693943173783458,
+                                      0.5452538663326288,
+                                      0.5221368912137069};
+__device__ __forceinline__ void exp2_tab_load(double* tab) {
+  if (threadIdx.x < 16) tab[threadIdx.x] = c_exp2_tab[threadIdx.x];
+}
+__device__ __forceinline__ double exp2_neg64(double u, float uu, const double* tab) {
+  const int k = __float2int_rd(fminf(fmaxf(uu, 0.0f), 60.0f) * 16.0f);
+  const double r = fma((double)k, -0.0625, u);
+  double p = -0.0013333558146428441;
+  p = fma(p, r, 0.009618129107628477);
+  p = fma(p, r, -0.055504108664821576);
+  p = fma(p, r, 0.2402265069591007);
+  p = fma(p, r, -0.6931471805599453);
+  p = fma(p, r, 1.0);
+  const double t = p * tab[k & 15];  // in (0.5, 1.03]: x 2^-(k >> 4) by the exponent field
+  return __hiloint2double(__double2hiint(t) - ((k >> 4) << 20), __double2loint(t));
+}
+// 1 / x for x in [0.01, 1] in fp64: SFU estimate from the high word
+// (relative error < 2^-19) + one Newton step (< 2^-38: far below what the
+// gradients need, ~1e-9)
+__device__ __forceinline__ double rcp64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 }  // namespace hgs

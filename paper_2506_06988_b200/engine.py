@@ -104,17 +104,21 @@ class HybridRenderer:
         ev.record(torch.cuda.current_stream(self.dev))
         self._cam_ev[k] = ev
 
-    def render_to_host(self, cam, out_host: torch.Tensor) -> torch.cuda.Event:
-        """Serving path: camera H2D, one replay of the frame graph, a device
-        snapshot of the colour image and its D2H into ``out_host`` (pinned,
-        H x W x 3 fp32) on a copy stream, so the transfer overlaps the next
-        frame.  Snapshots are double-buffered.  Returns the event that marks
-        the copy complete (the caller must not reuse ``out_host`` before)."""
+    def render_to_host(self, cam, out_color: torch.Tensor, out_depth: Optional[torch.Tensor] = None,
+                       out_trans: Optional[torch.Tensor] = None) -> torch.cuda.Event:
+        """Serving path: camera H2D, one replay of the frame graph, device
+        snapshots of the colour image (and, when given, the depth and
+        transmittance images -- the reference's RenderOutputs) and their D2H
+        into the pinned host tensors (H x W x 3 / H x W fp32) on a copy
+        stream, so the transfer overlaps the next frame.  Snapshots are
+        double-buffered.  Returns the event that marks the copies complete
+        (the caller must not reuse the host tensors before)."""
         if self.graph is None:
             self.capture()
         if getattr(self, "_copy", None) is None:
             self._copy = torch.cuda.Stream(self.dev)
-            self._snap = [torch.empty_like(self.color) for _ in range(2)]
+            self._snap = [(torch.empty_like(self.color), torch.empty_like(self.depth), torch.empty_like(self.trans))
+                          for _ in range(2)]
             self._snap_ev = [None, None]
             self._snap_k = 0
         k = self._snap_k
@@ -124,12 +128,17 @@ class HybridRenderer:
             main.wait_event(self._snap_ev[k])  # the previous D2H from this snapshot is done
         self.set_camera(cam)
         self.graph.replay()
-        self._snap[k].copy_(self.color, non_blocking=True)
+        pairs = [(out_color, self.color, self._snap[k][0]), (out_depth, self.depth, self._snap[k][1]),
+                 (out_trans, self.trans, self._snap[k][2])]
+        pairs = [p for p in pairs if p[0] is not None]
+        for _, src, snap in pairs:
+            snap.copy_(src, non_blocking=True)
         ready = torch.cuda.Event()
         ready.record(main)
         self._copy.wait_event(ready)
         with torch.cuda.stream(self._copy):
-            out_host.copy_(self._snap[k], non_blocking=True)
+            for host, _, snap in pairs:
+                host.copy_(snap, non_blocking=True)
         done = torch.cuda.Event()
         done.record(self._copy)
         self._snap_ev[k] = done
@@ -240,7 +249,8 @@ class HybridRenderer:
                                   self.height, TILE_PX, self.cull, self.sort_keys, self.tile_diff)
 
     def tiles(self) -> TileBins:
-        return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected())
+        return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected(),
+                        counters=self.counters, capacity=int(self.entries.numel()))
 
     def layer(self) -> Optional[MeshLayer]:
         if self.mesh is None:

@@ -134,8 +134,13 @@ class TileBins:
     ``entries_orig`` are the original Gaussian rows the kernels consume."""
 
     def __init__(self, tile_starts, entries_orig, tiles_x, tiles_y, tile_px, proj: Optional[ProjectedGaussians] = None,
-                 k: Optional[int] = None):
+                 k: Optional[int] = None, counters: Optional[torch.Tensor] = None, capacity: Optional[int] = None):
         self.tile_starts = tile_starts
+        # the binning counters (M, K, overflow flag, ...) travel with the bins:
+        # every consumer kernel returns early on an overflowed buffer instead
+        # of reading entries past the capacity
+        self.counters = counters
+        self.capacity = capacity
         self.entries_orig = entries_orig
         self.tiles_x, self.tiles_y, self.tile_px = tiles_x, tiles_y, tile_px
         self._proj = proj
@@ -169,9 +174,11 @@ class TileBins:
     def struct(self, counters=None, capacity=None) -> _lib.HGSTiles:
         s = _lib.HGSTiles()
         s.tiles_x, s.tiles_y, s.tile_px = self.tiles_x, self.tiles_y, self.tile_px
-        s.capacity = capacity if capacity is not None else len(self.entries_orig)
+        if capacity is None:
+            capacity = self.capacity if self.capacity is not None else len(self.entries_orig)
+        s.capacity = capacity
         s.entries, s.tile_starts = _lib.ptr(self.entries_orig), _lib.ptr(self.tile_starts)
-        s.counters = _lib.ptr(counters)
+        s.counters = _lib.ptr(counters if counters is not None else self.counters)
         return s
 
 
@@ -313,7 +320,7 @@ def _tiles_core(proj: ProjectedGaussians, width: int, height: int, tile_px: int,
     ts.entries, ts.tile_starts, ts.counters = _lib.ptr(entries), _lib.ptr(tile_starts), _lib.ptr(counters)
     ts.scratch, ts.scratch_bytes = _lib.ptr(scratch), scratch.numel()
     _lib.call("hgs_build_tiles", ctypes.byref(proj.struct()), proj.n, ctypes.byref(ts), _stream_ptr(dev))
-    return TileBins(tile_starts, entries, tx, ty, tile_px, proj), counters
+    return TileBins(tile_starts, entries, tx, ty, tile_px, proj, counters=counters, capacity=cap), counters
 
 
 def build_tiles(proj: ProjectedGaussians, width: int, height: int, tile_px: int = TILE_PX) -> TileBins:

@@ -155,13 +155,17 @@ class HybridTrainer:
         for lane in self.lanes:
             lane.alloc_rows(n, (self.tx, self.ty))
 
-    def _density_step(self, it: int) -> None:
-        """loop.py:226-233 after the optimiser steps of iteration ``it``."""
+    def _density_step(self, it: int, nb: int) -> None:
+        """loop.py:226-233 after the optimiser steps of iteration ``it``
+        (a step over ``nb`` views)."""
         from .densify import densify_and_prune, reset_opacity
         cfg = self.cfg
         if it >= cfg.densify_until_iter:
             return
-        self.dstate.update(self.grads.visible_count, self.grads.densify_norm)
+        # the views' losses were scaled by 1/nb (batch mean), and the norm
+        # is linear in that scale: x nb restores the sum of the per-view
+        # norms the reference accumulates one view at a time (densify.py:31-33)
+        self.dstate.update(self.grads.visible_count, self.grads.densify_norm * nb)
         if it >= cfg.densify_from_iter and it % cfg.densify_interval == 0:
             self.gs, stats = densify_and_prune(self.gs, self.opt, self.dstate, self.extent, cfg, self.rng)
             stats["iter"] = it
@@ -200,7 +204,8 @@ class HybridTrainer:
         ts.scratch, ts.scratch_bytes = _lib.ptr(lane.tiles_scratch), lane.tiles_scratch.numel()
         _lib.call("hgs_build_tiles", ctypes.byref(proj.struct()), len(self.gs), ctypes.byref(ts), _stream_ptr(self.dev))
         lane.overflow += lane.counters[2:3]
-        return TileBins(lane.tile_starts, lane.entries, self.tx, self.ty, TILE_PX, proj)
+        return TileBins(lane.tile_starts, lane.entries, self.tx, self.ty, TILE_PX, proj, counters=lane.counters,
+                        capacity=lane.capacity)
 
     def mesh_layer(self, v) -> Optional[MeshLayer]:
         """Texture lookup over the cached fragments (loop.py:189-199)."""
@@ -296,5 +301,5 @@ class HybridTrainer:
         if self.tex_opt is not None:
             self.tex_opt.step({"texture": self.tex_grad}, clamp=("texture",))
         if self.density_control:
-            self._density_step(it)
+            self._density_step(it, nb)
         return self.loss_sum

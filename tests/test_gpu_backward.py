@@ -15,6 +15,9 @@ from oracle import oracle as orc
 pytestmark = pytest.mark.gpu
 
 GROUPS = ("centers", "rotations", "log_scales", "logit_opacities", "colors_dc")
+# per-pixel loss gradients (fp32 maps, fp64 filter arithmetic) vs the fp64
+# reference, relative to the map's scale
+LOSS_GRAD_REL = 1e-5
 
 
 def np_(t):
@@ -105,10 +108,13 @@ def test_composite_loss_matches_reference(cuda_device):
                                              out.transmittance, it, _Cfg)
     got = np.array([bd.l1, bd.dssim, bd.l_c, bd.l_t, bd.total, bd.mean_t_on_mesh])
     assert_close(got, d["l_values"], atol=1e-6, rtol=1e-5, what="loss values")
-    # per-pixel loss gradients are ~1/(3HW): compare relative to their scale
+    # per-pixel loss gradients are ~1/(3HW): compare relative to their scale.
+    # LOSS_GRAD_REL: the gradient maps are stored fp32 and the SSIM
+    # derivative maps pass between the forward and adjoint tiles as fp32
     for a, b, nm in ((gih, d["l_grad_ih"], "grad_ih"), (gim, d["l_grad_im"], "grad_im"), (gt, d["l_grad_t"], "grad_t")):
         scale = np.abs(b).max()
-        assert np.abs(np_(a) - b).max() <= 1e-3 * scale, nm
+        err = np.abs(np_(a) - b).max()
+        assert err <= LOSS_GRAD_REL * scale, f"{nm}: {err / scale:.2e} of scale"
 
 
 def test_transmittance_mask_constants(cuda_device):
@@ -168,10 +174,11 @@ def test_c2_backward_matches_oracle(cuda_device):
     rng = np.random.default_rng(5)
     gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
     gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
-    *_, octx = orc.render(sc.gaussians, cam, (0, 0, 0), _mesh_oracle(sc.gaussians, cam, sc.mesh))
+    color, depth, tt, octx = orc.render(sc.gaussians, cam, (0, 0, 0), _mesh_oracle(sc.gaussians, cam, sc.mesh))
     og = orc.backward(octx, gc, gt)
     layer = mr.mesh_layer(m, c)
-    _, ctx = hgs.render(g, c, background=(0, 0, 0), mesh=layer)
+    out, ctx = hgs.render(g, c, background=(0, 0, 0), mesh=layer)
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
     gr = hgs.rasterize_backward(ctx, gc, gt)
     for k in GROUPS:
         grad_close(np_(getattr(gr, k)), getattr(og, k), atol=1e-4, scale_tol=1e-4, what=k)
@@ -208,8 +215,8 @@ def test_training_reduces_the_loss(cuda_device):
 def test_c3_frame_and_backward_match_oracle(cuda_device):
     """The headline configuration (1M Gaussians, 200k-triangle textured
     mesh, 1200x680): tile bins, triangle ids and last-consumed indices
-    bit-exact, colour / T within 1e-5, all parameter gradients within the
-    gradient tolerance."""
+    bit-exact, colour / T within 1e-5, depth within 1e-4, all parameter
+    gradients within 1e-4 absolute."""
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import meshraster as mr
     from paper_2506_06988_b200 import synthetic as syn
@@ -228,20 +235,18 @@ def test_c3_frame_and_backward_match_oracle(cuda_device):
     assert np.array_equal(np_(ctx.last_consumed), octx["last"])
     assert_close(np_(out.color), color, atol=1e-5, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
     rng = np.random.default_rng(9)
     gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
     gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
     og = orc.backward(octx, gc, gt)
     gr = hgs.rasterize_backward(ctx, gc, gt)
-    # At this scale the centre gradients reach |g| ~ 4e2 (the screen-space
-    # mean gradient times focal / depth); fp32 gradient arithmetic holds
-    # ~6e-7 of a group's scale, so the bound is max(1e-4, 2e-6 max|g|) per
-    # group -- 1e-4 absolute for every group whose scale is below 50.
+    # north_star: 1e-4 absolute for every group, although the centre
+    # gradients reach |g| ~ 4e2 here (screen-space mean gradient x focal /
+    # depth): the training forward carries the fp64 T and the backward its
+    # reverse recurrence in fp64 (measured max 3.9e-5, tools/diag_bw_variants.py)
     for k in GROUPS:
-        a, b = np_(getattr(gr, k)), getattr(og, k)
-        bound = max(1e-4, 2e-6 * np.abs(b).max())
-        err = np.abs(a - b).max()
-        assert err <= bound, f"{k}: max abs err {err:.3e} > {bound:.3e} (scale {np.abs(b).max():.3g})"
+        grad_close(np_(getattr(gr, k)), getattr(og, k), atol=1e-4, scale_tol=1e-4, what=k)
 
 
 def test_c2_sh1_forward_backward_match_oracle(cuda_device):
@@ -263,8 +268,9 @@ def test_c2_sh1_forward_backward_match_oracle(cuda_device):
     layer = mr.mesh_layer(m, c)
     out, ctx = hgs.render(g, c, background=(0.1, 0.2, 0.3), mesh=layer)
     assert np.array_equal(ctx.last_consumed.cpu().numpy(), octx["last"])
-    assert np.abs(np_(out.color) - color).max() < 1e-5
-    assert np.abs(np_(out.transmittance) - tt).max() < 1e-5
+    assert_close(np_(out.color), color, atol=1e-5, what="color")
+    assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
     gr = hgs.rasterize_backward(ctx, gc, gt)
     for k in GROUPS + ("colors_rest",):
         grad_close(np_(getattr(gr, k)), getattr(og, k), atol=1e-4, scale_tol=1e-4, what=k)
@@ -288,9 +294,9 @@ def test_engine_mask_epilogue_matches_oracle(variant, cuda_device):
 
 
 def test_c4_training_view_backward_matches_oracle(cuda_device):
-    """Gradients of a c4 training camera inside the room (1M Gaussians, most
-    rows culled) against the oracle, with the c3 bound: max(1e-4, 2e-6 of the
-    group's scale)."""
+    """Image, depth and gradients of a c4 training camera inside the room (1M
+    Gaussians, most rows culled) against the oracle; gradients at 1e-4
+    absolute."""
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import meshraster as mr
     from paper_2506_06988_b200 import synthetic as syn
@@ -300,16 +306,16 @@ def test_c4_training_view_backward_matches_oracle(cuda_device):
     color, depth, tt, octx = orc.render(sc.gaussians, cam, (0, 0, 0), _mesh_oracle(sc.gaussians, cam, sc.mesh))
     out, ctx = hgs.render(g, c, background=(0, 0, 0), mesh=mr.mesh_layer(m, c))
     assert np.array_equal(np_(ctx.last_consumed), octx["last"])
+    assert_close(np_(out.color), color, atol=1e-5, what="color")
+    assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
     rng = np.random.default_rng(21)
     gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
     gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
     og = orc.backward(octx, gc, gt)
     gr = hgs.rasterize_backward(ctx, gc, gt)
     for k in GROUPS:
-        a, b = np_(getattr(gr, k)), getattr(og, k)
-        bound = max(1e-4, 2e-6 * np.abs(b).max())
-        err = np.abs(a - b).max()
-        assert err <= bound, f"{k}: max abs err {err:.3e} > {bound:.3e} (scale {np.abs(b).max():.3g})"
+        grad_close(np_(getattr(gr, k)), getattr(og, k), atol=1e-4, scale_tol=1e-4, what=k)
     assert np.array_equal(np_(gr.visible).astype(bool), octx_visible(octx, len(sc.gaussians.centers)))
 
 
@@ -322,7 +328,7 @@ def octx_visible(octx, n):
 def test_c5_stress_matches_oracle(cuda_device):
     """The stress configuration (5M Gaussians, 1M-triangle mesh, 1920x1080,
     ~140M tile entries): tile bins, triangle ids and blend order bit-exact,
-    image within 1e-5, gradients within the c3 bound."""
+    image within 1e-5, depth within 1e-4, gradients within 1e-4 absolute."""
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import meshraster as mr
     from paper_2506_06988_b200 import synthetic as syn
@@ -340,22 +346,20 @@ def test_c5_stress_matches_oracle(cuda_device):
     assert np.array_equal(np_(ctx.last_consumed), octx["last"])
     assert_close(np_(out.color), color, atol=1e-5, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
     rng = np.random.default_rng(31)
     gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
     gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
     og = orc.backward(octx, gc, gt)
     gr = hgs.rasterize_backward(ctx, gc, gt)
     for k in GROUPS:
-        a, b = np_(getattr(gr, k)), getattr(og, k)
-        bound = max(1e-4, 2e-6 * np.abs(b).max())
-        err = np.abs(a - b).max()
-        assert err <= bound, f"{k}: max abs err {err:.3e} > {bound:.3e} (scale {np.abs(b).max():.3g})"
+        grad_close(np_(getattr(gr, k)), getattr(og, k), atol=1e-4, scale_tol=1e-4, what=k)
 
 
 def test_c4_composite_loss_matches_oracle(cuda_device):
     """composite_loss (L1 + D-SSIM + texture term, losses.py:139-174) at the
     c4 training resolution on a real render: loss values at 1e-6 abs / 1e-5
-    rel, per-pixel gradients at 1e-3 of their scale (as the golden test)."""
+    rel, per-pixel gradients at LOSS_GRAD_REL of their scale (as the golden test)."""
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import losses
     from paper_2506_06988_b200 import meshraster as mr
@@ -378,14 +382,15 @@ def test_c4_composite_loss_matches_oracle(cuda_device):
     assert_close(got, ref, atol=1e-6, rtol=1e-5, what="loss values")
     for a, b, nm in ((gih, ogih, "grad_ih"), (gim, ogim, "grad_im"), (gt, ogt, "grad_t")):
         scale = np.abs(b).max()
-        assert np.abs(np_(a) - b).max() <= 1e-3 * scale, nm
+        err = np.abs(np_(a) - b).max()
+        assert err <= LOSS_GRAD_REL * scale, f"{nm}: {err / scale:.2e} of scale"
 
 
 @pytest.mark.parametrize("variant", ["sigmoid", "identity_t"])
 def test_individual_loss_terms_match_oracle(variant, cuda_device):
     """l1_loss, ssim, dssim and texture_loss (losses.py:41-116), the
     reference's public loss terms, against the oracle: values at 1e-9
-    relative, gradients at 1e-3 of their scale; no coverage -> zero."""
+    relative, gradients at LOSS_GRAD_REL of their scale; no coverage -> zero."""
     from paper_2506_06988_b200 import losses
     rng = np.random.default_rng(12)
     h, w = 57, 83  # not a multiple of the 16-px SSIM tile
@@ -396,7 +401,8 @@ def test_individual_loss_terms_match_oracle(variant, cuda_device):
     t = rng.uniform(0, 1, (h, w)).astype(np.float32).astype(np.float64)
 
     def close_grad(a, b, nm):
-        assert np.abs(np_(a) - b).max() <= 1e-3 * np.abs(b).max() + 1e-12, nm
+        err = np.abs(np_(a) - b).max()
+        assert err <= LOSS_GRAD_REL * np.abs(b).max() + 1e-12, f"{nm}: {err / np.abs(b).max():.2e} of scale"
 
     for fn in ("l1_loss", "ssim", "dssim"):
         v, g = getattr(losses, fn)(pr, gt)

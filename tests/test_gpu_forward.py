@@ -158,6 +158,7 @@ def test_c2_matches_oracle(cfg, cuda_device):
     assert np.array_equal(np_(ctx.last_consumed), last)
     assert_close(np_(out.color), color, atol=1e-6, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-6, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")  # NaN pattern equal (no coverage)
 
 
 def test_depth_order_exact_under_key_truncation(cuda_device):
@@ -214,6 +215,7 @@ def test_large_grid_bins_and_blend_match_oracle(wh, n, cuda_device):
     assert np.array_equal(np_(ctx.last_consumed), last)
     assert_close(np_(out.color), color, atol=1e-5, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
 
 
 def test_engine_entry_overflow_grows_and_rerenders(cuda_device):
@@ -244,7 +246,6 @@ def test_c5_stress_forward_backward(cuda_device):
     the engine frame (CUDA graph) equals the functional render bit for bit,
     renders are deterministic, T stays in [0, 1], the mesh triangle ids are
     the oracle's, and the backward produces finite gradients."""
-    import time
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import meshraster as mr
     from paper_2506_06988_b200 import synthetic as syn
@@ -266,10 +267,8 @@ def test_c5_stress_forward_backward(cuda_device):
     assert torch.equal(out.color, out2.color)
     tt = out.transmittance
     assert bool(((tt >= 0) & (tt <= 1)).all())
-    t0 = time.time()
     fr = orc.rasterize_fragments(sc.mesh.vertices, sc.mesh.triangles, sc.mesh.uvs, cam)
-    if time.time() - t0 < 120:
-        assert np.array_equal(np_(layer.triangle_id), fr.triangle_id)
+    assert np.array_equal(np_(layer.triangle_id), fr.triangle_id)
     rng = np.random.default_rng(0)
     gc = torch.as_tensor(rng.uniform(-1, 1, (c.height, c.width, 3)), dtype=torch.float32, device="cuda")
     gr = hgs.rasterize_backward(ctx, gc)
@@ -295,13 +294,17 @@ def test_engine_render_to_host_matches_functional_render(cuda_device):
     for c in cams:  # size the entry buffer for every view
         r.frame(c, sync_check=True)
     r.capture()
-    hosts = [torch.empty(h, w, 3).pin_memory() for _ in cams]
-    events = [r.render_to_host(c, hb) for c, hb in zip(cams, hosts)]
+    hosts = [(torch.empty(h, w, 3).pin_memory(), torch.empty(h, w).pin_memory(), torch.empty(h, w).pin_memory())
+             for _ in cams]
+    events = [r.render_to_host(c, *hb) for c, hb in zip(cams, hosts)]
     for ev in events:
         ev.synchronize()
-    for c, hb in zip(cams, hosts):
+    for c, (hc, hd, ht) in zip(cams, hosts):
         out, _ = hgs.render(g, c, background=(0, 0, 0), mesh=mr.mesh_layer(m, c))
-        assert torch.equal(hb, out.color.cpu())
+        assert torch.equal(hc, out.color.cpu())
+        assert torch.equal(hd.isnan(), out.depth.cpu().isnan())
+        assert torch.equal(torch.nan_to_num(hd), torch.nan_to_num(out.depth.cpu()))
+        assert torch.equal(ht, out.transmittance.cpu())
 
 
 @pytest.mark.parametrize("view", [0, 17])
@@ -333,6 +336,7 @@ def test_c4_training_view_matches_oracle(view, cuda_device):
     # ~1e-6 here (north_star tolerance: 1e-4)
     assert_close(np_(out.color), color, atol=1e-5, what="color")
     assert_close(np_(out.transmittance), tt, atol=1e-5, what="T")
+    assert_close(np_(out.depth), depth, atol=1e-4, what="depth")
 
 
 def test_pdl_launch_chain_does_not_change_results(cuda_device, tmp_path):
@@ -362,3 +366,45 @@ def test_pdl_launch_chain_does_not_change_results(cuda_device, tmp_path):
     env_on = {k: v for k, v in os.environ.items() if k != "HGS_PDL"}
     subprocess.run([sys.executable, str(script), str(out_on)], env=env_on, check=True, timeout=600)
     assert np.array_equal(np.load(out_off), np.load(out_on))
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_device_matches_reference_fixture_at_scale(cfg, cuda_device):
+    """The device path directly against outputs the REFERENCE wrote at scale
+    (tests/golden/make_golden_scale.py; no oracle in between): tile bins,
+    triangle ids and last-consumed indices bit-exact (SHA-256 of the
+    reference's arrays), colour / T / depth at 20k sampled pixels, and at c2
+    every gradient group at 5k sampled rows within 1e-4 absolute."""
+    import hashlib
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import meshraster as mr
+    from paper_2506_06988_b200 import synthetic as syn
+
+    def digest(a):
+        a = np.ascontiguousarray(a)
+        return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+
+    d = load_golden(f"scale_{cfg}")
+    sc = syn.make_config(cfg, seed=0)
+    cam = sc.cameras[0]
+    g, c, m = dev_scene(sc.gaussians, cam, sc.mesh)
+    fr = mr.rasterize_fragments(m, c)
+    assert digest(np_(fr.triangle_id).astype(np.int32)) == str(d["sha_tri"])
+    out, ctx = hgs.render(g, c, background=(0, 0, 0), mesh=mr.mesh_layer(m, c, fr))
+    assert ctx.tiles.k == int(d["k_entries"])
+    assert digest(np_(ctx.tiles.tile_starts).astype(np.int64)) == str(d["sha_tile_starts"])
+    assert digest(np_(ctx.tiles.entries).astype(np.int32)) == str(d["sha_entries"])
+    assert digest(np_(ctx.last_consumed).astype(np.int32)) == str(d["sha_last"])
+    pi = d["pix_idx"]
+    assert_close(np_(out.color).reshape(-1, 3)[pi], d["color_s"], atol=1e-5, what="color")
+    assert_close(np_(out.transmittance).reshape(-1)[pi], d["t_s"], atol=1e-5, what="T")
+    assert_close(np_(out.depth).reshape(-1)[pi], d["depth_s"], atol=1e-4, what="depth")
+    if "row_idx" in d:
+        from _util import grad_close
+        rng = np.random.default_rng(9)
+        gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
+        gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
+        gr = hgs.rasterize_backward(ctx, gc, gt)
+        ri = d["row_idx"]
+        for k in ("centers", "rotations", "log_scales", "logit_opacities", "colors_dc"):
+            grad_close(np_(getattr(gr, k))[ri], d["g_" + k], atol=1e-4, scale_tol=1e-4, what=k)

@@ -191,3 +191,52 @@ def test_oracle_threads_do_not_change_results():
     b = orc.rasterize_forward(p, t1, cam.width, cam.height, d["bg"], None, nthreads=4)
     for x, y in zip(a, b):
         assert np.array_equal(x, y, equal_nan=True)
+
+
+# ---- at scale: reference-written c2 (forward + backward) and c3 (forward)
+# fixtures (tests/golden/make_golden_scale.py): integer outputs as SHA-256
+# digests (bit-exact), floats at fixed sampled pixels / rows plus sums.
+
+def _digest(a):
+    import hashlib
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.dtype.str.encode() + str(a.shape).encode() + a.tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_oracle_matches_reference_at_scale(cfg):
+    import hashlib
+    from paper_2506_06988_b200 import synthetic as syn
+    d = load_golden(f"scale_{cfg}")
+    sc = syn.make_config(cfg, seed=0)
+    g, m = sc.gaussians, sc.mesh
+    h = hashlib.sha256()
+    for p in (g.centers, g.rotations, g.log_scales, g.logit_opacities, g.colors_dc, m.vertices, m.triangles, m.uvs,
+              m.texture):
+        h.update(np.ascontiguousarray(p, dtype=np.float64 if p.dtype.kind == "f" else np.int64).tobytes())
+    assert h.hexdigest() == str(d["input_sha"]), "synthetic generator no longer reproduces the fixture's inputs"
+    cam = sc.cameras[0]
+    fr = orc.rasterize_fragments(m.vertices, m.triangles, m.uvs, cam)
+    assert _digest(fr.triangle_id.astype(np.int32)) == str(d["sha_tri"]), "triangle ids differ"
+    mc = orc.sample_texture(m.texture, fr.uv, fr.valid)
+    color, depth, tt, octx = orc.render(g, cam, (0.0, 0.0, 0.0), orc.Mesh(mc, fr.depth, fr.triangle_id))
+    assert len(octx["tiles"].entries) == int(d["k_entries"])
+    assert _digest(octx["tiles"].tile_starts.astype(np.int64)) == str(d["sha_tile_starts"]), "tile_starts differ"
+    assert _digest(octx["tiles"].entries.astype(np.int32)) == str(d["sha_entries"]), "entry order differs"
+    assert _digest(octx["last"].astype(np.int32)) == str(d["sha_last"]), "last-consumed indices differ"
+    pi = d["pix_idx"]
+    assert_close(color.reshape(-1, 3)[pi], d["color_s"], atol=1e-12, what="color")
+    assert_close(tt.reshape(-1)[pi], d["t_s"], atol=1e-12, what="T")
+    assert_close(depth.reshape(-1)[pi], d["depth_s"], atol=1e-10, what="depth")
+    assert_close(color.sum(axis=(0, 1)), d["color_sum"], atol=1e-8, rtol=1e-12, what="colour sum")
+    assert int(np.isnan(depth).sum()) == int(d["depth_nan"])
+    if "row_idx" in d:
+        rng = np.random.default_rng(9)
+        gc = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width, 3)))
+        gt = syn.q32(rng.uniform(-1, 1, (cam.height, cam.width)))
+        og = orc.backward(octx, gc, gt)
+        ri = d["row_idx"]
+        for k in ("centers", "rotations", "log_scales", "logit_opacities", "colors_dc"):
+            a = np.asarray(getattr(og, k))
+            assert_close(a[ri], d["g_" + k], atol=1e-9, rtol=1e-9, what=k)
+            assert abs(np.abs(a).sum() - float(d["gsum_" + k])) <= 1e-9 * float(d["gsum_" + k]), k
