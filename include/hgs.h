@@ -65,6 +65,18 @@ typedef struct hgs_gaussians {
   int64_t n;
 } hgs_gaussians;
 
+/* Mutable parameter rows (same layout as hgs_gaussians): the outputs of
+   density control (parameters and the Adam moments that move with them). */
+typedef struct hgs_gaussian_buf {
+  float* centers;
+  float* rotations;
+  float* log_scales;
+  float* logits;
+  float* colors_dc;
+  float* colors_rest; /* NULL iff the input has no colors_rest */
+  int64_t n;
+} hgs_gaussian_buf;
+
 /* Mutable twin of hgs_gaussians for parameter gradients (same layout). */
 typedef struct hgs_gaussian_grads {
   float* centers;
@@ -276,6 +288,39 @@ int hgs_composite_loss(const float* i_gt, const float* i_h, const float* i_m, co
    grads are multiplied by grad_scale first (view-batch mean). */
 int hgs_adam_step(const hgs_adam_group* groups_host, int32_t n_groups, int64_t step, float beta1, float beta2,
                   float eps, float grad_scale, void* stream);
+
+/* ---------------- adaptive density control ---------------- */
+
+/* densify_and_prune (train/densify.py:46-94) + Adam.append_rows /
+   prune_rows (train/adam.py:44-60) as a device stream compaction.
+   hgs_densify_plan: per-row clone / split / prune decisions (fp64: average
+   screen-gradient norm > grad_threshold, max scale <= scale_limit (=
+   percent_dense * extent), sigmoid(logit) < prune_alpha) and prefix counts;
+   writes counts_host[7] = {cloned, split, pruned, n_after, kept originals,
+   kept clones, kept split rows} (synchronises the stream: n_after sizes the
+   caller's new buffers).  hgs_densify_apply: writes the new rows -- kept
+   originals, clones, then two children per split row (np.repeat order), each
+   group of the parameters and of both Adam moments (zeros for appended rows);
+   split children get centre + R(q) (n * exp(log_scales)) and log_scales -
+   log(1.6), n = split_normals rows 2s, 2s + 1 for the s-th split row (the
+   reference's rng.normal(0, 1, (2 n_split, 3)) draw); accum_out / denom_out
+   (n_after doubles each, may be NULL) are zeroed: the fresh DensifyState
+   (densify.py:92).  Replaces densify.py:46-94 / adam.py:44-60. */
+size_t hgs_densify_scratch_bytes(int64_t n);
+int hgs_densify_plan(const hgs_gaussians* gs, const double* grad_accum, const double* denom, double grad_threshold,
+                     double scale_limit, double prune_alpha, void* scratch, size_t scratch_bytes, int64_t* counts_host,
+                     void* stream);
+int hgs_densify_apply(const hgs_gaussians* gs, const hgs_gaussians* m, const hgs_gaussians* v,
+                      const double* split_normals, const void* scratch, hgs_gaussian_buf* out, hgs_gaussian_buf* out_m,
+                      hgs_gaussian_buf* out_v, double* accum_out, double* denom_out, void* stream);
+/* DensifyState.update (densify.py:31-33) for a batch of views: where
+   visible_count[i] > 0, grad_accum[i] += norm_sum[i] * norm_scale and
+   denom[i] += visible_count[i]. */
+int hgs_densify_accumulate(const float* visible_count, const float* norm_sum, double norm_scale, int64_t n,
+                           double* grad_accum, double* denom, void* stream);
+/* reset_opacity (densify.py:97-101): logit <- logit(min(sigmoid(logit),
+   ceiling)), its Adam moments (m, v may be NULL) cleared. */
+int hgs_reset_opacity(float* logits, float* m, float* v, int64_t n, double ceiling, void* stream);
 
 #ifdef __cplusplus
 }

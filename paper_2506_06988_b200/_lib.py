@@ -41,6 +41,11 @@ class HGSGaussians(ctypes.Structure):
                 ("colors_dc", c_void_p), ("colors_rest", c_void_p), ("n", c_i64)]
 
 
+class HGSGaussianBuf(ctypes.Structure):
+    _fields_ = [("centers", c_void_p), ("rotations", c_void_p), ("log_scales", c_void_p), ("logits", c_void_p),
+                ("colors_dc", c_void_p), ("colors_rest", c_void_p), ("n", c_i64)]
+
+
 class HGSGaussianGrads(ctypes.Structure):
     _fields_ = [("centers", c_void_p), ("rotations", c_void_p), ("log_scales", c_void_p), ("logits", c_void_p),
                 ("colors_dc", c_void_p), ("colors_rest", c_void_p), ("densify_norm", c_void_p),
@@ -113,6 +118,14 @@ SIGNATURES = {
                                           c_i32, c_f64, c_f64, c_i32, _P(c_f64), c_f64, c_void_p, c_void_p,
                                           c_void_p, c_void_p, c_void_p, ctypes.c_size_t, c_void_p]),
     "hgs_adam_step": (ctypes.c_int, [_P(HGSAdamGroup), c_i32, c_i64, c_f32, c_f32, c_f32, c_f32, c_void_p]),
+    "hgs_densify_scratch_bytes": (ctypes.c_size_t, [c_i64]),
+    "hgs_densify_plan": (ctypes.c_int, [_P(HGSGaussians), c_void_p, c_void_p, c_f64, c_f64, c_f64, c_void_p,
+                                        ctypes.c_size_t, _P(c_i64), c_void_p]),
+    "hgs_densify_apply": (ctypes.c_int, [_P(HGSGaussians), _P(HGSGaussians), _P(HGSGaussians), c_void_p, c_void_p,
+                                         _P(HGSGaussianBuf), _P(HGSGaussianBuf), _P(HGSGaussianBuf), c_void_p, c_void_p,
+                                         c_void_p]),
+    "hgs_densify_accumulate": (ctypes.c_int, [c_void_p, c_void_p, c_f64, c_i64, c_void_p, c_void_p, c_void_p]),
+    "hgs_reset_opacity": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_f64, c_void_p]),
 }
 
 

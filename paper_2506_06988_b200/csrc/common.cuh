@@ -110,6 +110,34 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Block-wide exclusive scan of one value per thread (blockDim == 256).
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* s_warp /*[8]*/, T& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < 8 ? s_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < 8) s_warp[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  T warp_excl = warp > 0 ? s_warp[warp - 1] : T(0);
+  total = s_warp[7];
+  __syncthreads();
+  return warp_excl + x - v;
+}
+
 }  // namespace hgs
 
 // Every kernel launch is followed by HGS_CHECK_LAUNCH(): it surfaces launch

@@ -2,49 +2,32 @@
 gsmesh/train/densify.py (DensifyState :20-43, densify_and_prune :46-94,
 reset_opacity :97-101) and the Adam row surgery it drives (adam.py:44-60).
 
-Runs every ``densify_interval`` iterations, not per frame: the row surgery
-is device gather / concatenate over the flat parameter and moment buffers
-(PyTorch as plumbing); the per-Gaussian decisions reproduce the
-reference's fp64 arithmetic.  The split samples come from the caller's
+Every step runs in libhgs.so (csrc/densify.cu): the per-Gaussian decisions
+reproduce the reference's fp64 arithmetic, the row surgery is a stream
+compaction writing the new flat parameter buffer and both Adam moments in
+one pass (hgs_densify_plan / hgs_densify_apply), the statistic update and the
+opacity reset are one kernel each.  The split samples come from the caller's
 numpy ``Generator`` exactly as the reference draws them
-(``rng.normal(0, 1, (2 n_split, 3))``), so a run seeded like the reference
-splits into the same positions, and every data-parallel rank (same seed,
-all-reduced statistics) performs the identical surgery.
+(``rng.normal(0, 1, (2 n_split, 3))``, uploaded once), so a run seeded like
+the reference splits into the same positions, and every data-parallel rank
+(same seed, all-reduced statistics) performs the identical surgery.
 """
 
 from __future__ import annotations
 
-import math
-from typing import Dict, Optional, Tuple
+import ctypes
+from typing import Dict, Tuple
 
 import numpy as np
 import torch
 
+from . import _lib
 from .adam import Adam
-from .scene import GaussianSet
+from .scene import GROUPS, GaussianSet
 
 
-def inverse_sigmoid(x: torch.Tensor) -> torch.Tensor:
-    """densify.py:15-16."""
-    return torch.log(x / (1.0 - x))
-
-
-def quaternions_to_rotations(q: torch.Tensor) -> torch.Tensor:
-    """scene.py:126-141 in fp64: (N, 4) (w, x, y, z), normalised -> (N, 3, 3)."""
-    q = q.double()
-    qn = q / torch.linalg.norm(q, dim=-1, keepdim=True)
-    w, x, y, z = qn.unbind(-1)
-    r = torch.empty(q.shape[:-1] + (3, 3), dtype=torch.float64, device=q.device)
-    r[..., 0, 0] = 1 - 2 * (y * y + z * z)
-    r[..., 0, 1] = 2 * (x * y - w * z)
-    r[..., 0, 2] = 2 * (x * z + w * y)
-    r[..., 1, 0] = 2 * (x * y + w * z)
-    r[..., 1, 1] = 1 - 2 * (x * x + z * z)
-    r[..., 1, 2] = 2 * (y * z - w * x)
-    r[..., 2, 0] = 2 * (x * z - w * y)
-    r[..., 2, 1] = 2 * (y * z + w * x)
-    r[..., 2, 2] = 1 - 2 * (x * x + y * y)
-    return r
+def _stream(dev) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
 
 
 class DensifyState:
@@ -61,12 +44,14 @@ class DensifyState:
     def zeros(n: int, device) -> "DensifyState":
         return DensifyState(n, device)
 
-    def update(self, visible_count: torch.Tensor, grad_norm_sum: torch.Tensor) -> None:
+    def update(self, visible_count: torch.Tensor, grad_norm_sum: torch.Tensor, scale: float = 1.0) -> None:
+        """Where a row was visible: grad_accum += scale * grad_norm_sum,
+        denom += visible_count (densify.py:31-33 for a batch of views)."""
         n = self.grad_accum.numel()
-        vis = visible_count[:n].double()
-        seen = vis > 0
-        self.grad_accum += torch.where(seen, grad_norm_sum[:n].double(), torch.zeros_like(vis))
-        self.denom += vis
+        vc = visible_count[:n].float().contiguous()
+        ns = grad_norm_sum[:n].float().contiguous()
+        _lib.call("hgs_densify_accumulate", _lib.ptr(vc), _lib.ptr(ns), float(scale), n, _lib.ptr(self.grad_accum),
+                  _lib.ptr(self.denom), _stream(self.grad_accum.device))
 
     def average(self) -> torch.Tensor:
         seen = self.denom > 0
@@ -79,22 +64,22 @@ class DensifyState:
         self.denom = torch.zeros(n, dtype=torch.float64, device=dev)
 
 
-def _rows(gs: GaussianSet) -> Dict[str, torch.Tensor]:
-    return {k: gs.group(k) for k in gs.layout}
-
-
-def rebuild(gs: GaussianSet, rows: Dict[str, torch.Tensor]) -> GaussianSet:
-    """A GaussianSet (same device, same groups) holding ``rows``."""
-    return GaussianSet(rows["centers"], rows["rotations"], rows["log_scales"], rows["logit_opacities"],
-                       rows["colors_dc"], rows.get("colors_rest"), device=gs.device)
+def _moments(opt: Adam, which: Dict[str, torch.Tensor], gs: GaussianSet) -> _lib.HGSGaussians:
+    s = _lib.HGSGaussians()
+    s.centers, s.rotations = _lib.ptr(which["centers"]), _lib.ptr(which["rotations"])
+    s.log_scales, s.logits = _lib.ptr(which["log_scales"]), _lib.ptr(which["logit_opacities"])
+    s.colors_dc = _lib.ptr(which["colors_dc"])
+    s.colors_rest = _lib.ptr(which["colors_rest"]) if gs.sh_degree else None
+    s.n = len(gs)
+    return s
 
 
 def rebind(opt: Adam, gs: GaussianSet, m: Dict[str, torch.Tensor], v: Dict[str, torch.Tensor]) -> None:
     """Point the optimiser at the groups of ``gs`` (new row count) with
     moments ``m``, ``v`` (same shapes), keeping its step count and lrs."""
     opt.params = {k: gs.group(k) for k in opt.params}
-    opt.m = {k: m[k].contiguous() for k in opt.params}
-    opt.v = {k: v[k].contiguous() for k in opt.params}
+    opt.m = {k: m[k] for k in opt.params}
+    opt.v = {k: v[k] for k in opt.params}
 
 
 def densify_and_prune(gs: GaussianSet, opt: Adam, state: DensifyState, extent: float, config,
@@ -103,66 +88,39 @@ def densify_and_prune(gs: GaussianSet, opt: Adam, state: DensifyState, extent: f
     Gaussians, split large hot ones (2 samples each), then drop the split
     originals and every Gaussian whose opacity is below the prune threshold.
     Returns the new GaussianSet (the optimiser is rebound to it)."""
+    groups = [g for g in GROUPS if g in gs.layout]
+    if set(opt.params) != set(groups):
+        raise ValueError(f"optimiser groups {sorted(opt.params)} != Gaussian groups {groups}")
     dev = gs.device
     n0 = len(gs)
-    avg = state.average()
-    scales = torch.exp(gs.log_scales.double()).max(dim=1).values
-    hot = avg > config.densify_grad_threshold
-    small = scales <= config.percent_dense * extent
-    clone_mask = hot & small
-    split_mask = hot & ~small
-    n_clone, n_split = int(clone_mask.sum()), int(split_mask.sum())
-    stats = {"cloned": n_clone, "split": n_split}
-
-    rows = _rows(gs)
-    names = list(rows)
-    new_p = {k: [rows[k]] for k in names}
-    new_m = {k: [opt.m[k]] if k in opt.m else [] for k in names}
-    new_v = {k: [opt.v[k]] if k in opt.v else [] for k in names}
-
-    def append(block: Dict[str, torch.Tensor]):
-        for k in names:
-            new_p[k].append(block[k])
-            if k in opt.m:
-                new_m[k].append(torch.zeros_like(block[k]))
-                new_v[k].append(torch.zeros_like(block[k]))
-
-    if n_clone:
-        append({k: rows[k][clone_mask].clone() for k in names})
-    if n_split:
-        reps = 2
-        stds = torch.repeat_interleave(torch.exp(rows["log_scales"][split_mask].double()), reps, dim=0)
-        samples = torch.as_tensor(rng.normal(0.0, 1.0, tuple(stds.shape)), dtype=torch.float64, device=dev) * stds
-        rots = torch.repeat_interleave(quaternions_to_rotations(rows["rotations"][split_mask]), reps, dim=0)
-        block = {k: torch.repeat_interleave(rows[k][split_mask], reps, dim=0) for k in names}
-        block["centers"] = (torch.einsum("nij,nj->ni", rots, samples) + block["centers"].double()).float()
-        block["log_scales"] = (block["log_scales"].double() - math.log(1.6)).float()
-        append(block)
-
-    cat_p = {k: torch.cat(new_p[k]) for k in names}
-    n_now = len(cat_p["centers"])
-    keep = torch.ones(n_now, dtype=torch.bool, device=dev)
-    keep[:n0][split_mask] = False
-    alpha = torch.sigmoid(cat_p["logit_opacities"].double())
-    low = alpha < config.opacity_prune_threshold
-    stats["pruned"] = int((low & keep).sum())
-    keep &= ~low
-    out_p = {k: cat_p[k][keep] for k in names}
-    out_m = {k: torch.cat(new_m[k])[keep] for k in names if k in opt.m}
-    out_v = {k: torch.cat(new_v[k])[keep] for k in names if k in opt.v}
-    new_gs = rebuild(gs, out_p)
-    rebind(opt, new_gs, out_m, out_v)
-    state.reset(len(new_gs))
-    stats["n_after"] = len(new_gs)
+    nbytes = _lib.load().hgs_densify_scratch_bytes(n0)
+    scratch = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+    counts = (ctypes.c_int64 * 7)()
+    _lib.call("hgs_densify_plan", ctypes.byref(gs.struct()), _lib.ptr(state.grad_accum), _lib.ptr(state.denom),
+              float(config.densify_grad_threshold), float(config.percent_dense * extent),
+              float(config.opacity_prune_threshold), _lib.ptr(scratch), scratch.numel(), counts, _stream(dev))
+    n_clone, n_split, n_pruned, n_after = (int(counts[i]) for i in range(4))
+    normals = None
+    if n_split:  # the reference draws only when some row splits (densify.py:64-66)
+        normals = torch.as_tensor(rng.normal(0.0, 1.0, (2 * n_split, 3)), dtype=torch.float64).to(dev)
+    new_gs = GaussianSet.allocate(n_after, gs.sh_degree, dev)
+    new_m = GaussianSet.allocate(n_after, gs.sh_degree, dev)
+    new_v = GaussianSet.allocate(n_after, gs.sh_degree, dev)
+    state.grad_accum = torch.empty(n_after, dtype=torch.float64, device=dev)  # zeroed by the kernel (state.reset)
+    state.denom = torch.empty(n_after, dtype=torch.float64, device=dev)
+    _lib.call("hgs_densify_apply", ctypes.byref(gs.struct()), ctypes.byref(_moments(opt, opt.m, gs)),
+              ctypes.byref(_moments(opt, opt.v, gs)), _lib.ptr(normals), _lib.ptr(scratch),
+              ctypes.byref(new_gs.buf()), ctypes.byref(new_m.buf()), ctypes.byref(new_v.buf()),
+              _lib.ptr(state.grad_accum), _lib.ptr(state.denom), _stream(dev))
+    rebind(opt, new_gs, {k: new_m.group(k) for k in groups}, {k: new_v.group(k) for k in groups})
+    stats = {"cloned": n_clone, "split": n_split, "pruned": n_pruned, "n_after": n_after}
     return new_gs, stats
 
 
-def reset_opacity(gs: GaussianSet, opt: Optional[Adam] = None, ceiling: float = 0.01) -> None:
+def reset_opacity(gs: GaussianSet, opt: Adam = None, ceiling: float = 0.01) -> None:
     """densify.py:97-101: activated opacities clamped to <= ceiling (in
     place), their Adam moments cleared."""
-    lg = gs.logit_opacities
-    alpha = torch.sigmoid(lg.double())
-    lg.copy_(inverse_sigmoid(torch.clamp(alpha, max=ceiling)).float())
-    if opt is not None and "logit_opacities" in opt.m:
-        opt.m["logit_opacities"].zero_()
-        opt.v["logit_opacities"].zero_()
+    m = opt.m.get("logit_opacities") if opt is not None else None
+    v = opt.v.get("logit_opacities") if opt is not None else None
+    _lib.call("hgs_reset_opacity", _lib.ptr(gs.logit_opacities), _lib.ptr(m), _lib.ptr(v), len(gs), float(ceiling),
+              _stream(gs.device))

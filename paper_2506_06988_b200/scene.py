@@ -159,6 +159,24 @@ class GaussianSet:
         return s
 
     @staticmethod
+    def allocate(n: int, sh_degree: int, device) -> "GaussianSet":
+        """Uninitialised rows (filled by a device kernel, e.g. density control)."""
+        out = GaussianSet.__new__(GaussianSet)
+        out.n, out.sh_degree = int(n), int(sh_degree)
+        out.layout, total = group_layout(out.n, out.sh_degree)
+        out.params = torch.empty(max(total, 64), dtype=torch.float32, device=device)
+        return out
+
+    def buf(self) -> _lib.HGSGaussianBuf:
+        s = _lib.HGSGaussianBuf()
+        s.centers, s.rotations = _lib.ptr(self.centers), _lib.ptr(self.rotations)
+        s.log_scales, s.logits = _lib.ptr(self.log_scales), _lib.ptr(self.logit_opacities)
+        s.colors_dc = _lib.ptr(self.colors_dc)
+        s.colors_rest = _lib.ptr(self.colors_rest) if self.sh_degree else None
+        s.n = self.n
+        return s
+
+    @staticmethod
     def empty(sh_degree: int = 0, device=None) -> "GaussianSet":
         rest = np.zeros((0, 3, 3)) if sh_degree >= 1 else None
         return GaussianSet(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros((0,)), np.zeros((0, 3)),

@@ -12,7 +12,8 @@ the batch and a single all_reduce(SUM) over one flat fp32 bucket
 (Gaussian grads | texture grad | densify norms) precedes the identical Adam
 update on every rank, so replicas stay bit-identical.
 
-Density control (densify.py) is out of scope for this path.
+Adaptive density control (densify.py) is opt-in
+(density_control=True): every densify_interval iterations, on the device.
 """
 
 from __future__ import annotations
@@ -165,7 +166,7 @@ class HybridTrainer:
         # the views' losses were scaled by 1/nb (batch mean), and the norm
         # is linear in that scale: x nb restores the sum of the per-view
         # norms the reference accumulates one view at a time (densify.py:31-33)
-        self.dstate.update(self.grads.visible_count, self.grads.densify_norm * nb)
+        self.dstate.update(self.grads.visible_count, self.grads.densify_norm, scale=float(nb))
         if it >= cfg.densify_from_iter and it % cfg.densify_interval == 0:
             self.gs, stats = densify_and_prune(self.gs, self.opt, self.dstate, self.extent, cfg, self.rng)
             stats["iter"] = it
