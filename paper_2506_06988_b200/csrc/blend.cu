@@ -551,6 +551,384 @@ __global__ void __launch_bounds__(FAST_THREADS, PREC ? HGS_FAST_MINB_PREC : HGS_
               mask_variant, mask_k, PREC ? T64 : (double)T);
 }
 
+// ---------------------------------------------------------------------------
+// blend_tile_kernel: the production fast path (the kernel above is kept as
+// the A/B baseline, HGS_BLEND_V1).  Same numerics contract, re-shaped to
+// spend fewer instructions per (pixel, entry):
+//  * 4 consumer warps own 8x8 sub-tiles, TWO pixels per lane ((x, y) and
+//    (x, y + 4)): every per-entry cost -- shared-memory loads of the record,
+//    the list walk, the warp vote, dx = fx - mean x and conic_xx * dx (the
+//    two pixels share the column) -- is paid once for two pixels, and the two
+//    pixels' independent recurrences give the ILP the old kernel got from
+//    evaluating two entries per step;
+//  * the support and skip decisions are one compare against the entry's cut
+//    ucut = min(9 U, log2(255 alpha)) (entry_ucut, stage.cuh), computed once
+//    per (warp, entry) by the cull and kept next to the list index;
+//  * the producer moves each record with two bulk copies (TMA engine,
+//    cp.async.bulk, 64 B fp64 record head + 48 B fp32 cull record) whose
+//    bytes complete the stage's mbarrier, instead of seven 16-B cp.async.
+// Decisions stay the reference's: guard band around the cut (exact fp64
+// re-evaluation inside it), exact fp64 depth stop, fp32 T with the carried
+// error bound eT and the exact replay of pixels whose early stop is
+// ambiguous.
+#ifndef HGS_TB_BATCH
+#define HGS_TB_BATCH 64
+#endif
+#ifndef HGS_TB_NSTAGE
+#define HGS_TB_NSTAGE 2
+#endif
+#ifndef HGS_TB_MINB
+#define HGS_TB_MINB 5
+#endif
+#ifndef HGS_TB_MINB_PREC
+#define HGS_TB_MINB_PREC 4
+#endif
+#ifndef HGS_TB_BULK
+#define HGS_TB_BULK 0
+#endif
+constexpr int TB_BATCH = HGS_TB_BATCH;
+constexpr int TB_NSTAGE = HGS_TB_NSTAGE;
+constexpr int TB_CONSUMERS = 4;
+constexpr int TB_THREADS = (TB_CONSUMERS + 1) * 32;
+constexpr unsigned TB_REC_BYTES = 64, TB_CULL_BYTES = 48;
+
+// A culled entry, copied by the cull into the warp's own walk buffer (the
+// walk then reads consecutive records -- no index -> record load chain --
+// and the ring slot is released as soon as every warp has culled it).
+struct __align__(16) WalkRec {
+  double2 a;  // mean x, y
+  double2 b;  // U conic xx, U 2xy (U = log2(e)/2: the conic form is the exp2 argument)
+  double2 c;  // U conic yy, depth
+  double alpha;
+  float ucut;  // the entry's cut (entry_ucut)
+  int k;       // entry index relative to the tile start
+  float4 col;  // r, g, b, depth (fp32)
+};
+static_assert(sizeof(WalkRec) == 80, "walk record is 80 B");
+
+struct TileSmem {
+  StageEntry ent[TB_NSTAGE][TB_BATCH];
+  WalkRec walk[TB_CONSUMERS][TB_BATCH];
+  unsigned long long full[TB_NSTAGE];
+  unsigned long long empty[TB_NSTAGE];
+  double exp2tab[16];
+  int done_warps;
+  int end_batch;
+  unsigned long long stats[2];
+};
+
+struct TbPix {
+  float T, eT, acc, r, g, b, dacc;
+  int last;
+  int lim_hi;  // high word of the mesh depth limit (positive fp64: the word order is the value order)
+  bool done, flagged;
+  double T64;
+};
+
+// The general (sequential, exact where needed) treatment of one entry for
+// one pixel: depth stop, exact re-evaluation inside the cut band, the
+// early-stop region with the error bound.  k: entry index relative to the
+// tile start.
+// exact re-evaluation from the Gaussian's fp64 record in global memory (the
+// walk record holds the scaled conic)
+__device__ __noinline__ double exact_global(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
+                                            int64_t k, double fx, double fy) {
+  const BlendRec& R = rec[entries[k]];
+  const double dx = fx - R.mx, dy = fy - R.my;
+  const double m = R.ca * dx * dx + R.cb2 * dx * dy + R.cc * dy * dy;
+  if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0;
+  double sg = R.alpha * exp(-0.5 * m);
+  if (sg > ALPHA_CLAMP) sg = ALPHA_CLAMP;
+  return sg < SIGMA_SKIP ? -1.0 : sg;
+}
+
+template <bool STATS, bool PREC>
+__device__ __forceinline__ void tb_slow(TbPix& q, const WalkRec& E, double fx, double fy, const double* limit,
+                                        float uu, double um, float sg, float d, int k, const double* tab,
+                                        const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
+                                        int64_t s, unsigned& walked, unsigned& blended) {
+  if (q.done) return;
+  if (STATS) walked++;
+  // list is depth sorted; mesh is opaque.  Equal high words: the full fp64
+  // compare (limit NULL: no mesh here, +inf)
+  if (__double2hiint(E.c.y) >= q.lim_hi && limit && E.c.y >= *limit) {
+    q.done = true;
+    return;
+  }
+  bool ok = d < -U_BAND;
+  double sx = -1.0;
+  if (!(fabsf(d) > U_BAND)) {  // within the cut band (or a NaN cut): decide exactly
+    sx = exact_global(rec, entries, s + k, fx, fy);
+    ok = sx >= 0.0;
+    sg = (float)sx;
+  }
+  if (!ok) {
+    q.eT = fmaf(q.T, 1.1920929e-7f, q.eT);
+    return;
+  }
+  const float om = 1.0f - sg;
+  const float test = q.T * om;
+  const float w = q.T * sg;
+  q.eT = fmaf(w, EPS_SIG, fmaf(q.eT, om, test * 1.1920929e-7f));
+  if (fmaf(-2.0f, q.eT, test) < STOP_NEAR) {  // the early-stop region
+    if (fabsf(test - STOP_F) <= fmaf(q.eT, 1.001f, 3e-12f)) q.flagged = true;
+    if (test < STOP_F) {
+      q.done = true;
+      return;
+    }
+  }
+  q.r = fmaf(E.col.x, w, q.r);
+  q.g = fmaf(E.col.y, w, q.g);
+  q.b = fmaf(E.col.z, w, q.b);
+  q.dacc = fmaf(E.col.w, w, q.dacc);
+  q.acc += w;
+  q.T = test;
+  q.last = k;
+  if (STATS) blended++;
+  if (PREC) q.T64 *= 1.0 - (sx >= 0.0 ? sx : fmin(E.alpha * exp2_neg64(um, uu, tab), ALPHA_CLAMP));
+}
+
+template <bool STATS, bool PREC>
+__global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_MINB) blend_tile_kernel(
+    const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
+    const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
+    double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
+    const int64_t* __restrict__ counters) {
+  pdl_enter();
+  if (counters && counters[2]) return;  // entry buffer overflowed: bins are invalid, the caller re-renders
+  extern __shared__ __align__(128) unsigned char tile_smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(tile_smem_raw);
+  const int tile = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
+  const int nbatches = (int)((e - s + TB_BATCH - 1) / TB_BATCH);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TB_NSTAGE; i++) {
+      mbar_init(&sm.full[i], 32);
+      mbar_init(&sm.empty[i], TB_CONSUMERS);
+    }
+    sm.done_warps = 0;
+    sm.end_batch = 0x7fffffff;
+    sm.stats[0] = sm.stats[1] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (PREC) exp2_tab_load(sm.exp2tab);
+  __syncthreads();
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+
+  if (warp == TB_CONSUMERS) {
+    // ------------------------------------------------------------ producer
+    for (int b = 0; b < nbatches; b++) {
+      const int slot = b % TB_NSTAGE;
+      if (b >= TB_NSTAGE) warp_wait(&sm.empty[slot], ((b / TB_NSTAGE) - 1) & 1, lane);
+      if (*(volatile int*)&sm.done_warps == TB_CONSUMERS) {
+        if (lane == 0) *(volatile int*)&sm.end_batch = b;
+        __syncwarp();
+        mbar_arrive(&sm.full[slot]);  // 32 plain arrivals complete the phase
+        break;
+      }
+      const int64_t base = s + (int64_t)b * TB_BATCH;
+      const int nb = (int)min((int64_t)TB_BATCH, e - base);
+      const int mine = nb > lane ? (nb - lane + 31) >> 5 : 0;
+      uint32_t g[TB_BATCH / 32];
+#pragma unroll
+      for (int u = 0; u < TB_BATCH / 32; u++)
+        if (u < mine) g[u] = __ldg(entries + base + lane + 32 * u);
+#if HGS_TB_BULK
+      // A/B: bulk copies take their operands in uniform registers, so the
+      // compiler issues them one lane at a time (an elect loop of ~9
+      // instructions per copy): 3x the producer's issue slots of the
+      // cp.async version below and consumers starved (r02 profile)
+      mbar_arrive_expect_tx(&sm.full[slot], (unsigned)mine * (TB_REC_BYTES + TB_CULL_BYTES));
+#pragma unroll
+      for (int u = 0; u < TB_BATCH / 32; u++)
+        if (u < mine) {
+          StageEntry* dst = &sm.ent[slot][lane + 32 * u];
+          bulk_g2s(&dst->a, rec + g[u], TB_REC_BYTES, &sm.full[slot]);
+          bulk_g2s(&dst->f, cull + g[u], TB_CULL_BYTES, &sm.full[slot]);
+        }
+#else
+#pragma unroll
+      for (int u = 0; u < TB_BATCH / 32; u++)
+        if (u < mine) {
+          StageEntry* dst = &sm.ent[slot][lane + 32 * u];
+          const char* src = reinterpret_cast<const char*>(rec + g[u]);
+          const char* cs = reinterpret_cast<const char*>(cull + g[u]);
+          cp_async16(&dst->a, src);
+          cp_async16(&dst->b, src + 16);
+          cp_async16(&dst->c, src + 32);
+          cp_async16(&dst->d, src + 48);
+          cp_async16(&dst->f.box, cs);
+          cp_async16(&dst->f.con, cs + 16);
+          cp_async16(&dst->f.col, cs + 32);
+        }
+      cp_async_arrive_noinc(&sm.full[slot]);
+#endif
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  // warp w owns the 8x8 sub-tile (w & 1, w >> 1); lane (x, y) = (lane & 7,
+  // lane >> 3) holds pixels (x, y) and (x, y + 4)
+  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
+  const int px = tx * BLEND_TILE + sx0 + (lane & 7);
+  const int py0 = ty * BLEND_TILE + sy0 + (lane >> 3);
+  const double fx = px + 0.5, fy0 = py0 + 0.5;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const float wx0 = tx * BLEND_TILE + sx0 + 0.5f, wx1 = wx0 + 7.0f;
+  const float wy0 = ty * BLEND_TILE + sy0 + 0.5f, wy1 = wy0 + 7.0f;
+  TbPix q[2];
+  bool inside[2];
+  int64_t pix[2];
+  bool mesh_here[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int py = py0 + 4 * h;
+    inside[h] = px < width && py < height;
+    pix[h] = (int64_t)py * width + px;
+    mesh_here[h] = mesh.color != nullptr && inside[h] && mesh.triangle_id[pix[h]] >= 0;
+    q[h].lim_hi = __double2hiint(mesh_here[h] ? mesh.depth[pix[h]] : inf);
+    q[h].T = 1.0f;
+    q[h].eT = q[h].acc = q[h].r = q[h].g = q[h].b = q[h].dacc = 0.0f;
+    q[h].last = -1;
+    q[h].done = !inside[h];
+    q[h].flagged = false;
+    q[h].T64 = 1.0;
+  }
+  bool warp_done = false;
+  unsigned walked = 0, blended = 0;
+
+  for (int b = 0; b < nbatches; b++) {
+    const int slot = b % TB_NSTAGE;
+    warp_wait(&sm.full[slot], (b / TB_NSTAGE) & 1, lane);
+    if (b >= *(volatile int*)&sm.end_batch) break;
+    if (warp_done) {
+      if (lane == 0) mbar_arrive(&sm.empty[slot]);
+      continue;
+    }
+    const int nb = (int)min((int64_t)TB_BATCH, e - (s + (int64_t)b * TB_BATCH));
+    const int bb = b * TB_BATCH;
+    // order-preserving compaction of the stage to the entries whose effective
+    // ellipse touches the sub-tile, copied with their cut into the warp's
+    // walk buffer; then the ring slot is released
+    int nl = 0;
+#pragma unroll
+    for (int k = 0; k < TB_BATCH; k += 32) {
+      const int i = k + lane;
+      float4 bx = make_float4(0.f, 0.f, -1.f, -1.f);
+      if (i < nb) bx = sm.ent[slot][i].f.box;
+      const float cx = fminf(fmaxf(bx.x, wx0), wx1), cy = fminf(fmaxf(bx.y, wy0), wy1);
+      bool hit = fabsf(bx.x - cx) <= bx.z && fabsf(bx.y - cy) <= bx.w;
+      if (hit && (bx.x != cx || bx.y != cy)) hit = ellipse_meets_box(sm.ent[slot][i].f.con, bx, wx0, wx1, wy0, wy1);
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const StageEntry& S = sm.ent[slot][i];
+        WalkRec& W = sm.walk[warp][nl + __popc(m & lanemask_lt())];
+        W.a = S.a;
+        W.b = make_double2(S.b.x * U_SCALE, S.b.y * U_SCALE);
+        W.c = make_double2(S.c.x * U_SCALE, S.c.y);
+        W.alpha = S.d.x;
+        W.ucut = entry_ucut(S.f.col.x);
+        W.k = bb + i;
+        W.col = make_float4(S.f.col.y, S.f.col.z, S.f.col.w, S.f.con.w);
+      }
+      nl += __popc(m);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    for (int li = 0; li < nl; li++) {
+      const WalkRec& E = sm.walk[warp][li];
+      const double2 A = E.a, B = E.b, C = E.c;
+      const float ucut = E.ucut;
+      const float aabs = fabsf((float)E.alpha);
+      const double dx = fx - A.x;
+      const double adx = B.x * dx;
+      const int zhi = __double2hiint(C.y);
+      float uu[2], sg[2], dd[2], sv[2], Tn[2], eTn[2], w[2];
+      double um[2];
+      bool spec[2];
+      double dy = fy0 - A.y;
+      float thr[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) thr[h] = fmaf(2.0f, fmaf(q[h].T, EPS_SIG + 1.1920929e-7f, q[h].eT), STOP_NEAR);
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        if (h) dy = dy + 4.0;  // (x, y + 4): within the guard band of the direct difference
+        um[h] = fma(dx, fma(B.y, dy, adx), (C.x * dy) * dy);
+        uu[h] = __double2float_rn(um[h]);
+        sg[h] = fminf(aabs * ex2_neg(uu[h]), CLAMP_F);
+        dd[h] = uu[h] - ucut;
+        const bool ok = dd[h] < -U_BAND && !q[h].done;
+        sv[h] = ok ? sg[h] : 0.0f;
+        const float om = 1.0f - sv[h];
+        Tn[h] = q[h].T * om;
+        w[h] = q[h].T * sv[h];
+        eTn[h] = fmaf(w[h], EPS_SIG, fmaf(q[h].eT, om, Tn[h] * 1.1920929e-7f));
+        // a decision this entry could get wrong: depth stop, the cut band
+        // (or a NaN cut), the early-stop region.  The last is tested as
+        // Tn < STOP_NEAR + 2 (eT + T (EPS_SIG + 2^-23)) >= STOP_NEAR + 2 eTn
+        // (om <= 1, w <= T): the threshold comes from the state before the
+        // entry, off the entry's dependency chain.
+        spec[h] = !q[h].done && (zhi >= q[h].lim_hi || !(fabsf(dd[h]) > U_BAND) || Tn[h] < thr[h]);
+      }
+      if (!__any_sync(0xffffffffu, spec[0] || spec[1])) {
+        const float4 col = E.col;
+        const int k = E.k;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          if (STATS && !q[h].done) {
+            walked++;
+            blended += sv[h] > 0.0f;
+          }
+          q[h].T = Tn[h];
+          q[h].eT = eTn[h];
+          q[h].r = fmaf(col.x, w[h], q[h].r);
+          q[h].g = fmaf(col.y, w[h], q[h].g);
+          q[h].b = fmaf(col.z, w[h], q[h].b);
+          q[h].dacc = fmaf(col.w, w[h], q[h].dacc);
+          q[h].acc += w[h];
+          q[h].last = sv[h] > 0.0f ? k : q[h].last;
+          if (PREC && sv[h] > 0.0f)
+            q[h].T64 *= 1.0 - fmin(E.alpha * exp2_neg64(um[h], uu[h], sm.exp2tab), ALPHA_CLAMP);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+          tb_slow<STATS, PREC>(q[h], E, fx, fy0 + 4.0 * h, mesh_here[h] ? mesh.depth + pix[h] : nullptr, uu[h],
+                               um[h], sg[h], dd[h], E.k, sm.exp2tab, rec, entries, s, walked, blended);
+        if (__all_sync(0xffffffffu, q[0].done && q[1].done)) break;
+      }
+    }
+    if (__all_sync(0xffffffffu, q[0].done && q[1].done)) {
+      warp_done = true;
+      if (lane == 0) atomicAdd(&sm.done_warps, 1);
+    }
+  }
+  if (STATS) {
+    atomicAdd(&sm.stats[0], (unsigned long long)walked);
+    atomicAdd(&sm.stats[1], (unsigned long long)blended);
+    // consumers only: the producer may already have left
+    asm volatile("bar.sync 1, %0;" ::"n"(TB_CONSUMERS * 32));
+    if (threadIdx.x == 0) {
+      atomicAdd((unsigned long long*)&out.stats[0], sm.stats[0]);
+      atomicAdd((unsigned long long*)&out.stats[1], sm.stats[1]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    if (!inside[h]) continue;
+    if (q[h].flagged) {  // hand the pixel to the exact walk (work list: count, pixel ids)
+      const int slot = atomicAdd(&fixup[0], 1);
+      fixup[1 + slot] = (int32_t)pix[h];
+      continue;
+    }
+    write_pixel(out, mesh, mesh_here[h], pix[h], q[h].T, q[h].r, q[h].g, q[h].b, q[h].dacc, q[h].acc,
+                q[h].last >= 0 ? s + q[h].last : -1, bg0, bg1, bg2, mask_variant, mask_k,
+                PREC ? q[h].T64 : (double)q[h].T);
+  }
+}
+
 // The exact walk, one warp per pixel (persistent grid-stride): over the
 // fast kernel's work list of flagged pixels (fixup: count, pixel ids), or
 // over every pixel (fixup == NULL: projections without fp32 cull records).
@@ -603,6 +981,9 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
 #ifndef HGS_FWD_EXACT
 #define HGS_FWD_EXACT 0
 #endif
+#ifndef HGS_BLEND_V1
+#define HGS_BLEND_V1 0
+#endif
   if (out->fixup && proj->cull && !HGS_FWD_EXACT) {
     zero_pdl(st, out->fixup, sizeof(int32_t));
     HGS_CHECK_LAUNCH();
@@ -617,11 +998,30 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
       attr = true;
     }
     const bool prec = out->final_t != nullptr;
+#if HGS_BLEND_V1
     auto fn = out->stats ? (prec ? blend_fast_kernel<true, true> : blend_fast_kernel<true, false>)
                          : (prec ? blend_fast_kernel<false, true> : blend_fast_kernel<false, false>);
     launch_pdl(fn, dim3(n_tiles), dim3(FAST_THREADS), smem, st, (const BlendRec*)proj->rec,
                (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x, width, height, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
+#else
+    (void)smem;
+    const size_t tsmem = sizeof(TileSmem);
+    static bool tattr = false;
+    if (!tattr) {
+      for (auto fn : {blend_tile_kernel<false, false>, blend_tile_kernel<true, false>, blend_tile_kernel<false, true>,
+                      blend_tile_kernel<true, true>}) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      }
+      tattr = true;
+    }
+    auto fn = out->stats ? (prec ? blend_tile_kernel<true, true> : blend_tile_kernel<true, false>)
+                         : (prec ? blend_tile_kernel<false, true> : blend_tile_kernel<false, false>);
+    launch_pdl(fn, dim3(n_tiles), dim3(TB_THREADS), tsmem, st, (const BlendRec*)proj->rec,
+               (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x, width, height, ml,
+               bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
+#endif
     HGS_CHECK_LAUNCH();
     // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)
     launch_pdl(blend_exact_kernel, dim3(2 * NUM_SMS), dim3(256), 0, st, (const BlendRec*)proj->rec, tiles->entries,

@@ -59,6 +59,18 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Bulk (TMA engine) copy global -> shared of `bytes` (multiple of 16, both
+// addresses 16-B aligned); completion is signalled as transaction bytes on
+// the mbarrier, which the issuing thread announced with arrive_expect_tx.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 // Conservative test: does the ellipse {m <= mcut} reach any point of the
 // box [x0,x1] x [y0,y1] (centre outside the box)?  mcut is recovered from
 // the box half-width ex of the cull record (ex^2 = mcut cov_xx, cov_xx =
@@ -112,6 +124,22 @@ __device__ __forceinline__ float amb_key(float uu, float sgf, float a32) {
   const float k1 = fabsf(fmaf(uu, U9_BAND_INV, -U9 * U9_BAND_INV));
   const float k2 = fabsf(fmaf(sgf, SKIP_BAND_INV, -SKIP_F * SKIP_BAND_INV));
   return fminf(fminf(k1, k2), a32 * 1e4f);
+}
+// Cut form of the two blend decisions (support m <= 9 and skip
+// sigma >= 1/255, the clamp at 0.99 > 1/255 never decides): an entry is
+// blended iff u <= ucut = min(9 U, log2(255 alpha)) -- one compare per pixel.
+// ucut is computed once per (warp, entry) from the fp32 alpha with
+// lg2.approx (|err| <= 2^-22 relative of |log2| <= 8, plus alpha narrowing
+// and the product: < 2.3e-6), u is the fp32-rounded fp64 argument
+// (<= 6.5 * 2^-24), U9 its fp32 rounding: within U_BAND of the cut the entry
+// is re-evaluated exactly.  An ill-conditioned conic (alpha < 0) gets a NaN
+// cut: never "sure", always ambiguous.
+constexpr float U_BAND = 8e-6f;
+__device__ __forceinline__ float entry_ucut(float a32) {
+  if (a32 < 0.0f) return __int_as_float(0x7fc00000);
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(255.0f * a32));
+  return fminf(U9, l);
 }
 __device__ __forceinline__ float ex2_neg(float u) {
   float e;
