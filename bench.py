@@ -367,9 +367,10 @@ def run_ours(args):
     eval_peak = min(pk["fp32"] / FP32_OPS_PER_EVAL, pk["ex2"])
     # secondary: the algorithmic HBM floor of one blend launch (§8(d) K4, our
     # record sizes): the K entry indices once (4 B), each visible Gaussian's
-    # 80 B record + 32 B cull record once (the gathers are L2-resident), per
-    # pixel mesh colour 12 + depth 8 + id 4 B in, colour 12 + depth 4 + T 4 out
-    blend_bytes = k_entries * 4 + m_vis * (80 + 32) + npix * (12 + 8 + 4 + 12 + 4 + 4)
+    # staged 64 B fp64 record head + 48 B cull record once (the gathers are
+    # L2-resident), per pixel mesh colour 12 + depth 8 + id 4 B in, colour 12
+    # + depth 4 + T 4 out
+    blend_bytes = k_entries * 4 + m_vis * (64 + 48) + npix * (12 + 8 + 4 + 12 + 4 + 4)
     peak, peak_kind = measured_peaks()
     achieved = blend_bytes / (blend_ms * 1e-3) / 1e9
     prof = {}
@@ -408,7 +409,7 @@ def run_ours(args):
                                    "numpy; render() keeps the backward state (fp64 final T)"},
             "gpu_launches": int(launches_per_frame * args.steps * 2),
             "clocks": clk,
-            "roofline": {"kernel": "blend_fast_kernel (K4)", "bound": "fp32_issue", "achieved": eval_rate,
+            "roofline": {"kernel": "blend_tile_kernel (K4)", "bound": "fp32_issue", "achieved": eval_rate,
                          "peak": eval_peak, "unit": "evaluations/s", "frac": eval_rate / eval_peak,
                          "traffic": prof.get("dram_bytes"), "kernel_ms": blend_ms,
                          "evaluations_per_launch": walked,
