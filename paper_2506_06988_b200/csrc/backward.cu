@@ -17,9 +17,11 @@
 // atomic per component per warp.
 //
 // Numerics: the per-entry decisions (support m <= 9, skip sigma < 1/255,
-// clamp at 0.99) are the reference's: fp64 conic form, fp32 sigma from the
-// SFU with guard bands (stage.cuh), and an exact fp64 re-evaluation of the
-// entry inside a band.  The gradient arithmetic runs in fp64 (sigma from the
+// clamp at 0.99) are the reference's: the fp64 conic form, narrowed to the
+// fp32 exp2 argument u, is compared with the entry's two cuts (blend:
+// min(9U, log2(255 alpha)); clamp: log2(alpha / 0.99)), computed once per
+// (warp, entry) by the cull, and inside a guard band around either cut the
+// entry is re-evaluated exactly in fp64.  The gradient arithmetic runs in fp64 (sigma from the
 // fp64 exp2, T / Q recurrence, s_i, mean2d and cov products; alpha and colour
 // products in fp32): the reverse recurrence compounds every error of sigma
 // and T over the walk, and the centre gradients (|g| ~ 4e2 at c3) must hold
@@ -49,7 +51,7 @@ struct BwSmem {
   uint32_t gid[BW_NSTAGE][BW_BATCH];
   unsigned long long full[BW_NSTAGE];
   unsigned long long empty[BW_NSTAGE];
-  unsigned char list[BW_CONSUMERS][BW_BATCH];
+  int4 list[BW_CONSUMERS][BW_BATCH];  // (slot index, blend cut, clamp cut, -) of the entries touching the sub-tile
   double exp2tab[16];
   int max_last;
 };
@@ -104,6 +106,16 @@ __device__ __forceinline__ int reduce9_index(int lane) {
   const int n4 = (lane & 4) ? n8 - 2 : (n8 < 2 ? n8 : 2);
   const int n2 = (lane & 2) ? n4 - 1 : (n4 < 1 ? n4 : 1);
   return (n2 > 0 && (lane & 1) == 0) ? b16 + b8 + b4 + b2 : -1;  // lanes 2k, 2k+1 hold the same total
+}
+
+// Clamp cut of an entry: sigma = alpha 2^-u is clamped at 0.99 iff
+// u < log2(alpha / 0.99) (lg2.approx, as entry_ucut; NaN for an
+// ill-conditioned conic: always decided exactly).
+__device__ __forceinline__ float entry_uclamp(float a32) {
+  if (a32 < 0.0f) return __int_as_float(0x7fc00000);
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(a32 * (float)(1.0 / ALPHA_CLAMP)));
+  return l;
 }
 
 struct BwExact {
@@ -190,27 +202,28 @@ __device__ __forceinline__ void bw_pixel_init(BwPix& q, bool inside, int64_t p, 
 // (mean2d, cov: they reach the centre gradients through the focal / depth
 // chain) and fp32 for the rest (alpha, colour).
 __device__ __forceinline__ void bw_pixel_step(BwPix& q, const StageEntry& E, int rel, double fx, double fy,
-                                              const double* __restrict__ tab, double vd[5], float vf[4]) {
+                                              float ucut, float uclamp, const double* __restrict__ tab, double vd[5],
+                                              float vf[4]) {
   const bool act = q.last >= 0 && rel <= q.last;
   if (!act) return;  // entry after this pixel's last blended one
   const double dx = fx - E.a.x, dy = fy - E.a.y;
   const double m = fma(dx, fma(E.b.y, dy, E.b.x * dx), (E.c.x * dy) * dy);
   const double u = m * U_SCALE;
   const float uu = __double2float_rn(u);
-  const float a32 = E.f.col.x;
-  const float sraw = fabsf(a32) * ex2_neg(uu);
-  bool clamped = sraw > CLAMP_F;
-  bool ok = uu < U9_LO && fminf(sraw, CLAMP_F) >= SKIP_F;
-  const float key = fminf(amb_key(uu, fminf(sraw, CLAMP_F), a32),
-                          fabsf(fmaf(sraw, CLAMP_BAND_INV, -CLAMP_F * CLAMP_BAND_INV)));
+  // the blend and clamp decisions against the entry's cuts (stage.cuh
+  // entry_ucut; NaN cut: always exact)
+  const float dd = uu - ucut, dc = uu - uclamp;
+  bool ok = dd < -U_BAND;
+  bool clamped = dc < -U_BAND;
   double sg, gauss;
-  if (key <= 1.0f) {  // rare: decide (and evaluate) in the reference's order
+  if (!(fabsf(dd) > U_BAND) || !(fabsf(dc) > U_BAND)) {  // rare: decide (and evaluate) in the reference's order
     const BwExact x = bw_exact_entry(E, fx, fy);
     ok = x.sig >= 0.0;
     sg = x.sig;
     gauss = x.gauss;
     clamped = x.clamped;
   } else {
+    if (!ok) return;
     gauss = exp2_neg64(u, uu, tab);
     sg = clamped ? ALPHA_CLAMP : E.d.x * gauss;
   }
@@ -348,22 +361,29 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
           hit = ellipse_meets_box(sm.ent[slot][i].f.con, q, wx0, wx1, wy0, wy1);
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (hit) sm.list[warp][nl + __popc(m & lanemask_lt())] = (unsigned char)i;
+      if (hit) {
+        const float a32 = sm.ent[slot][i].f.col.x;
+        sm.list[warp][nl + __popc(m & lanemask_lt())] =
+            make_int4(i, __float_as_int(entry_ucut(a32)), __float_as_int(entry_uclamp(a32)), 0);
+      }
       nl += __popc(m);
     }
     __syncwarp();
     for (int li = 0; li < nl; li++) {
-      const int i = sm.list[warp][li];
+      const int4 L = sm.list[warp][li];
+      const int i = L.x;
       const StageEntry& E = sm.ent[slot][i];
+      const float ucut = __int_as_float(L.y), uclamp = __int_as_float(L.z);
       double vd[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       float vf[4] = {0.f, 0.f, 0.f, 0.f};
-      bw_pixel_step(q0, E, lo + i, fx, fy0, sm.exp2tab, vd, vf);
-      bw_pixel_step(q1, E, lo + i, fx, fy1, sm.exp2tab, vd, vf);
+      bw_pixel_step(q0, E, lo + i, fx, fy0, ucut, uclamp, sm.exp2tab, vd, vf);
+      bw_pixel_step(q1, E, lo + i, fx, fy1, ucut, uclamp, sm.exp2tab, vd, vf);
       const bool any = vf[1] != 0.f || vf[2] != 0.f || vf[3] != 0.f || vf[0] != 0.f || vd[0] != 0.0;
       if (!__any_sync(0xffffffffu, any)) continue;
+      double* dst = screen + 9 * (size_t)sm.gid[slot][i];
       double v[9] = {vd[0], vd[1], vd[2], vd[3], vd[4], (double)vf[0], (double)vf[1], (double)vf[2], (double)vf[3]};
       const double tot = warp_reduce9(v, lane);
-      if (vidx >= 0 && tot != 0) atomicAdd(&screen[9 * (size_t)sm.gid[slot][i] + vidx], (double)tot);
+      if (vidx >= 0 && tot != 0) atomicAdd(dst + vidx, (double)tot);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);

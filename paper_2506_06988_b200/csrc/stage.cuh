@@ -176,15 +176,19 @@ __constant__ double c_exp2_tab[16] = {1.0,
 __device__ __forceinline__ void exp2_tab_load(double* tab) {
   if (threadIdx.x < 16) tab[threadIdx.x] = c_exp2_tab[threadIdx.x];
 }
+// the polynomial's coefficients live in constant memory: DFMA reads them as
+// c[][] operands (as immediates every use costs two uniform moves)
+__constant__ double c_exp2_poly[6] = {-0.0013333558146428441, 0.009618129107628477, -0.055504108664821576,
+                                      0.2402265069591007,     -0.6931471805599453,  1.0};
 __device__ __forceinline__ double exp2_neg64(double u, float uu, const double* tab) {
   const int k = __float2int_rd(fminf(fmaxf(uu, 0.0f), 60.0f) * 16.0f);
   const double r = fma((double)k, -0.0625, u);
-  double p = -0.0013333558146428441;
-  p = fma(p, r, 0.009618129107628477);
-  p = fma(p, r, -0.055504108664821576);
-  p = fma(p, r, 0.2402265069591007);
-  p = fma(p, r, -0.6931471805599453);
-  p = fma(p, r, 1.0);
+  double p = c_exp2_poly[0];
+  p = fma(p, r, c_exp2_poly[1]);
+  p = fma(p, r, c_exp2_poly[2]);
+  p = fma(p, r, c_exp2_poly[3]);
+  p = fma(p, r, c_exp2_poly[4]);
+  p = fma(p, r, c_exp2_poly[5]);
   const double t = p * tab[k & 15];  // in (0.5, 1.03]: x 2^-(k >> 4) by the exponent field
   return __hiloint2double(__double2hiint(t) - ((k >> 4) << 20), __double2loint(t));
 }

@@ -29,6 +29,10 @@
 // of the bins skip their work; the caller grows the buffer and re-runs.
 #include "sort.cuh"
 
+#ifndef HGS_PREP_3K
+#define HGS_PREP_3K 0
+#endif
+
 namespace hgs {
 
 // Order-preserving compaction of the visible rows' sort keys (chained scan).
@@ -591,6 +595,67 @@ __global__ void __launch_bounds__(256) coarse_prep_offsets_kernel(const ushort4*
     run += c[q];
   }
   if (b0 + PREP_ROWS >= m && threadIdx.x == 0) pair_off[m] = *npairs;
+}
+
+// The three prep steps fused: one persistent chained-scan pass (decoupled
+// look-back, sort.cuh) gathers the rectangles in depth order, scans the
+// rows' coarse pair counts and writes the pair offsets, warp-range starts
+// and the total.
+__global__ void __launch_bounds__(SCAN_THREADS) coarse_prep_kernel(const uint32_t* __restrict__ sorted_rows,
+                                                                   const ushort4* __restrict__ rect,
+                                                                   const int64_t* counters, int ss,
+                                                                   ushort4* __restrict__ rsort,
+                                                                   uint32_t* __restrict__ pair_off,
+                                                                   uint32_t* __restrict__ wstart,
+                                                                   uint32_t* __restrict__ npairs, uint64_t* status,
+                                                                   uint32_t* part_ctr) {
+  pdl_enter();
+  __shared__ int s_part;
+  const int64_t m = counters[0];
+  if (m == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      pair_off[0] = 0;
+      *npairs = 0;
+    }
+    return;
+  }
+  const int nparts = (int)((m + SCAN_TILE - 1) / SCAN_TILE);
+  while (true) {
+    if (threadIdx.x == 0) s_part = (int)atomicAdd(part_ctr, 1u);
+    __syncthreads();
+    const int part = s_part;
+    __syncthreads();
+    if (part >= nparts) break;
+    const int64_t base = (int64_t)part * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+    uint32_t c[SCAN_IPT];
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; j++) {
+      const int64_t i = base + j;
+      c[j] = 0;
+      if (i < m) {
+        const ushort4 rc = rect[sorted_rows[i]];
+        rsort[i] = rc;
+        c[j] = coarse_pairs(rc, ss);
+      }
+    }
+    uint64_t excl[SCAN_IPT];
+    uint64_t total;
+    chained_scan_partition(part, m, [&](int64_t i) -> uint64_t { return (uint64_t)c[i - base]; }, status, excl,
+                           total);
+#pragma unroll
+    for (int j = 0; j < SCAN_IPT; j++) {
+      const int64_t i = base + j;
+      if (i < m) {
+        const uint32_t run = (uint32_t)excl[j];
+        pair_off[i] = run;
+        for (uint32_t k = (run + CP_WARP - 1) / CP_WARP; k * CP_WARP < run + c[j]; k++) wstart[k] = (uint32_t)i;
+      }
+    }
+    if (part == nparts - 1 && threadIdx.x == 0) {
+      pair_off[m] = (uint32_t)total;
+      *npairs = (uint32_t)total;
+    }
+  }
 }
 
 // Walk the CP_WARP pairs of warp range k in rounds of 32 (lane = pair):
@@ -1178,6 +1243,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     // 4. two-level rect binning straight into the final (tile, depth, row) order
     const int sx = (tx + (1 << ss) - 1) >> ss, sy = (ty + (1 << ss) - 1) >> ss, n_super = sx * sy;
     const int pblk = (int)((n + PREP_ROWS - 1) / PREP_ROWS);  // upper bound: kernels read m on the device
+#if HGS_PREP_3K
     launch_pdl(coarse_prep_sum_kernel, dim3(pblk), dim3(256), 0, st, rows, (const ushort4*)proj->rect, tiles->counters, ss, s.rsort,
                                                  s.bsum);
     HGS_CHECK_LAUNCH();
@@ -1186,6 +1252,15 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     launch_pdl(coarse_prep_offsets_kernel, dim3(pblk), dim3(256), 0, st, s.rsort, tiles->counters, ss, s.bsum, s.npairs, s.pair_off,
                                                      s.wstart);
     HGS_CHECK_LAUNCH();
+#else
+    // (the second half of scan_status and part_ctr[21] belong to offsets_kernel, unused on this path)
+    static int prep_cap = 0;
+    if (prep_cap == 0) prep_cap = persistent_grid((const void*)coarse_prep_kernel, SCAN_THREADS, 0);
+    launch_pdl(coarse_prep_kernel, dim3((int)tmax<int64_t>(1, tmin<int64_t>(prep_cap, pblk))), dim3(SCAN_THREADS), 0, st,
+               (const uint32_t*)rows, (const ushort4*)proj->rect, (const int64_t*)tiles->counters, ss, s.rsort,
+               s.pair_off, s.wstart, s.npairs, s.scan_status + s.parts_n + 1, s.part_ctr + 21);
+    HGS_CHECK_LAUNCH();
+#endif
     CoarseArgs ca{rows, s.rsort, s.pair_off, s.wstart, s.npairs, tiles->counters, tiles->capacity, ss, sx, n_super};
     static int cgrid = 0, sgrid = 0, sgrid_ns = -1;
     const size_t ssmem = scatter_smem_bytes(n_super);
