@@ -37,8 +37,8 @@ __global__ void mask_kernel(const float* __restrict__ t, int64_t n, double k, in
 
 // scalars: l1, dssim, l_c, l_t, total, mean_T_on_mesh (acc: 0 sum|d|, 1 n_cov,
 // 2 sum(mask sq), 3 sum T cov, 6 sum s)
-__global__ void loss_scalars_kernel(const double* __restrict__ acc, int64_t n, double lam, int tex_active,
-                                    double tex_w, int has_mesh, double* __restrict__ scalars) {
+__device__ void loss_scalars(const double* __restrict__ acc, int64_t n, double lam, int tex_active, double tex_w,
+                             int has_mesh, double* __restrict__ scalars) {
   const double l1 = acc[0] / (double)n;
   const double ssim = acc[6] / (double)n;
   const double ds = (1.0 - ssim) / 2.0;
@@ -53,6 +53,29 @@ __global__ void loss_scalars_kernel(const double* __restrict__ acc, int64_t n, d
   scalars[5] = (has_mesh && ncov > 0) ? acc[3] / ncov : __longlong_as_double(0x7ff8000000000000LL);
 }
 
+
+// The tile partials of the forward kernel (part[q][tile], q: |d|, n_cov,
+// mask sq, T cov, s) summed in a fixed order -- per thread over tiles
+// t, t + 256, ..., then a fixed tree -- and the loss scalars (one CTA).
+__global__ void __launch_bounds__(256) loss_reduce_kernel(const double* __restrict__ part, int tiles,
+                                                          double* __restrict__ acc, int64_t n, double lam,
+                                                          int tex_active, double tex_w, int has_mesh,
+                                                          double* __restrict__ scalars) {
+  __shared__ double red[256];
+  for (int q = 0; q < 5; q++) {
+    double x = 0.0;
+    for (int t = threadIdx.x; t < tiles; t += 256) x += part[(size_t)q * tiles + t];
+    red[threadIdx.x] = x;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) acc[q == 4 ? 6 : q] = red[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss_scalars(acc, n, lam, tex_active, tex_w, has_mesh, scalars);
+}
 
 // ---- fused SSIM tiles ------------------------------------------------------
 // One CTA (256 threads) per 16x16 output tile, all three channels.  The tile
@@ -118,7 +141,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_tile_kernel(const float* __re
                                                                const int32_t* __restrict__ tri,
                                                                const float* __restrict__ t, int h, int w, LossWin win,
                                                                double mask_k, int variant, int tex_active,
-                                                               float* __restrict__ d, double* __restrict__ acc) {
+                                                               float* __restrict__ d, double* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char ssf_raw[];
   SsimFwdSmem& sm = *reinterpret_cast<SsimFwdSmem*>(ssf_raw);
   const int x0 = blockIdx.x * SS_T - 5, y0 = blockIdx.y * SS_T - 5;
@@ -260,7 +283,8 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_tile_kernel(const float* __re
   if (threadIdx.x < 5) {
     double x = 0.0;
     for (int k = 0; k < 8; k++) x += red[threadIdx.x][k];
-    atomicAdd(&acc[threadIdx.x == 4 ? 6 : threadIdx.x], x);
+    // per-tile partials, summed in tile order by loss_reduce_kernel (run-to-run deterministic)
+    part[(size_t)threadIdx.x * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = x;
   }
 }
 
@@ -385,7 +409,8 @@ extern "C" int hgs_transmittance_mask(const float* t, int64_t n, double k, int32
 
 extern "C" size_t hgs_loss_scratch_bytes(int32_t height, int32_t width) {
   const size_t n = (size_t)height * width * 3;
-  return hgs::align_up(4 * 3 * n, 256) + 256;
+  const size_t tiles = (size_t)((width + hgs::SS_T - 1) / hgs::SS_T) * (size_t)((height + hgs::SS_T - 1) / hgs::SS_T);
+  return hgs::align_up(4 * 3 * n, 256) + 256 + 5 * 8 * tiles;
 }
 
 extern "C" int hgs_composite_loss(const float* i_gt, const float* i_h, const float* i_m, const int32_t* triangle_id,
@@ -408,9 +433,9 @@ extern "C" int hgs_composite_loss(const float* i_gt, const float* i_h, const flo
   float* dmaps = (float*)base;  // 3 x n SSIM derivative maps
   base += align_up(4 * 3 * n, 256);
   double* acc = (double*)base;  // 8 doubles
+  double* part = acc + 32;      // 5 x tiles per-tile partial sums
   LossWin win;
   for (int k = 0; k < 11; k++) win.w[k] = window11_host[k];
-  cudaMemsetAsync(acc, 0, 8 * sizeof(double), st);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ssim_fwd_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SsimFwdSmem));
@@ -419,10 +444,10 @@ extern "C" int hgs_composite_loss(const float* i_gt, const float* i_h, const flo
   }
   const dim3 tg((width + SS_T - 1) / SS_T, (height + SS_T - 1) / SS_T);
   ssim_fwd_tile_kernel<<<tg, 256, sizeof(SsimFwdSmem), st>>>(i_gt, i_h, i_m, triangle_id, t, height, width, win,
-                                                             mask_k, mask_variant, texture_active, dmaps, acc);
+                                                             mask_k, mask_variant, texture_active, dmaps, part);
   HGS_CHECK_LAUNCH();
-  loss_scalars_kernel<<<1, 1, 0, st>>>(acc, n, lam_dssim, texture_active, texture_weight, triangle_id != nullptr,
-                                       scalars);
+  loss_reduce_kernel<<<1, 256, 0, st>>>(part, (int)(tg.x * tg.y), acc, n, lam_dssim, texture_active, texture_weight,
+                                        triangle_id != nullptr, scalars);
   HGS_CHECK_LAUNCH();
   ssim_bwd_tile_kernel<<<tg, 256, sizeof(SsimBwdSmem), st>>>(i_gt, i_h, i_m, triangle_id, t, height, width, win, dmaps,
                                                              acc, lam_dssim, texture_active, texture_weight, mask_k,
