@@ -40,7 +40,10 @@ __device__ __forceinline__ void quat_to_rot(double q0, double q1, double q2, dou
   Rq[8] = 1.0 - 2.0 * (x * x + y * y);
 }
 
-__global__ void __launch_bounds__(256, 3) preprocess_kernel(const hgs_camera* __restrict__ cam_ptr, hgs_gaussians gs,
+#ifndef HGS_PP_MINB
+#define HGS_PP_MINB 3
+#endif
+__global__ void __launch_bounds__(256, HGS_PP_MINB) preprocess_kernel(const hgs_camera* __restrict__ cam_ptr, hgs_gaussians gs,
                                                          int tile_px, int tiles_x, int tiles_y, hgs_projected out) {
   pdl_enter();  // releases the binning chain's PDL launches early
   __shared__ CamConst cs;
