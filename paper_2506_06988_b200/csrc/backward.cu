@@ -42,7 +42,12 @@ namespace hgs {
 #endif
 constexpr int BW_BATCH = HGS_BW_BATCH;
 constexpr int BW_NSTAGE = HGS_BW_NSTAGE;
-constexpr int BW_CONSUMERS = 4;  // 8x8-pixel sub-tiles, two pixels per lane
+#ifndef HGS_BW_NPX
+#define HGS_BW_NPX 2
+#endif
+constexpr int BW_NPX = HGS_BW_NPX;          // pixels per lane
+constexpr int BW_CONSUMERS = 8 / BW_NPX;    // 8-wide sub-tiles of 4 * BW_NPX rows
+constexpr int BW_SUBH = 4 * BW_NPX;
 constexpr int BW_THREADS = (BW_CONSUMERS + 1) * 32;
 constexpr float CLAMP_BAND_INV = 1.0f / (2.0f * EPS_SIG * CLAMP_F);
 
@@ -287,18 +292,21 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
   }
   exp2_tab_load(sm.exp2tab);
   __syncthreads();
-  // consumer pixels: warp w owns the 8x8 sub-tile (w & 1, w >> 1); lane
-  // (x, y) = (lane & 7, lane >> 3) holds pixels (x, y) and (x, y + 4)
-  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
+  // consumer pixels: warp w owns the 8 x BW_SUBH sub-tile (w & 1, w >> 1);
+  // lane (x, y) = (lane & 7, lane >> 3) holds pixels (x, y + 4 k), k < BW_NPX
+  const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * BW_SUBH;
   const int px = tx * 16 + sx0 + (lane & 7);
-  const int py0 = ty * 16 + sy0 + (lane >> 3), py1 = py0 + 4;
+  const int py0 = ty * 16 + sy0 + (lane >> 3);
   const bool cons = warp < BW_CONSUMERS;
-  BwPix q0, q1;
-  bw_pixel_init(q0, cons && px < width && py0 < height, (int64_t)py0 * width + px, s, mesh, bg0, bg1, bg2, final_t,
-                last_idx, grad_color, grad_t, mesh_grad, accumulate_mesh);
-  bw_pixel_init(q1, cons && px < width && py1 < height, (int64_t)py1 * width + px, s, mesh, bg0, bg1, bg2, final_t,
-                last_idx, grad_color, grad_t, mesh_grad, accumulate_mesh);
-  const int ml = max(q0.last, q1.last);
+  BwPix q[BW_NPX];
+  int ml = -1;
+#pragma unroll
+  for (int k = 0; k < BW_NPX; k++) {
+    const int py = py0 + 4 * k;
+    bw_pixel_init(q[k], cons && px < width && py < height, (int64_t)py * width + px, s, mesh, bg0, bg1, bg2, final_t,
+                  last_idx, grad_color, grad_t, mesh_grad, accumulate_mesh);
+    ml = max(ml, q[k].last);
+  }
   if (ml >= 0) atomicMax(&sm.max_last, ml);
   __syncthreads();
   const int top = sm.max_last;  // newest entry any pixel of the tile used
@@ -335,11 +343,11 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
   }
 
   // -------------------------------------------------------------- consumers
-  const double fx = px + 0.5, fy0 = py0 + 0.5, fy1 = py1 + 0.5;
+  const double fx = px + 0.5, fy0 = py0 + 0.5;
   const float wx0 = tx * 16 + sx0 + 0.5f, wx1 = wx0 + 7.0f;
-  const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + 7.0f;
+  const float wy0 = ty * 16 + sy0 + 0.5f, wy1 = wy0 + (float)(BW_SUBH - 1);
   const int vidx = reduce9_index(lane);
-  int wlast = max(q0.last, q1.last);  // newest entry any pixel of this warp used
+  int wlast = ml;  // newest entry any pixel of this warp used
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
   for (int b = 0; b < nbatches; b++) {
@@ -376,8 +384,9 @@ __global__ void __launch_bounds__(BW_THREADS, HGS_BW_MINB) blend_backward_kernel
       const float ucut = __int_as_float(L.y), uclamp = __int_as_float(L.z);
       double vd[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       float vf[4] = {0.f, 0.f, 0.f, 0.f};
-      bw_pixel_step(q0, E, lo + i, fx, fy0, ucut, uclamp, sm.exp2tab, vd, vf);
-      bw_pixel_step(q1, E, lo + i, fx, fy1, ucut, uclamp, sm.exp2tab, vd, vf);
+#pragma unroll
+      for (int k = 0; k < BW_NPX; k++)
+        bw_pixel_step(q[k], E, lo + i, fx, fy0 + 4.0 * k, ucut, uclamp, sm.exp2tab, vd, vf);
       const bool any = vf[1] != 0.f || vf[2] != 0.f || vf[3] != 0.f || vf[0] != 0.f || vd[0] != 0.0;
       if (!__any_sync(0xffffffffu, any)) continue;
       double* dst = screen + 9 * (size_t)sm.gid[slot][i];
