@@ -34,6 +34,9 @@
 namespace hgs {
 
 constexpr int BLEND_TILE = 16;
+// hgs_blend_out.fixup layout (fast path): [0] slots reserved, [1] tiles
+// finished, [2] slots claimed, [3..] queue slots (flagged pixel + 1, 0 = empty)
+constexpr int FIX_RESERVED = 0, FIX_DONE = 1, FIX_CLAIMED = 2, FIX_SLOTS = 3;
 constexpr int BLEND_THREADS = BLEND_TILE * BLEND_TILE;
 
 #ifndef HGS_FAST_BATCH
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(FAST_THREADS, PREC ? HGS_FAST_MINB_PREC : HGS_
   if (!inside) return;
   if (flagged) {  // hand the pixel to the exact walk (work list: count, pixel ids)
     const int slot = atomicAdd(&fixup[0], 1);
-    fixup[1 + slot] = (int32_t)p;
+    fixup[1 + slot] = (int32_t)p + 1;
     return;
   }
   write_pixel(out, mesh, mesh_here, p, T, r, g, bl, dacc, acc, last >= 0 ? s + last : -1, bg0, bg1, bg2,
@@ -614,6 +617,7 @@ struct TileSmem {
   double exp2tab[16];
   int done_warps;
   int end_batch;
+  int finished_warps;
   unsigned long long stats[2];
 };
 
@@ -709,6 +713,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     }
     sm.done_warps = 0;
     sm.end_batch = 0x7fffffff;
+    sm.finished_warps = 0;
     sm.stats[0] = sm.stats[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -918,14 +923,22 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
 #pragma unroll
   for (int h = 0; h < 2; h++) {
     if (!inside[h]) continue;
-    if (q[h].flagged) {  // hand the pixel to the exact walk (work list: count, pixel ids)
-      const int slot = atomicAdd(&fixup[0], 1);
-      fixup[1 + slot] = (int32_t)pix[h];
+    if (q[h].flagged) {  // queue the pixel for the exact walk (slot value pixel + 1; 0 = empty)
+      const int slot = atomicAdd(&fixup[FIX_RESERVED], 1);
+      fixup[FIX_SLOTS + slot] = (int32_t)pix[h] + 1;
       continue;
     }
     write_pixel(out, mesh, mesh_here[h], pix[h], q[h].T, q[h].r, q[h].g, q[h].b, q[h].dacc, q[h].acc,
                 q[h].last >= 0 ? s + q[h].last : -1, bg0, bg1, bg2, mask_variant, mask_k,
                 PREC ? q[h].T64 : (double)q[h].T);
+  }
+  // the tile is finished once its last consumer warp is: count it for the
+  // exact-walk kernel, which drains the queue while the blend still runs
+  __threadfence();
+  __syncwarp();
+  if (lane == 0 && atomicAdd(&sm.finished_warps, 1) == TB_CONSUMERS - 1) {
+    __threadfence();
+    atomicAdd(&fixup[FIX_DONE], 1);
   }
 }
 
@@ -942,7 +955,57 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t wi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wi < count; wi += nwarps) {
-    const int64_t p = fixup ? fixup[1 + wi] : wi;
+    const int64_t p = fixup ? fixup[1 + wi] - 1 : wi;
+    const int px = (int)(p % width), py = (int)(p / width);
+    const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
+    const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
+    const double limit = mesh_here ? mesh.depth[p] : __longlong_as_double(0x7ff0000000000000LL);
+    const ExactPixel q = exact_walk2(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5,
+                                    limit, lane);
+    if (lane == 0)
+      write_pixel(out, mesh, mesh_here, p, q.T, q.r, q.g, q.b, q.dacc, 1.0 - q.T, q.last, bg0, bg1, bg2,
+                  mask_variant, mask_k, q.T);
+  }
+}
+
+// The exact walk as a queue consumer running beside the blend: launched
+// right behind blend_tile_kernel (programmatic launch: its CTAs start once
+// every blend CTA has started) it does NOT wait for the blend grid; warps
+// claim queue slots and replay each flagged pixel as soon as its tile has
+// queued it, so the replays overlap the blend's last waves instead of
+// following them.  Exits when every tile is finished and the queue is
+// drained.  Slots are reset to 0 after use (the queue is empty at rest).
+__global__ void __launch_bounds__(64) blend_exact_queue_kernel(
+    const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
+    int tiles_x, int n_tiles, int width, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
+    double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (counters && counters[2]) return;  // overflowed bins: the blend wrote nothing
+  const int lane = threadIdx.x & 31;
+  volatile int32_t* vf = fixup;
+  while (true) {
+    int idx = 0, quit = 0;
+    if (lane == 0) {
+      idx = atomicAdd(&fixup[FIX_CLAIMED], 1);
+      while (true) {
+        if (idx < vf[FIX_RESERVED]) break;  // a pixel is (or is being) queued in this slot
+        if (vf[FIX_DONE] == n_tiles) {  // all tiles finished: the reservation count is final
+          __threadfence();
+          if (idx >= vf[FIX_RESERVED]) quit = 1;
+          break;
+        }
+        __nanosleep(500);
+      }
+    }
+    quit = __shfl_sync(0xffffffffu, quit, 0);
+    if (quit) break;
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    int32_t v = 0;
+    if (lane == 0) {
+      while ((v = vf[FIX_SLOTS + idx]) == 0) __nanosleep(100);
+      vf[FIX_SLOTS + idx] = 0;
+    }
+    const int64_t p = __shfl_sync(0xffffffffu, v, 0) - 1;
     const int px = (int)(p % width), py = (int)(p / width);
     const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
     const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
@@ -985,7 +1048,7 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
 #define HGS_BLEND_V1 0
 #endif
   if (out->fixup && proj->cull && !HGS_FWD_EXACT) {
-    zero_pdl(st, out->fixup, sizeof(int32_t));
+    zero_pdl(st, out->fixup, (HGS_BLEND_V1 ? 1 : FIX_SLOTS) * sizeof(int32_t));
     HGS_CHECK_LAUNCH();
     const size_t smem = sizeof(FastSmem);
     static bool attr = false;
@@ -1023,11 +1086,21 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
 #endif
     HGS_CHECK_LAUNCH();
+#if HGS_BLEND_V1
     // exact fix-up: one warp per flagged pixel (persistent grid over the device-side work list)
     launch_pdl(blend_exact_kernel, dim3(2 * NUM_SMS), dim3(256), 0, st, (const BlendRec*)proj->rec, tiles->entries,
                                                     tiles->tile_starts, tiles->tiles_x, width, height, ml,
                                                     bg_host3[0], bg_host3[1], bg_host3[2], mask_variant,
                                                     mask_k, *out, out->fixup, tiles->counters);
+#else
+    // exact fix-up: queue consumer beside the blend (one warp per flagged pixel)
+    // small CTAs (2 warps, ~11k registers): they fit beside the blend's
+    // resident CTAs as soon as its last wave starts retiring
+    launch_pdl(blend_exact_queue_kernel, dim3(8 * NUM_SMS), dim3(64), 0, st, (const BlendRec*)proj->rec,
+               (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_tiles, width, ml,
+               bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
+               (const int64_t*)tiles->counters);
+#endif
     HGS_CHECK_LAUNCH();
   } else {
     launch_pdl(blend_exact_kernel, dim3(ceil_div(npix * 32, 256)), dim3(256), 0, st, (const BlendRec*)proj->rec, tiles->entries,

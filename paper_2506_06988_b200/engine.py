@@ -57,7 +57,7 @@ class HybridRenderer:
         self.cull = torch.empty(n * 12, dtype=torch.float32, device=dev)
         self.sort_keys = torch.empty(n, dtype=torch.int64, device=dev)
         self.tile_diff = torch.empty(16 * (self.tiles_x + 1) * (self.tiles_y + 1), dtype=torch.int32, device=dev)
-        self.fixup = torch.zeros(h * w + 1, dtype=torch.int32, device=dev)
+        self.fixup = torch.zeros(h * w + 4, dtype=torch.int32, device=dev)
         self.tile_starts = torch.zeros(self.n_tiles + 1, dtype=torch.int64, device=dev)
         self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
         self.counters_host = torch.zeros(4, dtype=torch.int64).pin_memory()

@@ -227,13 +227,16 @@ class _Scratch:
     def __init__(self):
         self.bufs = {}
 
-    def get(self, name: str, nbytes: int, device) -> torch.Tensor:
+    def get(self, name: str, nbytes: int, device, zeroed: bool = False) -> torch.Tensor:
+        """zeroed: allocated as zeros (buffers whose users keep them zero at
+        rest, e.g. the exact-walk queue of hgs_blend_forward)."""
         device = torch.device(device)
         sid = torch.cuda.current_stream(device).cuda_stream if device.type == "cuda" else 0
         key = (name, device, sid)
         b = self.bufs.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty((max(int(nbytes * 1.25), 256) + 255) // 256 * 256, dtype=torch.uint8, device=device)
+            n = (max(int(nbytes * 1.25), 256) + 255) // 256 * 256
+            b = (torch.zeros if zeroed else torch.empty)(n, dtype=torch.uint8, device=device)
             self.bufs[key] = b
         return b
 
@@ -354,7 +357,7 @@ def _blend(proj, tiles: TileBins, width, height, mesh: Optional[MeshLayer], bg: 
         mask_t = torch.empty(height, width, dtype=torch.float32, device=dev)
         out.mask = _lib.ptr(mask_t)
     out.stats = _lib.ptr(stats)
-    fixup = SCRATCH.get("fixup", 4 * (height * width + 1), dev)
+    fixup = SCRATCH.get("fixup", 4 * (height * width + 4), dev, zeroed=True)
     out.fixup = _lib.ptr(fixup)
     ml = mesh.struct() if mesh is not None else _lib.HGSMeshLayer()
     _lib.call("hgs_blend_forward", ctypes.byref(proj.struct()), ctypes.byref(tiles.struct()), int(width), int(height),
