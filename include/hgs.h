@@ -135,7 +135,11 @@ typedef struct hgs_tiles {
   int64_t* counters;    /* 4 */
   void* scratch;
   size_t scratch_bytes; /* >= hgs_tiles_scratch_bytes(n, capacity, tiles) */
+  int32_t* ready;       /* device int32[HGS_READY_INTS] or NULL: hgs_build_tiles publishes each finished block of
+                           4x4 tiles here and hgs_blend_forward claims tiles in that order, starting while the
+                           last blocks are still being binned (NULL: the blend waits for the whole binning) */
 } hgs_tiles;
+#define HGS_READY_INTS (2 + 2048)
 
 /* MeshLayer (splat/render.py:26-41).  color == NULL means "no mesh". */
 typedef struct hgs_mesh_layer {

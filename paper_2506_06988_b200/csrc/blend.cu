@@ -34,9 +34,13 @@
 namespace hgs {
 
 constexpr int BLEND_TILE = 16;
-// hgs_blend_out.fixup layout (fast path): [0] slots reserved, [1] tiles
-// finished, [2] slots claimed, [3..] queue slots (flagged pixel + 1, 0 = empty)
-constexpr int FIX_RESERVED = 0, FIX_DONE = 1, FIX_CLAIMED = 2, FIX_SLOTS = 3;
+// hgs_blend_out.fixup layout (fast path): [0] slots reserved, [1] blend CTAs
+// finished, [2] slots claimed, [3] queue-consumer warps exited, [4..] queue
+// slots (flagged pixel + 1, 0 = empty); all zero at rest
+constexpr int FIX_RESERVED = 0, FIX_DONE = 1, FIX_CLAIMED = 2, FIX_EXITED = 3, FIX_SLOTS = 4;
+// spin-wait bound of the queue consumers (~ tens of seconds of nanosleeps):
+// a broken handoff traps (a launch error) instead of hanging the device
+constexpr uint32_t QUEUE_SPIN_LIMIT = 1u << 26;
 constexpr int BLEND_THREADS = BLEND_TILE * BLEND_TILE;
 
 #ifndef HGS_FAST_BATCH
@@ -147,7 +151,7 @@ __device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec,
   bool done = false;
   auto idx = [&](int64_t rbase, int u) -> uint32_t {
     const int64_t k = rbase + EW * lane + u;
-    return k < e ? __ldg(entries + k) : 0u;
+    return k < e ? __ldcg(entries + k) : 0u;  // L2 (the queue consumer runs beside the binning's writers)
   };
   uint32_t ix[4][EW];
 #pragma unroll
@@ -618,6 +622,7 @@ struct TileSmem {
   int done_warps;
   int end_batch;
   int finished_warps;
+  int tile_id;
   unsigned long long stats[2];
 };
 
@@ -697,15 +702,18 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
-    const int64_t* __restrict__ counters) {
-  pdl_enter();
+    const int64_t* __restrict__ counters, int* ready, int qs, int sx_super) {
+  // ready != NULL: launched behind the fine binning without waiting for its
+  // grid; each CTA claims the next tile of the quads it has published
+  // (common.cuh).  Otherwise: one CTA per tile after the binning completed.
+  if (ready)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  else
+    pdl_enter();
   if (counters && counters[2]) return;  // entry buffer overflowed: bins are invalid, the caller re-renders
   extern __shared__ __align__(128) unsigned char tile_smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(tile_smem_raw);
-  const int tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
-  const int nbatches = (int)((e - s + TB_BATCH - 1) / TB_BATCH);
   if (threadIdx.x == 0) {
     for (int i = 0; i < TB_NSTAGE; i++) {
       mbar_init(&sm.full[i], 32);
@@ -715,10 +723,35 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     sm.end_batch = 0x7fffffff;
     sm.finished_warps = 0;
     sm.stats[0] = sm.stats[1] = 0;
+    int t = blockIdx.x;
+    if (ready) {
+      const int idx = atomicAdd(&ready[1], 1);
+      const volatile int* vr = ready;
+      int qv;
+      for (uint32_t spin = 0; (qv = vr[READY_HDR + (idx >> 4)]) == 0; spin++) {
+        if (spin > QUEUE_SPIN_LIMIT) __trap();  // never hang the GPU on a broken handoff
+        __nanosleep(256);
+      }
+      __threadfence();  // the quad's entries (published after a fence) are visible from here on
+      const int sq = qv - 1;
+      const int sup = sq >> (2 * qs), quad = sq & ((1 << (2 * qs)) - 1);
+      const int tx0 = (sup % sx_super) * (4 << qs) + (quad & ((1 << qs) - 1)) * 4;
+      const int ty0 = (sup / sx_super) * (4 << qs) + (quad >> qs) * 4;
+      const int ttx = tx0 + (idx & 3), tty = ty0 + ((idx >> 2) & 3);
+      t = (ttx < tiles_x && tty * BLEND_TILE < height) ? tty * tiles_x + ttx : -1;
+    }
+    sm.tile_id = t;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (PREC) exp2_tab_load(sm.exp2tab);
   __syncthreads();
+  const int tile = sm.tile_id;
+  if (tile < 0) {  // a claim past the grid edge: no tile, but counted as finished
+    if (threadIdx.x == 0) atomicAdd(&fixup[FIX_DONE], 1);
+    return;
+  }
+  const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
+  const int nbatches = (int)((e - s + TB_BATCH - 1) / TB_BATCH);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
 
   if (warp == TB_CONSUMERS) {
@@ -738,7 +771,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       uint32_t g[TB_BATCH / 32];
 #pragma unroll
       for (int u = 0; u < TB_BATCH / 32; u++)
-        if (u < mine) g[u] = __ldg(entries + base + lane + 32 * u);
+        if (u < mine) g[u] = __ldcg(entries + base + lane + 32 * u);  // L2: written while the blend started
 #if HGS_TB_BULK
       // A/B: bulk copies take their operands in uniform registers, so the
       // compiler issues them one lane at a time (an elect loop of ~9
@@ -978,16 +1011,35 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
 __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
     const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
     int tiles_x, int n_tiles, int width, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
-    double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters) {
+    double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters, int* ready) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (counters && counters[2]) return;  // overflowed bins: the blend wrote nothing
   const int lane = threadIdx.x & 31;
   volatile int32_t* vf = fixup;
+  // n_tiles: blend CTAs to wait for.  The last warp to leave puts the
+  // counters (and the blend's tile-claim counter) back to 0: the queue is
+  // zero at rest, no reset launch sits between the binning and the blend.
+  struct Leave {
+    int32_t* f;
+    int* r;
+    int lane, nw;
+    __device__ ~Leave() {
+      if (lane == 0 && atomicAdd(&f[FIX_EXITED], 1) == nw - 1) {
+        f[FIX_RESERVED] = 0;
+        f[FIX_DONE] = 0;
+        f[FIX_CLAIMED] = 0;
+        f[FIX_EXITED] = 0;
+        if (r) r[1] = 0;
+        __threadfence();
+      }
+    }
+  } leave{fixup, ready, lane, (int)(gridDim.x * (blockDim.x >> 5))};
   while (true) {
     int idx = 0, quit = 0;
     if (lane == 0) {
       idx = atomicAdd(&fixup[FIX_CLAIMED], 1);
-      while (true) {
+      for (uint32_t spin = 0;; spin++) {
+        if (spin > QUEUE_SPIN_LIMIT) __trap();
         if (idx < vf[FIX_RESERVED]) break;  // a pixel is (or is being) queued in this slot
         if (vf[FIX_DONE] == n_tiles) {  // all tiles finished: the reservation count is final
           __threadfence();
@@ -1002,7 +1054,10 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
     idx = __shfl_sync(0xffffffffu, idx, 0);
     int32_t v = 0;
     if (lane == 0) {
-      while ((v = vf[FIX_SLOTS + idx]) == 0) __nanosleep(100);
+      for (uint32_t spin = 0; (v = vf[FIX_SLOTS + idx]) == 0; spin++) {
+        if (spin > QUEUE_SPIN_LIMIT) __trap();
+        __nanosleep(100);
+      }
       vf[FIX_SLOTS + idx] = 0;
     }
     const int64_t p = __shfl_sync(0xffffffffu, v, 0) - 1;
@@ -1047,9 +1102,14 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
 #ifndef HGS_BLEND_V1
 #define HGS_BLEND_V1 0
 #endif
+#ifndef HGS_BLEND_QUEUE
+#define HGS_BLEND_QUEUE 1
+#endif
   if (out->fixup && proj->cull && !HGS_FWD_EXACT) {
-    zero_pdl(st, out->fixup, (HGS_BLEND_V1 ? 1 : FIX_SLOTS) * sizeof(int32_t));
+#if HGS_BLEND_V1
+    zero_pdl(st, out->fixup, sizeof(int32_t));
     HGS_CHECK_LAUNCH();
+#endif
     const size_t smem = sizeof(FastSmem);
     static bool attr = false;
     if (!attr) {
@@ -1081,9 +1141,19 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     }
     auto fn = out->stats ? (prec ? blend_tile_kernel<true, true> : blend_tile_kernel<true, false>)
                          : (prec ? blend_tile_kernel<false, true> : blend_tile_kernel<false, false>);
-    launch_pdl(fn, dim3(n_tiles), dim3(TB_THREADS), tsmem, st, (const BlendRec*)proj->rec,
-               (const CullRec*)proj->cull, tiles->entries, tiles->tile_starts, tiles->tiles_x, width, height, ml,
-               bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
+    // binned tile grids: claim tiles from the fine binning's ready queue (at
+    // the scratch base, common.cuh), starting while the last quads are binned
+    const int ss = super_shift(tiles->tiles_x, tiles->tiles_y);
+    const bool queued = ss >= 0 && HGS_BLEND_QUEUE && tiles->ready != nullptr;
+    int* ready = queued ? reinterpret_cast<int*>(tiles->ready) : nullptr;
+    const int qs = queued ? ss - 2 : 0;
+    const int sxs = queued ? (tiles->tiles_x + (1 << ss) - 1) >> ss : 0;
+    const int sys = queued ? (tiles->tiles_y + (1 << ss) - 1) >> ss : 0;
+    const int n_cta = queued ? (sxs * sys << (2 * qs)) * 16 : n_tiles;
+    launch_pdl(fn, dim3(n_cta), dim3(TB_THREADS), tsmem, st, (const BlendRec*)proj->rec, (const CullRec*)proj->cull,
+               (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, width, height, ml,
+               bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
+               (const int64_t*)tiles->counters, ready, qs, sxs);
 #endif
     HGS_CHECK_LAUNCH();
 #if HGS_BLEND_V1
@@ -1097,9 +1167,9 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     // small CTAs (2 warps, ~11k registers): they fit beside the blend's
     // resident CTAs as soon as its last wave starts retiring
     launch_pdl(blend_exact_queue_kernel, dim3(8 * NUM_SMS), dim3(64), 0, st, (const BlendRec*)proj->rec,
-               (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_tiles, width, ml,
+               (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_cta, width, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
-               (const int64_t*)tiles->counters);
+               (const int64_t*)tiles->counters, ready);
 #endif
     HGS_CHECK_LAUNCH();
   } else {

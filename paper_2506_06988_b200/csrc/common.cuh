@@ -69,6 +69,28 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Tile binning <-> blend handoff (tiles.cu, blend.cu).  Tile grids of at
+// most BIN_MAX_SUPER super-tiles of 4x4 (or 8x8) tiles are binned per
+// super-tile block of 4x4 tiles ("quad"); each fine-binning CTA publishes its
+// quad in a ready queue (hgs_tiles.ready) as soon as its
+// entries are written, and the blend claims tiles in publication order, so
+// its first tiles start while the last quads are still being binned
+// (tile_counts_kernel empties the queue at every build; the bins and the
+// blend must get the same buffer).
+// ready[0]: quads published, ready[1]: tiles claimed, ready[2 + k]: quad + 1.
+constexpr int BIN_MAX_SUPER = 512;
+constexpr int READY_HDR = 2;
+constexpr int READY_MAX_QUADS = 4 * BIN_MAX_SUPER;
+static_assert(READY_HDR + READY_MAX_QUADS == HGS_READY_INTS, "hgs_tiles.ready size (hgs.h)");
+// smallest super-tile shift with at most BIN_MAX_SUPER super-tiles (or -1)
+__host__ __device__ inline int super_shift(int tiles_x, int tiles_y) {
+  for (int ss = 2; ss <= 3; ss++) {
+    const int sx = (tiles_x + (1 << ss) - 1) >> ss, sy = (tiles_y + (1 << ss) - 1) >> ss;
+    if (sx * sy <= BIN_MAX_SUPER) return ss;
+  }
+  return -1;
+}
+
 // SFU reciprocal estimate (rcp.approx.ftz: ~1 ulp); callers either refine it
 // or correct an integer quotient derived from it
 __device__ __forceinline__ float rcp_approx(float x) {

@@ -183,8 +183,14 @@ __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __rest
 // loads in flight together); preprocess re-zeroes the grids every frame.
 __global__ void __launch_bounds__(1024) tile_counts_kernel(int* __restrict__ diff, int tiles_x, int tiles_y,
                                                            int64_t capacity, int64_t* tile_starts, int64_t* counters,
-                                                           uint32_t* hist, int in_global) {
+                                                           uint32_t* hist, int in_global, int* ready,
+                                                           int publish_quads) {
   pdl_enter();
+  // the ready queue of the fine binning -> blend handoff starts empty; with
+  // no visible rows there is no fine binning: every quad is published here
+  if (ready)
+    for (int i = threadIdx.x; i < READY_HDR + READY_MAX_QUADS; i += blockDim.x)
+      ready[i] = i == 0 ? publish_quads : (i >= READY_HDR && i < READY_HDR + publish_quads ? i - READY_HDR + 1 : 0);
   extern __shared__ int g_smem[];  // (tiles_x + 1) x (tiles_y + 1)
   int* g = in_global ? diff : g_smem;
   __shared__ uint32_t sh[3][RADIX];
@@ -439,21 +445,13 @@ constexpr int BIN_THREADS = 256;
 constexpr int BIN_WARPS = BIN_THREADS / 32;
 constexpr int BIN_PG = 1024;                 // depth-ordered rows per partition
 constexpr int BIN_SUB = BIN_PG / BIN_WARPS;  // rows per warp
-constexpr int BIN_MAX_SUPER = 512;           // super-tile capacity (two per thread in the scans);
-                                              // loops run to the frame's super-tile count
+// BIN_MAX_SUPER (common.cuh): super-tile capacity (two per thread in the
+// scans); loops run to the frame's super-tile count
 static_assert(BIN_MAX_SUPER == 2 * BIN_THREADS, "coarse scans hold two super-tiles per thread");
 // warps per fine CTA (two CTAs per SM: the grid is one wave of super-tiles)
 __host__ __device__ constexpr int fine_warps(int S) { return S == 4 ? 16 : 8; }
 constexpr int FINE_DEPTH = 4;  // rounds of 32 list entries in flight per warp
 
-// smallest super-tile shift with at most BIN_MAX_SUPER super-tiles (or -1)
-__host__ __device__ inline int super_shift(int tiles_x, int tiles_y) {
-  for (int ss = 2; ss <= 3; ss++) {
-    const int sx = (tiles_x + (1 << ss) - 1) >> ss, sy = (tiles_y + (1 << ss) - 1) >> ss;
-    if (sx * sy <= BIN_MAX_SUPER) return ss;
-  }
-  return -1;
-}
 
 // tile id of the l-th tile (row-major) of a rectangle of width rw in a grid
 // of width gx
@@ -923,7 +921,7 @@ template <int S>
 __global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
     const uint32_t* __restrict__ crow, const ushort4* __restrict__ crect, const uint32_t* __restrict__ cstart,
     const int64_t* __restrict__ tile_starts, const int64_t* counters, int64_t capacity, int tiles_x, int tiles_y,
-    int sx, uint32_t* __restrict__ entries, int qs) {
+    int sx, uint32_t* __restrict__ entries, int qs, int* __restrict__ ready) {
   pdl_enter();
   constexpr int NT = S * S;
   using M = FineMask<S>;
@@ -1007,6 +1005,13 @@ __global__ void __launch_bounds__(fine_warps(S) * 32) fine_bin_kernel(
       }
     }
   }
+  // publish this quad: its tiles' entries are complete
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int k = atomicAdd(&ready[0], 1);
+    atomicExch(&ready[READY_HDR + k], (int)blockIdx.x + 1);
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -1059,6 +1064,17 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
     return base ? (void*)(base + o) : nullptr;
   };
   TilesScratch t{};
+  // the zeroed control block
+  const size_t ctl0 = off;
+  t.control_begin = base ? base + ctl0 : nullptr;
+  t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 3 * parts_k));
+  t.scan_status = (uint64_t*)take(sizeof(uint64_t) * (size_t)(2 * (parts_n + 1)));
+  t.hist = (uint32_t*)take(sizeof(uint32_t) * 11 * RADIX);
+  t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);  // [24..27]: depth key min/max (u64 x 2)
+  t.diff = (int*)take(sizeof(int) * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1));
+  const bool binned = (n_super_hint > 0 ? n_super_hint <= BIN_MAX_SUPER : super_shift(tiles_x, tiles_y) >= 0);
+  t.chist = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER) : nullptr;
+  t.control_bytes = off - ctl0;
   t.dk[0] = (uint64_t*)take(8 * nn);
   t.dk[1] = (uint64_t*)take(8 * nn);
   t.dv[0] = (uint32_t*)take(4 * nn);
@@ -1069,7 +1085,6 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.tk[1] = take(tkw * cc);
   t.tv0 = (uint32_t*)take(4 * cc);
   t.tv1 = (uint32_t*)take(4 * cc);
-  const bool binned = (n_super_hint > 0 ? n_super_hint <= BIN_MAX_SUPER : super_shift(tiles_x, tiles_y) >= 0);
   t.crow = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)cc) : nullptr;
   const size_t cparts = (size_t)(cc / CP_PART + 2);
   t.bin_mat = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER * cparts) : nullptr;
@@ -1082,15 +1097,6 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.npairs = binned ? (uint32_t*)take(sizeof(uint32_t) * 4) : nullptr;
   t.crect = binned ? (ushort4*)take(sizeof(ushort4) * (size_t)cc) : nullptr;
   t.cstart = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(BIN_MAX_SUPER + 1)) : nullptr;
-  const size_t ctl0 = off;
-  t.control_begin = base ? base + ctl0 : nullptr;
-  t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 3 * parts_k));
-  t.scan_status = (uint64_t*)take(sizeof(uint64_t) * (size_t)(2 * (parts_n + 1)));
-  t.hist = (uint32_t*)take(sizeof(uint32_t) * 11 * RADIX);
-  t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);  // [24..27]: depth key min/max (u64 x 2)
-  t.diff = (int*)take(sizeof(int) * (size_t)(tiles_x + 1) * (size_t)(tiles_y + 1));
-  t.chist = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER) : nullptr;
-  t.control_bytes = off - ctl0;
   t.parts_n = parts_n;
   t.parts_k = parts_k;
   if (s) *s = t;
@@ -1210,6 +1216,10 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     HGS_CHECK_LAUNCH();
   }
   // 2. per-tile counts -> tile_starts, K, overflow, tile-key histograms
+  const int ss_all = super_shift(tx, ty);
+  const int n_quads_all = ss_all >= 0 ? (((tx + (1 << ss_all) - 1) >> ss_all) * ((ty + (1 << ss_all) - 1) >> ss_all))
+                                            << (2 * (ss_all - 2))
+                                      : 0;
   const size_t grid_bytes = sizeof(int) * (size_t)(tx + 1) * (size_t)(ty + 1);
   const int tc_global = grid_bytes > 200 * 1024 ? 1 : 0;  // prefix sums in global memory for huge grids
   const size_t grid_smem = tc_global ? 0 : grid_bytes;
@@ -1219,7 +1229,8 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     tc_attr = true;
   }
   launch_pdl(tile_counts_kernel, dim3(1), dim3(1024), grid_smem, st, proj->tile_diff, tx, ty, tiles->capacity, tiles->tile_starts,
-                                                 tiles->counters, s.hist + 8 * RADIX, tc_global);
+                                                 tiles->counters, s.hist + 8 * RADIX, tc_global, (int*)tiles->ready,
+                                                 n == 0 && ss_all >= 0 ? n_quads_all : 0);
   HGS_CHECK_LAUNCH();
   if (n == 0) return HGS_OK;
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
@@ -1282,9 +1293,9 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                                                                           s.crow, s.crect);
     HGS_CHECK_LAUNCH();
     if (ss == 2 || ss == 3)  // 8x8 super-tiles: four 4x4-tile CTAs each (parallelism at 1080p)
-      launch_pdl(fine_bin_kernel<4>, dim3(n_super << (2 * (ss - 2))), dim3(fine_warps(4) * 32), 0, st, s.crow,
+        launch_pdl(fine_bin_kernel<4>, dim3(n_super << (2 * (ss - 2))), dim3(fine_warps(4) * 32), 0, st, s.crow,
                  s.crect, s.cstart, tiles->tile_starts, tiles->counters, tiles->capacity, tx, ty, sx, tiles->entries,
-                 ss - 2);
+                 ss - 2, (int*)tiles->ready);
     else
       return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large for binning");
     HGS_CHECK_LAUNCH();

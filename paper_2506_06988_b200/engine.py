@@ -87,6 +87,7 @@ class HybridRenderer:
         self.entries = torch.empty(capacity, dtype=torch.int32, device=self.dev)
         nbytes = _lib.load().hgs_tiles_scratch_bytes(len(self.gs), capacity, self.n_tiles)
         self.tiles_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        self.ready = torch.zeros(_lib.READY_INTS, dtype=torch.int32, device=self.dev)
         self.graph = None
 
     def set_camera(self, cam) -> None:
@@ -153,6 +154,7 @@ class HybridRenderer:
         ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tiles_x, self.tiles_y, TILE_PX, self.capacity
         ts.entries, ts.tile_starts, ts.counters = _lib.ptr(self.entries), _lib.ptr(self.tile_starts), _lib.ptr(self.counters)
         ts.scratch, ts.scratch_bytes = _lib.ptr(self.tiles_scratch), self.tiles_scratch.numel()
+        ts.ready = _lib.ptr(self.ready)
         return ps, ts
 
     def enqueue(self, rasterize_mesh: bool = True, mesh_layer: Optional[MeshLayer] = None) -> None:
@@ -250,7 +252,7 @@ class HybridRenderer:
 
     def tiles(self) -> TileBins:
         return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected(),
-                        counters=self.counters, capacity=int(self.entries.numel()))
+                        counters=self.counters, capacity=int(self.entries.numel()), ready=self.ready)
 
     def layer(self) -> Optional[MeshLayer]:
         if self.mesh is None:

@@ -134,8 +134,11 @@ class TileBins:
     ``entries_orig`` are the original Gaussian rows the kernels consume."""
 
     def __init__(self, tile_starts, entries_orig, tiles_x, tiles_y, tile_px, proj: Optional[ProjectedGaussians] = None,
-                 k: Optional[int] = None, counters: Optional[torch.Tensor] = None, capacity: Optional[int] = None):
+                 k: Optional[int] = None, counters: Optional[torch.Tensor] = None, capacity: Optional[int] = None,
+                 ready: Optional[torch.Tensor] = None):
         self.tile_starts = tile_starts
+        # the binning -> blend ready queue of these bins (hgs_tiles.ready)
+        self.ready = ready
         # the binning counters (M, K, overflow flag, ...) travel with the bins:
         # every consumer kernel returns early on an overflowed buffer instead
         # of reading entries past the capacity
@@ -179,6 +182,7 @@ class TileBins:
         s.capacity = capacity
         s.entries, s.tile_starts = _lib.ptr(self.entries_orig), _lib.ptr(self.tile_starts)
         s.counters = _lib.ptr(counters if counters is not None else self.counters)
+        s.ready = _lib.ptr(self.ready) if self.ready is not None else None
         return s
 
 
@@ -316,14 +320,16 @@ def _tiles_core(proj: ProjectedGaussians, width: int, height: int, tile_px: int,
     tile_starts = torch.empty(tx * ty + 1, dtype=torch.int64, device=dev)
     entries = torch.empty(cap, dtype=torch.int32, device=dev)
     counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    ready = torch.zeros(_lib.READY_INTS, dtype=torch.int32, device=dev)
     nbytes = _lib.load().hgs_tiles_scratch_bytes(proj.n, cap, tx * ty)
     scratch = SCRATCH.get("tiles", nbytes, dev)
     ts = _lib.HGSTiles()
     ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = tx, ty, tile_px, cap
     ts.entries, ts.tile_starts, ts.counters = _lib.ptr(entries), _lib.ptr(tile_starts), _lib.ptr(counters)
     ts.scratch, ts.scratch_bytes = _lib.ptr(scratch), scratch.numel()
+    ts.ready = _lib.ptr(ready)
     _lib.call("hgs_build_tiles", ctypes.byref(proj.struct()), proj.n, ctypes.byref(ts), _stream_ptr(dev))
-    return TileBins(tile_starts, entries, tx, ty, tile_px, proj, counters=counters, capacity=cap), counters
+    return TileBins(tile_starts, entries, tx, ty, tile_px, proj, counters=counters, capacity=cap, ready=ready), counters
 
 
 def build_tiles(proj: ProjectedGaussians, width: int, height: int, tile_px: int = TILE_PX) -> TileBins:

@@ -73,6 +73,7 @@ class _Lane:
         self.tile_starts = torch.empty(tx * ty + 1, dtype=torch.int64, device=self.dev)
         nbytes = _lib.load().hgs_tiles_scratch_bytes(n, cap, tx * ty)
         self.tiles_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        self.ready = torch.zeros(_lib.READY_INTS, dtype=torch.int32, device=self.dev)
 
 
 class HybridTrainer:
@@ -203,10 +204,11 @@ class HybridTrainer:
         ts.tiles_x, ts.tiles_y, ts.tile_px, ts.capacity = self.tx, self.ty, TILE_PX, lane.capacity
         ts.entries, ts.tile_starts, ts.counters = _lib.ptr(lane.entries), _lib.ptr(lane.tile_starts), _lib.ptr(lane.counters)
         ts.scratch, ts.scratch_bytes = _lib.ptr(lane.tiles_scratch), lane.tiles_scratch.numel()
+        ts.ready = _lib.ptr(lane.ready)
         _lib.call("hgs_build_tiles", ctypes.byref(proj.struct()), len(self.gs), ctypes.byref(ts), _stream_ptr(self.dev))
         lane.overflow += lane.counters[2:3]
         return TileBins(lane.tile_starts, lane.entries, self.tx, self.ty, TILE_PX, proj, counters=lane.counters,
-                        capacity=lane.capacity)
+                        capacity=lane.capacity, ready=lane.ready)
 
     def mesh_layer(self, v) -> Optional[MeshLayer]:
         """Texture lookup over the cached fragments (loop.py:189-199)."""

@@ -408,3 +408,36 @@ def test_device_matches_reference_fixture_at_scale(cfg, cuda_device):
         ri = d["row_idx"]
         for k in ("centers", "rotations", "log_scales", "logit_opacities", "colors_dc"):
             grad_close(np_(getattr(gr, k))[ri], d["g_" + k], atol=1e-4, scale_tol=1e-4, what=k)
+
+
+def test_binning_to_blend_handoff(cuda_device):
+    """The blend claims tiles from the fine binning's ready queue
+    (hgs_tiles.ready): the same bins blended twice, and blended without the
+    queue (the blend then waits for the whole binning, raster tile order),
+    give bit-identical images; a frame with no visible Gaussian publishes
+    every block itself (nothing to wait for)."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import splat
+    from paper_2506_06988_b200.splat import TileBins
+    d = load_golden("c1")
+    g, c, _ = dev_scene(*golden_scene(d))
+    w, h = int(c.width), int(c.height)
+    proj = splat.project(g, c)
+    tiles = splat.build_tiles(proj, w, h)
+    a, _, _ = splat.rasterize_forward(proj, tiles, w, h, (0.0, 0.0, 0.0))
+    b, _, _ = splat.rasterize_forward(proj, tiles, w, h, (0.0, 0.0, 0.0))
+    plain = TileBins(tiles.tile_starts, tiles.entries_orig, tiles.tiles_x, tiles.tiles_y, tiles.tile_px, proj,
+                     counters=tiles.counters, capacity=tiles.capacity, ready=None)
+    r, _, _ = splat.rasterize_forward(proj, plain, w, h, (0.0, 0.0, 0.0))
+    for x in (b, r):
+        assert torch.equal(a.color, x.color) and torch.equal(a.transmittance, x.transmittance)
+        assert torch.equal(a.depth.isnan(), x.depth.isnan())
+    # no visible row: behind the camera
+    far = hgs.GaussianSet.from_any(golden_scene(d)[0])
+    with torch.no_grad():
+        far.group("centers")[:, 2] = -1e3
+    p0 = splat.project(far, c)
+    t0 = splat.build_tiles(p0, w, h)
+    o0, _, _ = splat.rasterize_forward(p0, t0, w, h, (0.0, 0.0, 0.0))
+    torch.cuda.synchronize()
+    assert torch.all(o0.transmittance == 1.0)
