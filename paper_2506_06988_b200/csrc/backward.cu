@@ -57,7 +57,7 @@ struct BwSmem {
   unsigned long long full[BW_NSTAGE];
   unsigned long long empty[BW_NSTAGE];
   int4 list[BW_CONSUMERS][BW_BATCH];  // (slot index, blend cut, clamp cut, -) of the entries touching the sub-tile
-  double exp2tab[16];
+  double exp2tab[EXP2_N];
   int max_last;
 };
 

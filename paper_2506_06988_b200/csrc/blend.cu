@@ -65,7 +65,7 @@ struct FastSmem {
   unsigned long long full[NSTAGE];
   unsigned long long empty[NSTAGE];
   unsigned char list[CONSUMERS][BATCH];
-  double exp2tab[16];
+  double exp2tab[EXP2_N];
   int done_warps;
   int end_batch;
   unsigned long long stats[2];
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(FAST_THREADS, PREC ? HGS_FAST_MINB_PREC : HGS_
 #define HGS_TB_MINB 5
 #endif
 #ifndef HGS_TB_MINB_PREC
-#define HGS_TB_MINB_PREC 4
+#define HGS_TB_MINB_PREC 5
 #endif
 #ifndef HGS_TB_BULK
 #define HGS_TB_BULK 0
@@ -618,7 +618,7 @@ struct TileSmem {
   WalkRec walk[TB_CONSUMERS][TB_BATCH];
   unsigned long long full[TB_NSTAGE];
   unsigned long long empty[TB_NSTAGE];
-  double exp2tab[16];
+  double exp2tab[EXP2_N];
   int done_warps;
   int end_batch;
   int finished_warps;

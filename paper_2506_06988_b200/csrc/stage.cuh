@@ -152,45 +152,36 @@ __device__ __forceinline__ float ex2_neg(float u) {
 // forward, so the final T and the per-entry sigma it is built from must be
 // accurate far beyond fp32 for the gradients to hold the 1e-4 absolute
 // contract at |g| ~ 4e2 (measured: fp32 T / sigma leave 2.6e-4 at c3).
-// 2^-u in fp64, u >= 0: u = k/16 + r with k = floor(16 uu) from the fp32
-// argument (r in [-2^-20, 1/16)), 2^-r by a degree-5 Taylor polynomial
-// (|r ln2| < 0.0434: truncation < 1e-11 relative), 2^(-k/16) = table[k & 15]
-// x 2^-(k >> 4) (exact power of two).  The 16-entry table lives in shared
-// memory (128 B: one entry per bank pair, conflict-free).
-__constant__ double c_exp2_tab[16] = {1.0,
-                                      0.9576032806985737,
-                                      0.9170040432046712,
-                                      0.8781260801866497,
-                                      0.8408964152537145,
-                                      0.8052451659746271,
-                                      0.7711054127039704,
-                                      0.7384130729697497,
-                                      0.7071067811865476,
-                                      0.6771277734684463,
-                                      0.6484197773255048,
-                                      0.620928906036742,
-                                      0.5946035575013605,
-                                      0.5693943173783458,
-                                      0.5452538663326288,
-                                      0.5221368912137069};
+// 2^-u in fp64, u >= 0: u = k/N + r with k = floor(N uu) from the fp32
+// argument (r in [-2^-20, 1/N)), 2^-r by a Taylor polynomial, 2^(-k/N) =
+// table[k mod N] x 2^-(k / N) (an exact power of two, by the exponent field).
+// Table size N = 2^HGS_EXP2_BITS: 256 entries x a degree-3 Taylor polynomial
+// (default; 2 KB of shared memory), 64 x degree 4 or 16 x degree 5 -- all
+// < 3e-12 relative (c4 step: 162.6 vs 164.4 ms with 16 entries).  The
+// table (2^(-j/N), exact to 1 ulp from the device exp2) is built per CTA in
+// shared memory.
+#ifndef HGS_EXP2_BITS
+#define HGS_EXP2_BITS 8
+#endif
+constexpr int EXP2_BITS = HGS_EXP2_BITS;
+constexpr int EXP2_N = 1 << EXP2_BITS;
+constexpr int EXP2_DEG = EXP2_BITS <= 4 ? 5 : (EXP2_BITS <= 6 ? 4 : 3);
 __device__ __forceinline__ void exp2_tab_load(double* tab) {
-  if (threadIdx.x < 16) tab[threadIdx.x] = c_exp2_tab[threadIdx.x];
+  for (int j = threadIdx.x; j < EXP2_N; j += blockDim.x) tab[j] = exp2(-(double)j / EXP2_N);
 }
-// the polynomial's coefficients live in constant memory: DFMA reads them as
-// c[][] operands (as immediates every use costs two uniform moves)
+// the polynomial's coefficients ((-ln 2)^k / k!, highest first) live in
+// constant memory: DFMA reads them as c[][] operands (as immediates every use
+// costs two uniform moves)
 __constant__ double c_exp2_poly[6] = {-0.0013333558146428441, 0.009618129107628477, -0.055504108664821576,
                                       0.2402265069591007,     -0.6931471805599453,  1.0};
 __device__ __forceinline__ double exp2_neg64(double u, float uu, const double* tab) {
-  const int k = __float2int_rd(fminf(fmaxf(uu, 0.0f), 60.0f) * 16.0f);
-  const double r = fma((double)k, -0.0625, u);
-  double p = c_exp2_poly[0];
-  p = fma(p, r, c_exp2_poly[1]);
-  p = fma(p, r, c_exp2_poly[2]);
-  p = fma(p, r, c_exp2_poly[3]);
-  p = fma(p, r, c_exp2_poly[4]);
-  p = fma(p, r, c_exp2_poly[5]);
-  const double t = p * tab[k & 15];  // in (0.5, 1.03]: x 2^-(k >> 4) by the exponent field
-  return __hiloint2double(__double2hiint(t) - ((k >> 4) << 20), __double2loint(t));
+  const int k = __float2int_rd(fminf(fmaxf(uu, 0.0f), 60.0f) * (float)EXP2_N);
+  const double r = fma((double)k, -1.0 / EXP2_N, u);
+  double p = c_exp2_poly[5 - EXP2_DEG];
+#pragma unroll
+  for (int d = 6 - EXP2_DEG; d < 6; d++) p = fma(p, r, c_exp2_poly[d]);
+  const double t = p * tab[k & (EXP2_N - 1)];  // in (0.5, 1.03]: x 2^-(k >> BITS) by the exponent field
+  return __hiloint2double(__double2hiint(t) - ((k >> EXP2_BITS) << 20), __double2loint(t));
 }
 // 1 / x for x in [0.01, 1] in fp64: SFU estimate from the high word
 // (relative error < 2^-19) + one Newton step (< 2^-38: far below what the
