@@ -2,7 +2,13 @@
 // forward_kernel (splat/kernels.py:12-74), with the transmittance-mask
 // epilogue (train/losses.py:79-91).
 //
-// Fast path (blend_fast_kernel): one CTA per 16x16 tile, warp-specialised:
+// Production fast path: blend_tile_kernel (below; 2 pixels per lane, cut-form
+// decisions, per-warp walk buffers, tiles claimed from the binning's ready
+// queue) with blend_exact_queue_kernel draining the flagged pixels beside
+// it.  The round-1 kernel blend_fast_kernel is kept as the A/B baseline
+// (HGS_BLEND_V1=1):
+//
+// blend_fast_kernel: one CTA per 16x16 tile, warp-specialised:
 // 8 consumer warps each own an 8x4 sub-tile (one pixel per lane), 1
 // producer warp streams the tile's depth-sorted entry list through a
 // 2-stage shared-memory ring (128 entries x 112 B per stage: 64 B of the
