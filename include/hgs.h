@@ -197,6 +197,13 @@ int hgs_abi_version(void);
 int hgs_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 /* number of kernels this library has launched (or enqueued into a graph) */
 int64_t hgs_kernel_launches(void);
+/* CUDA-graph helpers (host layer): instantiate a captured cudaGraph_t, with
+   use_node_priority the kernel nodes keep the priority of the stream they
+   were captured from (cudaGraphInstantiateFlagUseNodePriority); launch;
+   destroy. */
+int hgs_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out);
+int hgs_graph_launch(void* exec, void* stream);
+int hgs_graph_exec_destroy(void* exec);
 
 /* ---------------- splat forward ---------------- */
 

@@ -98,6 +98,9 @@ SIGNATURES = {
     "hgs_abi_version": (ctypes.c_int, []),
     "hgs_device_info": (ctypes.c_int, [_P(c_i32), _P(c_i32), _P(c_i32)]),
     "hgs_kernel_launches": (c_i64, []),
+    "hgs_graph_instantiate": (ctypes.c_int, [c_void_p, c_i32, _P(c_void_p)]),
+    "hgs_graph_launch": (ctypes.c_int, [c_void_p, c_void_p]),
+    "hgs_graph_exec_destroy": (ctypes.c_int, [c_void_p]),
     "hgs_preprocess": (ctypes.c_int, [c_void_p, c_i32, c_i32, _P(HGSGaussians), c_i32, _P(HGSProjected), c_void_p]),
     "hgs_tiles_scratch_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i32]),
     "hgs_build_tiles": (ctypes.c_int, [_P(HGSProjected), c_i64, _P(HGSTiles), c_void_p]),

@@ -70,3 +70,29 @@ extern "C" int hgs_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc
   if (cc_minor) *cc_minor = v;
   return HGS_OK;
 }
+
+// CUDA-graph helpers for the host layer: instantiate a captured graph so that
+// its kernel nodes run at the priority of the stream they were captured from
+// (the frame's Gaussian chain on a high-priority stream, the mesh branch on
+// a normal one: when both want SMs, the critical path gets them first).
+extern "C" int hgs_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out) {
+  if (!graph || !exec_out) return hgs_set_error(HGS_ERR_INVALID, "hgs_graph_instantiate: null argument");
+  cudaGraphExec_t ex = nullptr;
+  const unsigned long long flags = use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
+  cudaError_t e = cudaGraphInstantiateWithFlags(&ex, (cudaGraph_t)graph, flags);
+  if (e != cudaSuccess) return hgs_set_cuda_error(e, __FILE__, __LINE__);
+  *exec_out = (void*)ex;
+  return HGS_OK;
+}
+
+extern "C" int hgs_graph_launch(void* exec, void* stream) {
+  if (!exec) return hgs_set_error(HGS_ERR_INVALID, "hgs_graph_launch: null graph");
+  cudaError_t e = cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream);
+  if (e != cudaSuccess) return hgs_set_cuda_error(e, __FILE__, __LINE__);
+  return HGS_OK;
+}
+
+extern "C" int hgs_graph_exec_destroy(void* exec) {
+  if (exec) cudaGraphExecDestroy((cudaGraphExec_t)exec);
+  return HGS_OK;
+}

@@ -88,6 +88,7 @@ class HybridRenderer:
         nbytes = _lib.load().hgs_tiles_scratch_bytes(len(self.gs), capacity, self.n_tiles)
         self.tiles_scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         self.ready = torch.zeros(_lib.READY_INTS, dtype=torch.int32, device=self.dev)
+        self._drop_exec()
         self.graph = None
 
     def set_camera(self, cam) -> None:
@@ -128,7 +129,7 @@ class HybridRenderer:
         if self._snap_ev[k] is not None:
             main.wait_event(self._snap_ev[k])  # the previous D2H from this snapshot is done
         self.set_camera(cam)
-        self.graph.replay()
+        self.replay()
         pairs = [(out_color, self.color, self._snap[k][0]), (out_depth, self.depth, self._snap[k][1]),
                  (out_trans, self.trans, self._snap[k][2])]
         pairs = [p for p in pairs if p[0] is not None]
@@ -170,12 +171,22 @@ class HybridRenderer:
         w, h = self.width, self.height
         ml = _lib.HGSMeshLayer()
         joined = None
-        if self.mesh is not None and mesh_layer is None:
+        side_branch = self.mesh is not None and mesh_layer is None
+        if side_branch:
             if self._side is None:
                 self._side = torch.cuda.Stream(self.dev)
                 self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
             self._ev_fork.record(main)
             self._side.wait_event(self._ev_fork)
+        elif mesh_layer is not None:
+            ml = mesh_layer.struct()
+        # the Gaussian chain (the critical path) is enqueued first, so that in
+        # the captured graph its nodes launch ahead of the mesh branch
+        ps, ts = self._structs()
+        _lib.check(L.hgs_preprocess(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.gs.struct()), TILE_PX,
+                                    ctypes.byref(ps), st), "preprocess")
+        _lib.check(L.hgs_build_tiles(ctypes.byref(ps), len(self.gs), ctypes.byref(ts), st), "build_tiles")
+        if side_branch:
             side = self._side.cuda_stream
             if rasterize_mesh:
                 fr = _lib.HGSFragments()
@@ -190,12 +201,6 @@ class HybridRenderer:
             self._ev_join.record(self._side)
             joined = self._ev_join
             ml.color, ml.depth, ml.triangle_id = _lib.ptr(self.mesh_color), _lib.ptr(self.frag_depth), _lib.ptr(self.frag_tri)
-        elif mesh_layer is not None:
-            ml = mesh_layer.struct()
-        ps, ts = self._structs()
-        _lib.check(L.hgs_preprocess(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.gs.struct()), TILE_PX,
-                                    ctypes.byref(ps), st), "preprocess")
-        _lib.check(L.hgs_build_tiles(ctypes.byref(ps), len(self.gs), ctypes.byref(ts), st), "build_tiles")
         out = _lib.HGSBlendOut()
         out.color, out.depth, out.transmittance = _lib.ptr(self.color), _lib.ptr(self.depth), _lib.ptr(self.trans)
         out.final_t, out.last = _lib.ptr(self.final_t), _lib.ptr(self.last)
@@ -231,19 +236,44 @@ class HybridRenderer:
 
     # CUDA graph of one frame (camera read from cam_dev at replay time) --------
     def capture(self, rasterize_mesh: bool = True) -> None:
-        s = torch.cuda.Stream(self.dev)
+        """Capture one frame into a CUDA graph.  The Gaussian chain
+        (preprocess -> binning -> blend) is captured from a high-priority
+        stream and the mesh branch from a normal one, and the graph is
+        instantiated with per-node priorities (hgs_graph_instantiate): when
+        the two branches compete for SMs, the critical path's CTAs are
+        scheduled first.  HGS_GRAPH_PRIO=0 instantiates without priorities."""
+        import os
+        prio = os.environ.get("HGS_GRAPH_PRIO", "1") != "0"
+        s = torch.cuda.Stream(self.dev, priority=-1 if prio else 0)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
             self.enqueue(rasterize_mesh)  # warm (lazy attributes, occupancy queries)
         torch.cuda.current_stream(self.dev).wait_stream(s)
         torch.cuda.synchronize(self.dev)
-        g = torch.cuda.CUDAGraph()
+        self._drop_exec()
+        g = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(g, stream=s):
             self.enqueue(rasterize_mesh)
-        self.graph = g
+        ex = ctypes.c_void_p()
+        _lib.call("hgs_graph_instantiate", ctypes.c_void_p(int(g.raw_cuda_graph())), 1 if prio else 0,
+                  ctypes.byref(ex))
+        self.graph, self._exec = g, ex
+
+    def _drop_exec(self) -> None:
+        ex = getattr(self, "_exec", None)
+        if ex is not None and ex.value:
+            torch.cuda.synchronize(self.dev)
+            _lib.call("hgs_graph_exec_destroy", ex)
+        self._exec = None
+
+    def __del__(self):
+        try:
+            self._drop_exec()
+        except Exception:
+            pass
 
     def replay(self) -> None:
-        self.graph.replay()
+        _lib.call("hgs_graph_launch", self._exec, torch.cuda.current_stream(self.dev).cuda_stream)
 
     # views for the API / backward ----------------------------------------
     def projected(self) -> ProjectedGaussians:
