@@ -78,6 +78,8 @@ class HybridRenderer:
         self.capacity = 0
         self._alloc_entries(capacity if capacity is not None else 16 * n)
         self.graph = None
+        self._exec = self._exec_alt = None
+        self._alt_out = None
         self._side = None
 
     # ------------------------------------------------------------------
@@ -108,43 +110,49 @@ class HybridRenderer:
 
     def render_to_host(self, cam, out_color: torch.Tensor, out_depth: Optional[torch.Tensor] = None,
                        out_trans: Optional[torch.Tensor] = None) -> torch.cuda.Event:
-        """Serving path: camera H2D, one replay of the frame graph, device
-        snapshots of the colour image (and, when given, the depth and
-        transmittance images -- the reference's RenderOutputs) and their D2H
-        into the pinned host tensors (H x W x 3 / H x W fp32) on a copy
-        stream, so the transfer overlaps the next frame.  Snapshots are
-        double-buffered.  Returns the event that marks the copies complete
-        (the caller must not reuse the host tensors before)."""
+        """Serving path: camera H2D, one graph replay, and the D2H of the
+        colour image (and, when given, the depth and transmittance images --
+        the reference's RenderOutputs) into the pinned host tensors (H x W x 3
+        / H x W fp32) on a copy stream, so the transfer overlaps the next
+        frame.  Two frame graphs alternate between two sets of output images
+        (no device-side snapshot copies): frame i+1 renders into the set frame
+        i is not copying out of.  Returns the event that marks the copies
+        complete (the caller must not reuse the host tensors before)."""
         if self.graph is None:
             self.capture()
         if getattr(self, "_copy", None) is None:
             self._copy = torch.cuda.Stream(self.dev)
-            self._snap = [(torch.empty_like(self.color), torch.empty_like(self.depth), torch.empty_like(self.trans))
-                          for _ in range(2)]
             self._snap_ev = [None, None]
             self._snap_k = 0
+        if self._alt_out is None:
+            self._alt_out = (torch.empty_like(self.color), torch.empty_like(self.depth), torch.empty_like(self.trans))
+        if self._exec_alt is None:
+            self.capture(out_set=1)
         k = self._snap_k
         self._snap_k ^= 1
         main = torch.cuda.current_stream(self.dev)
         if self._snap_ev[k] is not None:
-            main.wait_event(self._snap_ev[k])  # the previous D2H from this snapshot is done
+            main.wait_event(self._snap_ev[k])  # the previous D2H out of this output set is done
         self.set_camera(cam)
-        self.replay()
-        pairs = [(out_color, self.color, self._snap[k][0]), (out_depth, self.depth, self._snap[k][1]),
-                 (out_trans, self.trans, self._snap[k][2])]
-        pairs = [p for p in pairs if p[0] is not None]
-        for _, src, snap in pairs:
-            snap.copy_(src, non_blocking=True)
+        self.replay(out_set=k)
+        dev_out = self._out3(k)
+        pairs = [(out_color, dev_out[0]), (out_depth, dev_out[1]), (out_trans, dev_out[2])]
         ready = torch.cuda.Event()
         ready.record(main)
         self._copy.wait_event(ready)
         with torch.cuda.stream(self._copy):
-            for host, _, snap in pairs:
-                host.copy_(snap, non_blocking=True)
+            for host, src in pairs:
+                if host is not None:
+                    host.copy_(src, non_blocking=True)
         done = torch.cuda.Event()
         done.record(self._copy)
         self._snap_ev[k] = done
         return done
+
+    def _out3(self, out_set: int):
+        """(colour, depth, transmittance) device images of output set 0 (the
+        public ones) or 1 (the serving path's second set)."""
+        return (self.color, self.depth, self.trans) if out_set == 0 else self._alt_out
 
     def _structs(self):
         ps = _lib.HGSProjected()
@@ -158,7 +166,7 @@ class HybridRenderer:
         ts.ready = _lib.ptr(self.ready)
         return ps, ts
 
-    def enqueue(self, rasterize_mesh: bool = True, mesh_layer: Optional[MeshLayer] = None) -> None:
+    def enqueue(self, rasterize_mesh: bool = True, mesh_layer: Optional[MeshLayer] = None, out_set: int = 0) -> None:
         """Enqueue one frame for the camera currently in cam_dev.
 
         The mesh layer (raster + texture fetch) does not depend on the
@@ -202,7 +210,8 @@ class HybridRenderer:
             joined = self._ev_join
             ml.color, ml.depth, ml.triangle_id = _lib.ptr(self.mesh_color), _lib.ptr(self.frag_depth), _lib.ptr(self.frag_tri)
         out = _lib.HGSBlendOut()
-        out.color, out.depth, out.transmittance = _lib.ptr(self.color), _lib.ptr(self.depth), _lib.ptr(self.trans)
+        oc, od, ot = self._out3(out_set)
+        out.color, out.depth, out.transmittance = _lib.ptr(oc), _lib.ptr(od), _lib.ptr(ot)
         out.final_t, out.last = _lib.ptr(self.final_t), _lib.ptr(self.last)
         variant, k = 0, 20.0
         if self.mask is not None:
@@ -235,36 +244,43 @@ class HybridRenderer:
                 return
 
     # CUDA graph of one frame (camera read from cam_dev at replay time) --------
-    def capture(self, rasterize_mesh: bool = True) -> None:
-        """Capture one frame into a CUDA graph.  The Gaussian chain
-        (preprocess -> binning -> blend) is captured from a high-priority
-        stream and the mesh branch from a normal one, and the graph is
-        instantiated with per-node priorities (hgs_graph_instantiate): when
-        the two branches compete for SMs, the critical path's CTAs are
-        scheduled first.  HGS_GRAPH_PRIO=0 instantiates without priorities."""
+    def capture(self, rasterize_mesh: bool = True, out_set: int = 0) -> None:
+        """Capture one frame into a CUDA graph (out_set: which output images
+        it writes, see render_to_host).  The Gaussian chain (preprocess ->
+        binning -> blend) is captured from a high-priority stream and the mesh
+        branch from a normal one, and the graph is instantiated with per-node
+        priorities (hgs_graph_instantiate): when the two branches compete for
+        SMs, the critical path's CTAs are scheduled first.  HGS_GRAPH_PRIO=0
+        instantiates without priorities."""
         import os
         prio = os.environ.get("HGS_GRAPH_PRIO", "1") != "0"
         s = torch.cuda.Stream(self.dev, priority=-1 if prio else 0)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
-            self.enqueue(rasterize_mesh)  # warm (lazy attributes, occupancy queries)
+            self.enqueue(rasterize_mesh, out_set=out_set)  # warm (lazy attributes, occupancy queries)
         torch.cuda.current_stream(self.dev).wait_stream(s)
         torch.cuda.synchronize(self.dev)
-        self._drop_exec()
+        self._drop_exec(out_set)
         g = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(g, stream=s):
-            self.enqueue(rasterize_mesh)
+            self.enqueue(rasterize_mesh, out_set=out_set)
         ex = ctypes.c_void_p()
         _lib.call("hgs_graph_instantiate", ctypes.c_void_p(int(g.raw_cuda_graph())), 1 if prio else 0,
                   ctypes.byref(ex))
-        self.graph, self._exec = g, ex
+        if out_set == 0:
+            self.graph, self._exec = g, ex
+        else:
+            self._graph_alt, self._exec_alt = g, ex
 
-    def _drop_exec(self) -> None:
-        ex = getattr(self, "_exec", None)
-        if ex is not None and ex.value:
-            torch.cuda.synchronize(self.dev)
-            _lib.call("hgs_graph_exec_destroy", ex)
-        self._exec = None
+    def _drop_exec(self, out_set: Optional[int] = None) -> None:
+        """Destroy the instantiated graph(s) of one output set (None: both)."""
+        for k in ((0, 1) if out_set is None else (out_set,)):
+            name = "_exec" if k == 0 else "_exec_alt"
+            ex = getattr(self, name, None)
+            if ex is not None and ex.value:
+                torch.cuda.synchronize(self.dev)
+                _lib.call("hgs_graph_exec_destroy", ex)
+            setattr(self, name, None)
 
     def __del__(self):
         try:
@@ -272,8 +288,9 @@ class HybridRenderer:
         except Exception:
             pass
 
-    def replay(self) -> None:
-        _lib.call("hgs_graph_launch", self._exec, torch.cuda.current_stream(self.dev).cuda_stream)
+    def replay(self, out_set: int = 0) -> None:
+        _lib.call("hgs_graph_launch", self._exec if out_set == 0 else self._exec_alt,
+                  torch.cuda.current_stream(self.dev).cuda_stream)
 
     # views for the API / backward ----------------------------------------
     def projected(self) -> ProjectedGaussians:
