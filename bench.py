@@ -281,7 +281,7 @@ def run_ours(args):
     host_imgs = [(torch.empty(H, W, 3, dtype=torch.float32).pin_memory(),
                   torch.empty(H, W, dtype=torch.float32).pin_memory(),
                   torch.empty(H, W, dtype=torch.float32).pin_memory()) for _ in range(2)]
-    for i in range(2):  # warm the copy stream / snapshots
+    for i in range(2):  # warm the copy stream and the second frame graph
         r.render_to_host(cam, *host_imgs[i])
     torch.cuda.synchronize()
     e2e_0, e2e_1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
