@@ -174,8 +174,11 @@ __device__ __forceinline__ void exp2_tab_load(double* tab) {
 // costs two uniform moves)
 __constant__ double c_exp2_poly[6] = {-0.0013333558146428441, 0.009618129107628477, -0.055504108664821576,
                                       0.2402265069591007,     -0.6931471805599453,  1.0};
+// Callers pass blended entries only: 0 <= u < 9 U (a tiny negative u, from
+// rounding, gives k = -1 and still the right value: the table index wraps and
+// the exponent step is -1), so the argument needs no clamp.
 __device__ __forceinline__ double exp2_neg64(double u, float uu, const double* tab) {
-  const int k = __float2int_rd(fminf(fmaxf(uu, 0.0f), 60.0f) * (float)EXP2_N);
+  const int k = __float2int_rd(uu * (float)EXP2_N);
   const double r = fma((double)k, -1.0 / EXP2_N, u);
   double p = c_exp2_poly[5 - EXP2_DEG];
 #pragma unroll
