@@ -138,6 +138,9 @@ typedef struct hgs_tiles {
   int32_t* ready;       /* device int32[HGS_READY_INTS] or NULL: hgs_build_tiles publishes each finished block of
                            4x4 tiles here and hgs_blend_forward claims tiles in that order, starting while the
                            last blocks are still being binned (NULL: the blend waits for the whole binning) */
+  void* join_event;     /* cudaEvent_t or NULL: hgs_build_tiles makes its last (fine binning) kernel wait for it.
+                           Joins an independent branch the blend needs (the mesh layer) there, so that the blend
+                           itself has the fine binning as its only dependency and can start programmatically */
 } hgs_tiles;
 #define HGS_READY_INTS (2 + 2048)
 

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <vector>
 
 namespace {
 thread_local char g_last_error[512] = "";
@@ -75,8 +76,61 @@ extern "C" int hgs_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc
 // its kernel nodes run at the priority of the stream they were captured from
 // (the frame's Gaussian chain on a high-priority stream, the mesh branch on
 // a normal one: when both want SMs, the critical path gets them first).
+const void* hgs_fine_bin_fn();
+bool hgs_is_blend_tile_fn(const void* f);
+
+// The blend's dependencies in a captured frame graph: the fine binning
+// (programmatic: the blend claims the quads it publishes, ready queue) and,
+// when a mesh branch is joined right before it, the mesh branch's last
+// kernel.  Capture makes that second edge programmatic too, but in queue mode
+// the blend never waits on its grid dependencies (no griddepcontrol.wait), so
+// the mesh layer's writes would not be guaranteed visible: make every
+// non-fine dependency of the blend a full one.  (HGS_GRAPH_DEBUG prints the
+// edges.)  Returns the number of edges changed.
+static int fix_blend_edges(cudaGraph_t g) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess || n == 0) return 0;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return 0;
+  const void* fine = hgs_fine_bin_fn();
+  static const bool dbg = std::getenv("HGS_GRAPH_DEBUG") != nullptr;
+  auto kfunc = [](cudaGraphNode_t nd) -> const void* {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return nullptr;
+    cudaKernelNodeParams kp{};
+    if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) return nullptr;
+    return kp.func;
+  };
+  int changed = 0;
+  for (cudaGraphNode_t nd : nodes) {
+    if (!hgs_is_blend_tile_fn(kfunc(nd))) continue;
+    size_t nd_deps = 0;
+    if (cudaGraphNodeGetDependencies_v2(nd, nullptr, nullptr, &nd_deps) != cudaSuccess || nd_deps == 0) continue;
+    std::vector<cudaGraphNode_t> deps(nd_deps);
+    std::vector<cudaGraphEdgeData> ed(nd_deps);
+    if (cudaGraphNodeGetDependencies_v2(nd, deps.data(), ed.data(), &nd_deps) != cudaSuccess) continue;
+    for (size_t i = 0; i < nd_deps; i++) {
+      const bool is_fine = kfunc(deps[i]) == fine;
+      if (dbg)
+        std::fprintf(stderr, "blend dep %zu: %s, edge type %d port %d\n", i, is_fine ? "fine binning" : "other",
+                     (int)ed[i].type, (int)ed[i].from_port);
+      if (is_fine || ed[i].type == cudaGraphDependencyTypeDefault) continue;
+      const cudaGraphEdgeData full{};
+      if (cudaGraphRemoveDependencies_v2(g, &deps[i], &nd, &ed[i], 1) != cudaSuccess) continue;
+      if (cudaGraphAddDependencies_v2(g, &deps[i], &nd, &full, 1) != cudaSuccess) {
+        cudaGraphAddDependencies_v2(g, &deps[i], &nd, &ed[i], 1);
+        continue;
+      }
+      changed++;
+    }
+  }
+  cudaGetLastError();
+  return changed;
+}
+
 extern "C" int hgs_graph_instantiate(void* graph, int32_t use_node_priority, void** exec_out) {
   if (!graph || !exec_out) return hgs_set_error(HGS_ERR_INVALID, "hgs_graph_instantiate: null argument");
+  fix_blend_edges((cudaGraph_t)graph);
   cudaGraphExec_t ex = nullptr;
   const unsigned long long flags = use_node_priority ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
   cudaError_t e = cudaGraphInstantiateWithFlags(&ex, (cudaGraph_t)graph, flags);

@@ -1081,6 +1081,13 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
 
 }  // namespace hgs
 
+// Is f one of the blend kernels that consume the fine binning's ready queue?
+bool hgs_is_blend_tile_fn(const void* f) {
+  using namespace hgs;
+  return f == (const void*)blend_tile_kernel<false, false> || f == (const void*)blend_tile_kernel<true, false> ||
+         f == (const void*)blend_tile_kernel<false, true> || f == (const void*)blend_tile_kernel<true, true>;
+}
+
 extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* tiles, int32_t width, int32_t height,
                                  const hgs_mesh_layer* mesh, const double* bg_host3, int32_t mask_variant,
                                  double mask_k, hgs_blend_out* out, void* stream) {

@@ -1175,6 +1175,10 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
 
 }  // namespace hgs
 
+// The fine binning kernel's entry point (hgs_graph_instantiate restores its
+// programmatic edge to the blend, abi.cu)
+const void* hgs_fine_bin_fn() { return (const void*)hgs::fine_bin_kernel<4>; }
+
 extern "C" size_t hgs_tiles_scratch_bytes(int64_t n, int64_t capacity, int32_t n_tiles) {
   // n_tiles is an upper bound on tiles_x * tiles_y; size the difference grid
   // for the worst aspect ratio (tiles_x + 1) * (tiles_y + 1) <= 2 * n_tiles + 1
@@ -1232,7 +1236,12 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                                                  tiles->counters, s.hist + 8 * RADIX, tc_global, (int*)tiles->ready,
                                                  n == 0 && ss_all >= 0 ? n_quads_all : 0);
   HGS_CHECK_LAUNCH();
-  if (n == 0) return HGS_OK;
+  auto join = [&]() -> int {  // the caller's independent branch joins the stream (hgs.h join_event)
+    if (!tiles->join_event) return HGS_OK;
+    const cudaError_t e = cudaStreamWaitEvent(st, (cudaEvent_t)tiles->join_event, 0);
+    return e == cudaSuccess ? HGS_OK : hgs_set_cuda_error(e, __FILE__, __LINE__);
+  };
+  if (n == 0) return join();
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
   // order-preserving remap of the depth keys to DEPTH_KEY_BITS, LSD passes, exact fix-up of truncation ties
   uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
@@ -1292,12 +1301,12 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     launch_pdl(coarse_scatter_kernel, dim3(sgrid), dim3(BIN_THREADS), ssmem, st, ca, s.bin_mat, s.bin_slot, s.bin_wmat,
                                                                           s.crow, s.crect);
     HGS_CHECK_LAUNCH();
-    if (ss == 2 || ss == 3)  // 8x8 super-tiles: four 4x4-tile CTAs each (parallelism at 1080p)
-        launch_pdl(fine_bin_kernel<4>, dim3(n_super << (2 * (ss - 2))), dim3(fine_warps(4) * 32), 0, st, s.crow,
-                 s.crect, s.cstart, tiles->tile_starts, tiles->counters, tiles->capacity, tx, ty, sx, tiles->entries,
-                 ss - 2, (int*)tiles->ready);
-    else
-      return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large for binning");
+    if (ss != 2 && ss != 3) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large for binning");
+    if (const int jr = join()) return jr;  // before the fine binning: the blend then depends on it alone
+    // 8x8 super-tiles: four 4x4-tile CTAs each (parallelism at 1080p)
+    launch_pdl(fine_bin_kernel<4>, dim3(n_super << (2 * (ss - 2))), dim3(fine_warps(4) * 32), 0, st, s.crow,
+               s.crect, s.cstart, tiles->tile_starts, tiles->counters, tiles->capacity, tx, ty, sx, tiles->entries,
+               ss - 2, (int*)tiles->ready);
     HGS_CHECK_LAUNCH();
     return HGS_OK;
   }
@@ -1337,5 +1346,6 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
                               tiles->counters + 1, tiles->capacity, 0, tpasses, s.hist + 8 * RADIX, true, rs_tile_status,
                               s.parts_k, s.part_ctr + 8, st, nullptr, false);
   }
+  if (rc == HGS_OK) rc = join();
   return rc;
 }

@@ -12,7 +12,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 sc = syn.make_config(cfg, seed=0)
 g = hgs.GaussianSet.from_any(sc.gaussians); m = hgs.TexturedMesh.from_any(sc.mesh)
 c = hgs.Camera.from_any(sc.cameras[0])
-r = HybridRenderer(g, m, c.width, c.height)
+r = HybridRenderer(g, None if os.environ.get("NOMESH") else m, c.width, c.height)
 r.frame(c, sync_check=True)
 r.capture()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
