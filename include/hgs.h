@@ -276,6 +276,14 @@ int hgs_sample_texture(const float* texture, int32_t th, int32_t tw, const doubl
    grad_texture (Ht x Wt x 3 fp32). */
 int hgs_texture_backward(const double* uv, const int32_t* triangle_id, const float* grad_image, int64_t npix,
                          int32_t th, int32_t tw, float* grad_texture, void* stream);
+/* Deterministic texture_backward for accumulation over many views: adds the
+   taps' contributions into acc (int64[th*tw*3], zero at start) as 2^-32 fixed
+   point -- integer atomics, so the sum is independent of their order.
+   hgs_fixed_to_float converts acc to fp32 (out = value, or out += value with
+   accumulate) and zeroes acc. */
+int hgs_texture_backward_fixed(const double* uv, const int32_t* triangle_id, const float* grad_image, int64_t npix,
+                               int32_t th, int32_t tw, int64_t* acc, void* stream);
+int hgs_fixed_to_float(int64_t* acc, int64_t n, float* out, int32_t accumulate, void* stream);
 
 /* ---------------- losses (train/losses.py) ---------------- */
 

@@ -118,6 +118,9 @@ SIGNATURES = {
                                                ctypes.c_size_t, c_void_p]),
     "hgs_sample_texture": (ctypes.c_int, [c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "hgs_texture_backward": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i32, c_i32, c_void_p, c_void_p]),
+    "hgs_texture_backward_fixed": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i32, c_i32, c_void_p,
+                                                  c_void_p]),
+    "hgs_fixed_to_float": (ctypes.c_int, [c_void_p, c_i64, c_void_p, c_i32, c_void_p]),
     "hgs_transmittance_mask": (ctypes.c_int, [c_void_p, c_i64, c_f64, c_i32, c_void_p, c_void_p]),
     "hgs_loss_scratch_bytes": (ctypes.c_size_t, [c_i32, c_i32]),
     "hgs_composite_loss": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_f64,

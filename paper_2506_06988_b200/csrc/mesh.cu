@@ -15,6 +15,8 @@
 // CTA each (binned by the one-thread-per-triangle pass).
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace hgs {
 
 constexpr int SMALL_TRI_PIXELS = 32;
@@ -294,6 +296,43 @@ __global__ void __launch_bounds__(256) texture_backward_kernel(const double* __r
   }
 }
 
+// Deterministic variant: each tap's contribution rounded to a 2^-32 grid and
+// added as a 64-bit integer (two's complement wraps correctly for negative
+// values): integer addition is associative, so the sum does not depend on
+// the order of the atomics (|sum| < 2^31, resolution 2.3e-10 per tap -- finer
+// than fp32 accumulation at any texel value above 4e-3).
+constexpr double TEX_FIXED_SCALE = 4294967296.0;  // 2^32
+__global__ void __launch_bounds__(256) texture_backward_fixed_kernel(const double* __restrict__ uv,
+                                                                     const int32_t* __restrict__ tri,
+                                                                     const float* __restrict__ grad, int64_t npix,
+                                                                     int th, int tw,
+                                                                     unsigned long long* __restrict__ acc) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npix || tri[p] < 0) return;
+  const double2 uvp = reinterpret_cast<const double2*>(uv)[p];
+  const Taps t = texel_taps(uvp.x, uvp.y, th, tw);
+  const double g0 = grad[3 * p], g1 = grad[3 * p + 1], g2 = grad[3 * p + 2];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    unsigned long long* tp = acc + 3 * t.i[k];
+    atomicAdd(tp, (unsigned long long)__double2ll_rn(g0 * t.w[k] * TEX_FIXED_SCALE));
+    atomicAdd(tp + 1, (unsigned long long)__double2ll_rn(g1 * t.w[k] * TEX_FIXED_SCALE));
+    atomicAdd(tp + 2, (unsigned long long)__double2ll_rn(g2 * t.w[k] * TEX_FIXED_SCALE));
+  }
+}
+
+// fixed-point accumulator -> fp32 (out = value, or out += value), and the
+// accumulator back to zero
+__global__ void __launch_bounds__(256) fixed_to_float_kernel(unsigned long long* __restrict__ acc, int64_t n,
+                                                             float* __restrict__ out, int accumulate) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = (float)((double)(long long)acc[i] * (1.0 / TEX_FIXED_SCALE));
+    out[i] = accumulate ? out[i] + v : v;
+    acc[i] = 0ull;
+  }
+}
+
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace hgs
@@ -376,6 +415,27 @@ extern "C" int hgs_texture_backward(const double* uv, const int32_t* triangle_id
   if (npix == 0) return HGS_OK;
   hgs::texture_backward_kernel<<<hgs::ceil_div(npix, 256), 256, 0, (cudaStream_t)stream>>>(
       uv, triangle_id, grad_image, npix, th, tw, grad_texture);
+  HGS_CHECK_LAUNCH();
+  return HGS_OK;
+}
+
+extern "C" int hgs_texture_backward_fixed(const double* uv, const int32_t* triangle_id, const float* grad_image,
+                                          int64_t npix, int32_t th, int32_t tw, int64_t* acc, void* stream) {
+  if (!uv || !triangle_id || !grad_image || !acc)
+    return hgs_set_error(HGS_ERR_INVALID, "hgs_texture_backward_fixed: null argument");
+  if (th <= 0 || tw <= 0) return hgs_set_error(HGS_ERR_INVALID, "hgs_texture_backward_fixed: empty texture");
+  if (npix == 0) return HGS_OK;
+  hgs::texture_backward_fixed_kernel<<<hgs::ceil_div(npix, 256), 256, 0, (cudaStream_t)stream>>>(
+      uv, triangle_id, grad_image, npix, th, tw, (unsigned long long*)acc);
+  HGS_CHECK_LAUNCH();
+  return HGS_OK;
+}
+
+extern "C" int hgs_fixed_to_float(int64_t* acc, int64_t n, float* out, int32_t accumulate, void* stream) {
+  if (!acc || !out) return hgs_set_error(HGS_ERR_INVALID, "hgs_fixed_to_float: null argument");
+  if (n <= 0) return HGS_OK;
+  const int blocks = (int)std::min<int64_t>(hgs::ceil_div(n, 256), 8 * hgs::NUM_SMS);
+  hgs::fixed_to_float_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((unsigned long long*)acc, n, out, accumulate);
   HGS_CHECK_LAUNCH();
   return HGS_OK;
 }

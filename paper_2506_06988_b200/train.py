@@ -149,6 +149,11 @@ class HybridTrainer:
         o = p_sz + t_sz
         self.grads = GradBuffer(gs, self.bucket[:p_sz], self.bucket[o:o + n], self.bucket[o + n:o + 2 * n])
         self.tex_grad = self.bucket[p_sz:p_sz + t_sz].view_as(mesh.texture) if t_sz else None
+        # the views' texture gradients meet in a 2^-32 fixed-point accumulator
+        # (integer atomics: order-independent, so the step is run-to-run
+        # reproducible), converted into tex_grad once per step
+        if t_sz and getattr(self, "tex_acc", None) is None:
+            self.tex_acc = torch.zeros(t_sz, dtype=torch.int64, device=dev)
 
     def _alloc_rows(self):
         """Per-view work buffers sized by the Gaussian count, one set per
@@ -248,8 +253,9 @@ class HybridTrainer:
             lane.chain_done = torch.cuda.Event()
             lane.chain_done.record(torch.cuda.current_stream(self.dev))
         if layer is not None and self.tex_grad is not None:
-            from .meshraster import texture_backward
-            texture_backward(fr, mesh_grad, tuple(self.mesh.texture.shape[:2]), out=self.tex_grad)
+            th, tw = (int(x) for x in self.mesh.texture.shape[:2])
+            _lib.call("hgs_texture_backward_fixed", _lib.ptr(fr.uv), _lib.ptr(fr.triangle_id), _lib.ptr(mesh_grad),
+                      fr.triangle_id.numel(), th, tw, _lib.ptr(self.tex_acc), _stream_ptr(self.dev))
         return bd.scalars
 
     def step(self, it: int, views: Sequence[int]) -> torch.Tensor:
@@ -284,8 +290,13 @@ class HybridTrainer:
         for lane in self.lanes[1:]:
             overflow = overflow + lane.overflow
         if int(overflow.item()):
+            if self.tex_grad is not None:
+                self.tex_acc.zero_()  # discard the partial texture sums of the failed pass
             self._size_entries()
             return self.step(it, views)
+        if self.tex_grad is not None:
+            _lib.call("hgs_fixed_to_float", _lib.ptr(self.tex_acc), self.tex_acc.numel(), _lib.ptr(self.tex_grad), 0,
+                      _stream_ptr(self.dev))
         for lane in self.lanes:
             self.loss_sum += lane.loss_sum
         if self.world > 1:
