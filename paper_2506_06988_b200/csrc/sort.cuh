@@ -5,7 +5,7 @@
 //
 // Radix pass: 256 threads x IPT items per partition (the depth sort uses
 // IPT = 8: 2048 keys, 3 passes over 24-bit keys).  Ranking is
-// warp-level multisplit (__match_any_sync) with per-warp digit counters in
+// warp-level multisplit (8 ballots per key) with per-warp digit counters in
 // shared memory, which preserves input order inside a partition (stability);
 // partitions are ordered by their dynamically assigned id, and the look-back
 // over predecessor partitions gives each digit's global offset.  Items are
@@ -117,6 +117,20 @@ __device__ __forceinline__ void chained_scan_partition(int part, int64_t n, F va
   __syncthreads();
 }
 
+// Lanes of `active` holding the same BITS-bit value v: one ballot per bit
+// (MATCH.ANY on a warp of mostly distinct values is a long-latency
+// multi-pass instruction; this is BITS votes + selects)
+template <int BITS>
+__device__ __forceinline__ unsigned warp_peers(uint32_t v, unsigned active) {
+  unsigned peers = active;
+#pragma unroll
+  for (int b = 0; b < BITS; b++) {
+    const unsigned bb = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+    peers &= ((v >> b) & 1u) ? bb : ~bb;
+  }
+  return peers;
+}
+
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
   return (uint32_t)((k >> shift) & (K)(RADIX - 1));
@@ -182,6 +196,7 @@ __global__ void __launch_bounds__(RSCAN_DIGITS * RSCAN_GROUPS) radix_scan_kernel
                                                                                 int tile, uint32_t* __restrict__ pcnt) {
   __shared__ uint32_t s_sum[RSCAN_GROUPS][RSCAN_DIGITS + 1];
   __shared__ uint32_t s_base[RSCAN_DIGITS];
+  pdl_enter();
   int64_t n = count_ptr ? *count_ptr : cap;
   if (n > cap) n = cap;
   const int nparts = (int)((n + tile - 1) / tile);
@@ -232,7 +247,8 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
                                                                 const int64_t* count_ptr, int64_t cap, int shift,
                                                                 const uint32_t* __restrict__ hist, uint32_t* status,
                                                                 int nparts_cap, uint32_t* part_ctr, int write_keys,
-                                                                const uint32_t* __restrict__ poff = nullptr) {
+                                                                const uint32_t* __restrict__ poff = nullptr,
+                                                                uint32_t* __restrict__ pcnt_next = nullptr) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RadixSmem<K, IPT>& sm = *reinterpret_cast<RadixSmem<K, IPT>*>(smem_raw);
@@ -282,9 +298,9 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
       const bool valid = li < tile_n;
       const unsigned active = __ballot_sync(0xffffffffu, valid);
       uint32_t d = 0, peers = 0, base_cnt = 0;
+      if (valid) d = digit_of<K>(k[j], shift);
+      peers = warp_peers<8>(d, active);
       if (valid) {
-        d = digit_of<K>(k[j], shift);
-        peers = __match_any_sync(active, d);
         base_cnt = whist[warp][d];
         rank[j] = base_cnt + __popc(peers & lanemask_lt());
       }
@@ -365,6 +381,9 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
       const uint32_t out = s_gstart[d] + (uint32_t)i - s_lstart[d];
       if (write_keys) kout[out] = key;
       vout[out] = sm.vals[i];
+      // reduce-then-scan: the next pass's per-partition digit counts, so that
+      // pass needs no upsweep over its input
+      if (pcnt_next) atomicAdd(&pcnt_next[(size_t)(out / TILE) * RADIX + digit_of<K>(key, shift + 8)], 1u);
     }
     __syncthreads();
   }

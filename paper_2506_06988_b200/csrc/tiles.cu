@@ -29,6 +29,9 @@
 // of the bins skip their work; the caller grows the buffer and re-runs.
 #include "sort.cuh"
 
+#ifndef HGS_FIXUP_V2
+#define HGS_FIXUP_V2 1
+#endif
 #ifndef HGS_PREP_3K
 #define HGS_PREP_3K 0
 #endif
@@ -97,6 +100,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
 // order of keys that collide after the shift is restored by
 // depth_fixup_kernel (1M keys: ~1e4 short runs).
 constexpr int DEPTH_KEY_BITS = 24;
+// depth sort partition (radix_pass_kernel<uint32_t, 8>: 256 threads x 8 keys)
+constexpr int RS_DEPTH_IPT = 8;
+constexpr int RS_PART = RS_THREADS * RS_DEPTH_IPT;
+// HGS_SORT_RTS=1: reduce-then-scan depth passes (every pass counts the next
+// pass's per-partition digits as it scatters; a scan kernel turns them into
+// offsets) instead of the onesweep decoupled look-back
+#ifndef HGS_SORT_RTS
+#define HGS_SORT_RTS 1
+#endif
 __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
   const unsigned long long lo = ~minmax[0], hi = minmax[1];
   const unsigned long long range = hi > lo ? hi - lo : 0;
@@ -108,20 +120,46 @@ __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
 // (hist: DEPTH_KEY_BITS / 8 x 256, zeroed), in the same read.
 __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __restrict__ keys, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax,
-                                                          uint32_t* __restrict__ k32, uint32_t* __restrict__ hist) {
+                                                          uint32_t* __restrict__ k32, uint32_t* __restrict__ hist,
+                                                          uint32_t* __restrict__ pcnt0) {
   pdl_enter();
   constexpr int NP = DEPTH_KEY_BITS / 8;
   __shared__ uint32_t sh_h[NP][256];
   for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) (&sh_h[0][0])[i] = 0;
+  __shared__ uint32_t sh_part[256];
   __syncthreads();
   const int64_t m = counters[0];
   const unsigned long long lo = ~minmax[0];
   const int sh = depth_shift(minmax);
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = (uint32_t)((keys[j] - lo) >> sh);
-    k32[j] = k;
+  if (pcnt0) {
+    // reduce-then-scan sort: also the first pass's per-partition digit counts
+    // (partitions of RS_PART keys, one per CTA iteration)
+    const int64_t nparts = (m + RS_PART - 1) / RS_PART;
+    for (int64_t part = blockIdx.x; part < nparts; part += gridDim.x) {
+      sh_part[threadIdx.x] = 0;
+      __syncthreads();
 #pragma unroll
-    for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
+      for (int u = 0; u < RS_PART / 256; u++) {
+        const int64_t j = part * RS_PART + u * 256 + threadIdx.x;
+        if (j < m) {
+          const uint32_t k = (uint32_t)((keys[j] - lo) >> sh);
+          k32[j] = k;
+#pragma unroll
+          for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
+          atomicAdd(&sh_part[k & 255u], 1u);
+        }
+      }
+      __syncthreads();
+      pcnt0[part * RADIX + threadIdx.x] = sh_part[threadIdx.x];
+      __syncthreads();
+    }
+  } else {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+      const uint32_t k = (uint32_t)((keys[j] - lo) >> sh);
+      k32[j] = k;
+#pragma unroll
+      for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) {
@@ -133,8 +171,109 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
 // After the stable 32-bit sort, rows with equal truncated keys are in row
 // order; the reference order is (fp64 depth, row): re-sort each such run by
 // the full 64-bit depth key (runs are rare and short; long runs of exactly
-// equal depths are already ordered and only verified).
+// equal depths are already ordered and only verified).  One CTA per chunk of
+// FIX_CHUNK sorted positions: the chunk's keys are staged in shared memory,
+// its run starts listed, then one thread per run: runs of up to FIX_SHORT
+// rows are loaded at once (rows, then their full keys) and sorted in
+// registers, longer ones by a Shell sort in place.
+constexpr int FIX_CHUNK = 2048, FIX_SHORT = 8;
 __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ rows,
+                                                          const uint64_t* __restrict__ sort_keys, const int64_t* counters,
+                                                          const unsigned long long* __restrict__ minmax) {
+  pdl_enter();
+  __shared__ uint32_t sk[FIX_CHUNK + 2];  // [0]: the key before the chunk, [FIX_CHUNK + 1]: the one after
+  __shared__ int s_run[FIX_CHUNK / 2];     // run starts of the chunk (chunk offsets)
+  __shared__ int s_nrun;
+  const int64_t m = counters[0];
+  if (depth_shift(minmax) == 0) return;  // keys were exact
+  // full keys by row from the 8-byte sort_keys array (the fp64 depth bit
+  // pattern preprocess wrote; L2-resident) rather than the 80-byte records
+  auto key64 = [&](uint32_t row) { return (unsigned long long)__ldg(sort_keys + row); };
+  for (int64_t base = (int64_t)blockIdx.x * FIX_CHUNK; base < m; base += (int64_t)gridDim.x * FIX_CHUNK) {
+    if (threadIdx.x == 0) s_nrun = 0;
+    for (int i = threadIdx.x; i < FIX_CHUNK + 2; i += blockDim.x) {
+      const int64_t j = base + i - 1;
+      sk[i] = (j >= 0 && j < m) ? __ldcg(k32 + j) : 0u;
+    }
+    __syncthreads();
+    // the chunk's run starts first, so that the runs are then handled in
+    // parallel (one thread each) rather than one position stride at a time
+    for (int i = threadIdx.x; i < FIX_CHUNK; i += blockDim.x) {
+      const int64_t j = base + i;
+      if (j >= m) break;
+      const uint32_t kj = sk[i + 1];
+      if (j > 0 && sk[i] == kj) continue;            // not a run start
+      if (j + 1 >= m || sk[i + 2] != kj) continue;   // singleton
+      s_run[atomicAdd(&s_nrun, 1)] = i;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int ri = threadIdx.x; ri < s_nrun; ri += blockDim.x) {
+      const int i = s_run[ri];
+      const int64_t j = base + i;
+      const uint32_t kj = sk[i + 1];
+      int64_t e = j + 1;
+      while (e < m && (e - base + 1 <= FIX_CHUNK ? sk[e - base + 1] : __ldcg(k32 + e)) == kj) e++;
+      const int64_t len = e - j;
+      if (len <= FIX_SHORT) {
+        uint32_t r[FIX_SHORT];
+        unsigned long long kk[FIX_SHORT];
+#pragma unroll
+        for (int t = 0; t < FIX_SHORT; t++) r[t] = t < len ? rows[j + t] : 0xffffffffu;
+#pragma unroll
+        for (int t = 0; t < FIX_SHORT; t++) kk[t] = t < len ? key64(r[t]) : ~0ull;
+        bool sorted = true;
+#pragma unroll
+        for (int t = 1; t < FIX_SHORT; t++) sorted = sorted && (kk[t - 1] < kk[t] || (kk[t - 1] == kk[t] && r[t - 1] < r[t]));
+        if (sorted) continue;
+        // odd-even transposition sort by (key, row); padding (~0, ~0) stays last
+#pragma unroll
+        for (int rd = 0; rd < FIX_SHORT; rd++)
+#pragma unroll
+          for (int t = rd & 1; t + 1 < FIX_SHORT; t += 2) {
+            const bool sw = kk[t] > kk[t + 1] || (kk[t] == kk[t + 1] && r[t] > r[t + 1]);
+            const unsigned long long ka = sw ? kk[t + 1] : kk[t], kb = sw ? kk[t] : kk[t + 1];
+            const uint32_t ra = sw ? r[t + 1] : r[t], rb = sw ? r[t] : r[t + 1];
+            kk[t] = ka, kk[t + 1] = kb, r[t] = ra, r[t + 1] = rb;
+          }
+#pragma unroll
+        for (int t = 0; t < FIX_SHORT; t++)
+          if (t < len) rows[j + t] = r[t];
+        continue;
+      }
+      bool sorted = true;
+      for (int64_t t = j + 1; t < e && sorted; t++) {
+        const unsigned long long a = key64(rows[t - 1]), b = key64(rows[t]);
+        sorted = a < b || (a == b && rows[t - 1] < rows[t]);
+      }
+      if (sorted) continue;
+      // Shell sort by (key64, row): correct for any run length
+      for (int64_t gap = len / 2; gap > 0; gap /= 2)
+        for (int64_t t = j + gap; t < e; t++) {
+          const uint32_t rr = rows[t];
+          const unsigned long long kr = key64(rr);
+          int64_t u = t;
+          while (u >= j + gap) {
+            const uint32_t ru = rows[u - gap];
+            const unsigned long long ku = key64(ru);
+            if (ku < kr || (ku == kr && ru < rr)) break;
+            rows[u] = ru;
+            u -= gap;
+          }
+          rows[u] = rr;
+        }
+    }
+    __syncthreads();
+  }
+}
+
+#if !HGS_FIXUP_V2
+// round-1 fix-up (A/B baseline): one thread per sorted position
+// After the stable 32-bit sort, rows with equal truncated keys are in row
+// order; the reference order is (fp64 depth, row): re-sort each such run by
+// the full 64-bit depth key (runs are rare and short; long runs of exactly
+// equal depths are already ordered and only verified).
+__global__ void __launch_bounds__(256) depth_fixup_v1_kernel(const uint32_t* __restrict__ k32, uint32_t* __restrict__ rows,
                                                           const uint64_t* __restrict__ sort_keys, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax) {
   pdl_enter();
@@ -173,6 +312,8 @@ __global__ void __launch_bounds__(256) depth_fixup_kernel(const uint32_t* __rest
       }
   }
 }
+
+#endif
 
 // Per-tile counts from the difference grid (2D inclusive prefix sums, in
 // shared memory), the CSR starts (exclusive scan), K, the overflow flag, and
@@ -866,7 +1007,8 @@ __global__ void __launch_bounds__(BIN_THREADS) coarse_scatter_kernel(CoarseArgs 
     __syncthreads();
     walk_pairs(k, P, m, a.pair_off, a.rsort, a.sorted_rows, a.wstart, a.ss, a.sx, lane,
                [&](bool valid, uint32_t sti, uint32_t g, ushort4 rc) {
-                 const unsigned peers = __match_any_sync(0xffffffffu, sti);
+                 static_assert(BIN_MAX_SUPER <= 512, "super-tile index: 9 bits");
+                 const unsigned peers = warp_peers<9>(sti, __ballot_sync(0xffffffffu, valid));
                  uint32_t cur = 0;
                  if (valid) cur = cnt[warp * nsp + sti];
                  __syncwarp();
@@ -1025,7 +1167,8 @@ struct TilesScratch {
   uint32_t* tv0;
   uint32_t* tv1;
   // zeroed control block
-  uint32_t* rs_status;    // 8 depth passes x parts_n x 256, then 3 tile passes x parts_k x 256
+  uint32_t* rs_status;    // 3 depth passes x 2 parts_n (2048-key partitions) x 256
+  uint32_t* rs_tile_status;  // 3 tile passes x parts_k x 256 (outside the zeroed block: zeroed only when used)
   uint64_t* scan_status;  // 2 x (parts_n + 1)
   uint32_t* hist;         // 10 x 256
   uint32_t* part_ctr;     // 32
@@ -1067,7 +1210,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   // the zeroed control block
   const size_t ctl0 = off;
   t.control_begin = base ? base + ctl0 : nullptr;
-  t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(8 * parts_n + 3 * parts_k));
+  t.rs_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(3 * 2 * parts_n));
   t.scan_status = (uint64_t*)take(sizeof(uint64_t) * (size_t)(2 * (parts_n + 1)));
   t.hist = (uint32_t*)take(sizeof(uint32_t) * 11 * RADIX);
   t.part_ctr = (uint32_t*)take(sizeof(uint32_t) * 32);  // [24..27]: depth key min/max (u64 x 2)
@@ -1075,6 +1218,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   const bool binned = (n_super_hint > 0 ? n_super_hint <= BIN_MAX_SUPER : super_shift(tiles_x, tiles_y) >= 0);
   t.chist = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER) : nullptr;
   t.control_bytes = off - ctl0;
+  t.rs_tile_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(3 * parts_k));
   t.dk[0] = (uint64_t*)take(8 * nn);
   t.dk[1] = (uint64_t*)take(8 * nn);
   t.dv[0] = (uint32_t*)take(4 * nn);
@@ -1128,11 +1272,15 @@ static int persistent_grid(const void* fn, int threads, size_t smem) {
 // pcnt != nullptr: reduce-then-scan passes (upsweep counts, one scan CTA,
 // rank + scatter from precomputed offsets; pcnt holds parts x 256 words)
 // instead of the single-pass decoupled look-back.
+// counted: reduce-then-scan without upsweeps -- status holds npasses x parts
+// x 256 count words, zero except the first pass's, which the
+// caller wrote (depth_remap_kernel); each pass counts the next one's as it
+// scatters, and radix_scan_kernel turns a pass's counts into offsets.
 template <typename K, int IPT = RS_IPT>
 static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_vals, const int64_t* count_ptr,
                       int64_t cap, int shift0, int npasses, uint32_t* hist, bool hist_ready, uint32_t* status,
                       int64_t parts, uint32_t* part_ctr, cudaStream_t st, K** keys_result, bool last_keys,
-                      uint32_t** vals_result = nullptr, uint32_t* pcnt = nullptr) {
+                      uint32_t** vals_result = nullptr, uint32_t* pcnt = nullptr, bool counted = false) {
   const size_t smem = sizeof(RadixSmem<K, IPT>);
   static int grid = 0;
   if (grid == 0) {
@@ -1153,16 +1301,31 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
   for (int p = 0; p < npasses; p++) {
     const bool last = p == npasses - 1;
     uint32_t* vdst = last && final_vals ? final_vals : vout;
-    if (pcnt) {
+    uint32_t* poff = nullptr;
+    uint32_t* pnext = nullptr;
+    if (counted) {
+      // counted reduce-then-scan: pass p's counts were written by the
+      // previous kernel (pass 0: the caller) into status[p]; scan them into
+      // offsets in place, count pass p + 1's digits while scattering
+      poff = status + (size_t)p * parts * RADIX;
+      pnext = last ? nullptr : status + (size_t)(p + 1) * parts * RADIX;
+      // (16 CTAs: a one-CTA-per-digit scan was 47 us / frame slower in the
+      // chain although faster alone -- its CTAs, scheduled early by PDL,
+      // hold SM slots while the previous pass runs)
+      launch_pdl(radix_scan_kernel, dim3(RADIX / RSCAN_DIGITS), dim3(RSCAN_DIGITS * RSCAN_GROUPS), 0, st,
+                 (const uint32_t*)(hist + RADIX * p), count_ptr, cap, (int)tile, poff);
+      HGS_CHECK_LAUNCH();
+    } else if (pcnt) {
       radix_upsweep_kernel<K, IPT><<<(int)parts, RS_THREADS, 0, st>>>(kin, count_ptr, cap, shift0 + 8 * p, pcnt);
       HGS_CHECK_LAUNCH();
       radix_scan_kernel<<<RADIX / RSCAN_DIGITS, RSCAN_DIGITS * RSCAN_GROUPS, 0, st>>>(hist + RADIX * p, count_ptr, cap,
                                                                                  (int)tile, pcnt);
       HGS_CHECK_LAUNCH();
+      poff = pcnt;
     }
     launch_pdl(radix_pass_kernel<K, IPT>, dim3(g), dim3(RS_THREADS), smem, st, kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
-                                                      hist + RADIX * p, status + (size_t)p * parts * RADIX, (int)parts,
-                                                      part_ctr + p, (!last || last_keys) ? 1 : 0, pcnt);
+                                                      (const uint32_t*)(hist + RADIX * p), status + (size_t)p * parts * RADIX, (int)parts,
+                                                      part_ctr + p, (!last || last_keys) ? 1 : 0, (const uint32_t*)poff, pnext);
     HGS_CHECK_LAUNCH();
     std::swap(kin, kout);
     vin = vdst;
@@ -1247,15 +1410,23 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
   uint32_t* k32b = k32a + (n > 0 ? n : 1);
   unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
-  launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, s.dk[0], tiles->counters, minmax, k32a, s.hist);
+  const bool rts = HGS_SORT_RTS != 0;
+  launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, s.dk[0], tiles->counters, minmax, k32a, s.hist,
+             rts ? s.rs_status : (uint32_t*)nullptr);
   HGS_CHECK_LAUNCH();
   uint32_t* k32res = nullptr;
   uint32_t* rows = nullptr;  // visible rows in (depth, row) order
-  int rc = radix_sort<uint32_t, 8>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0,
-                                   DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr, st,
-                                   &k32res, true, &rows);
+  int rc = radix_sort<uint32_t, RS_DEPTH_IPT>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0,
+                                              DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr, st,
+                                              &k32res, true, &rows, nullptr, rts);
   if (rc) return rc;
-  launch_pdl(depth_fixup_kernel, dim3(4 * sm_count()), dim3(256), 0, st, k32res, rows, (const uint64_t*)proj->sort_keys, tiles->counters,
+  launch_pdl(
+#if HGS_FIXUP_V2
+      depth_fixup_kernel,
+#else
+      depth_fixup_v1_kernel,
+#endif
+      dim3(4 * sm_count()), dim3(256), 0, st, k32res, rows, (const uint64_t*)proj->sort_keys, tiles->counters,
                                                      minmax);
   HGS_CHECK_LAUNCH();
   const int ss = super_shift(tx, ty);
@@ -1319,8 +1490,10 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   int bits = 1;
   while ((1 << bits) < n_tiles) bits++;
   const int tpasses = (bits + 7) / 8;
-  uint32_t* rs_tile_status = s.rs_status + (size_t)8 * s.parts_n * RADIX;
+  uint32_t* rs_tile_status = s.rs_tile_status;
   if (tpasses > 3) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: more than 2^24 tiles");
+  zero_pdl(st, rs_tile_status, sizeof(uint32_t) * RADIX * (size_t)tpasses * s.parts_k);
+  HGS_CHECK_LAUNCH();
   if (n_tiles > 65535) {
     emit_kernel<uint32_t><<<4 * sm_count(), 256, 0, st>>>(rows, s.offsets, (const ushort4*)proj->rect,
                                                           tiles->counters, tx, tiles->capacity, (uint32_t*)s.tk[0],
