@@ -234,6 +234,13 @@ __global__ void __launch_bounds__(RSCAN_DIGITS * RSCAN_GROUPS) radix_scan_kernel
   }
 }
 
+// 16-byte global -> shared copy; bytes < 16 zero-fills the rest (0: none read)
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+
 template <typename K, int IPT = RS_IPT>
 struct RadixSmem {
   K keys[RS_THREADS * IPT];
@@ -281,16 +288,32 @@ __global__ void __launch_bounds__(RS_THREADS, IPT <= 8 ? 4 : (sizeof(K) == 8 ? 2
     const int64_t base = (int64_t)part * TILE;
     const int tile_n = (int)tmin<int64_t>(TILE, n - base);
 
+    // the partition's keys and values are staged in shared memory with
+    // every copy in flight at once (loaded into registers directly, ptxas
+    // sinks the loads into the ranking loop under the 64-register cap and
+    // pays the L2 latency item by item)
+    {
+      constexpr int KV = 16 / (int)sizeof(K);
+      for (int c = tid; c < TILE / KV; c += RS_THREADS) {
+        const int nv = tile_n - c * KV;
+        cp_async16_zfill(&sm.keys[c * KV], kin + base + (nv > 0 ? c * KV : 0), nv <= 0 ? 0u : (unsigned)(min(nv, KV) * sizeof(K)));
+      }
+      if (vin)  // (NULL: the values are the input positions)
+        for (int c = tid; c < TILE / 4; c += RS_THREADS) {
+          const int nv = tile_n - c * 4;
+          cp_async16_zfill(&sm.vals[c * 4], vin + base + (nv > 0 ? c * 4 : 0), nv <= 0 ? 0u : (unsigned)(min(nv, 4) * 4));
+        }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
     K k[IPT];
     uint32_t v[IPT];
     uint32_t rank[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; j++) {
       const int li = warp * (IPT * 32) + j * 32 + lane;
-      if (li < tile_n) {
-        k[j] = kin[base + li];
-        v[j] = vin[base + li];
-      }
+      k[j] = sm.keys[li];
+      v[j] = vin ? sm.vals[li] : (uint32_t)(base + li);
     }
 #pragma unroll
     for (int j = 0; j < IPT; j++) {

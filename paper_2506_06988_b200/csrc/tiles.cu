@@ -93,6 +93,48 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
   }
 }
 
+// HGS_SORT_ALL: no compaction -- every row's key is sorted, the culled rows
+// (key ~0) with the reserved largest 24-bit key, so they end up behind the
+// M visible rows in the sorted order.  This kernel only gathers what the
+// compaction did on the side: M and the min / max of the visible keys.
+__global__ void __launch_bounds__(256) depth_stats_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                                          int64_t* counters, unsigned long long* minmax) {
+  pdl_enter();
+  __shared__ unsigned long long s_min[8], s_max[8];
+  __shared__ long long s_cnt[8];
+  unsigned long long nmin = 0, kmax = 0;
+  long long cnt = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; j < n; j += 2 * stride) {
+    uint64_t k0, k1;
+    if (j + 1 < n) {
+      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + j));
+      k0 = v.x, k1 = v.y;
+    } else {
+      k0 = keys[j], k1 = ~0ull;
+    }
+    if (k0 != ~0ull) { nmin = max(nmin, (unsigned long long)~k0); kmax = max(kmax, (unsigned long long)k0); cnt++; }
+    if (k1 != ~0ull) { nmin = max(nmin, (unsigned long long)~k1); kmax = max(kmax, (unsigned long long)k1); cnt++; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nmin = max(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_min[warp] = nmin, s_max[warp] = kmax, s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; w++) nmin = max(nmin, s_min[w]), kmax = max(kmax, s_max[w]), cnt += s_cnt[w];
+    if (cnt) {
+      atomicMax(&minmax[0], nmin);
+      atomicMax(&minmax[1], kmax);
+      atomicAdd((unsigned long long*)&counters[0], (unsigned long long)cnt);
+    }
+  }
+}
+
 // Depth keys -> DEPTH_KEY_BITS bits, order preserving: (bits - min) >> shift, where
 // shift drops the low bits the visible range does not need.  Equal 32-bit
 // keys from distinct fp64 depths are re-ordered exactly by depth_fixup_kernel.
@@ -100,6 +142,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
 // order of keys that collide after the shift is restored by
 // depth_fixup_kernel (1M keys: ~1e4 short runs).
 constexpr int DEPTH_KEY_BITS = 24;
+constexpr uint32_t KEY_CULLED = (1u << DEPTH_KEY_BITS) - 1;
+#ifndef HGS_SORT_ALL
+#define HGS_SORT_ALL 1
+#endif
 // depth sort partition (radix_pass_kernel<uint32_t, 8>: 256 threads x 8 keys)
 constexpr int RS_DEPTH_IPT = 8;
 constexpr int RS_PART = RS_THREADS * RS_DEPTH_IPT;
@@ -113,7 +159,9 @@ __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
   const unsigned long long lo = ~minmax[0], hi = minmax[1];
   const unsigned long long range = hi > lo ? hi - lo : 0;
   const int bits = range ? 64 - __clzll((long long)range) : 0;
-  return bits > DEPTH_KEY_BITS ? bits - DEPTH_KEY_BITS : 0;
+  int sh = bits > DEPTH_KEY_BITS ? bits - DEPTH_KEY_BITS : 0;
+  if (HGS_SORT_ALL && (range >> sh) >= KEY_CULLED) sh++;  // the top key is reserved for culled rows
+  return sh;
 }
 
 // ... and the digit histograms of the remapped keys for the LSD passes
@@ -121,16 +169,21 @@ __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
 __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __restrict__ keys, const int64_t* counters,
                                                           const unsigned long long* __restrict__ minmax,
                                                           uint32_t* __restrict__ k32, uint32_t* __restrict__ hist,
-                                                          uint32_t* __restrict__ pcnt0) {
+                                                          uint32_t* __restrict__ pcnt0, int64_t nkeys) {
   pdl_enter();
   constexpr int NP = DEPTH_KEY_BITS / 8;
   __shared__ uint32_t sh_h[NP][256];
   for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) (&sh_h[0][0])[i] = 0;
   __shared__ uint32_t sh_part[256];
   __syncthreads();
-  const int64_t m = counters[0];
+  // nkeys >= 0 (HGS_SORT_ALL): every row's key, culled rows (~0) -> the
+  // reserved key KEY_CULLED (depth_shift keeps the visible ones below it)
+  const int64_t m = nkeys >= 0 ? nkeys : counters[0];
   const unsigned long long lo = ~minmax[0];
   const int sh = depth_shift(minmax);
+  auto remap = [&](uint64_t key) -> uint32_t {
+    return (nkeys >= 0 && key == ~0ull) ? KEY_CULLED : (uint32_t)((key - lo) >> sh);
+  };
   if (pcnt0) {
     // reduce-then-scan sort: also the first pass's per-partition digit counts
     // (partitions of RS_PART keys, one per CTA iteration)
@@ -142,7 +195,7 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
       for (int u = 0; u < RS_PART / 256; u++) {
         const int64_t j = part * RS_PART + u * 256 + threadIdx.x;
         if (j < m) {
-          const uint32_t k = (uint32_t)((keys[j] - lo) >> sh);
+          const uint32_t k = remap(keys[j]);
           k32[j] = k;
 #pragma unroll
           for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
@@ -155,7 +208,7 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
     }
   } else {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
-      const uint32_t k = (uint32_t)((keys[j] - lo) >> sh);
+      const uint32_t k = remap(keys[j]);
       k32[j] = k;
 #pragma unroll
       for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
@@ -348,14 +401,39 @@ __global__ void __launch_bounds__(1024) tile_counts_kernel(int* __restrict__ dif
   }
   __syncthreads();
   if (!in_global) {
-    for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along x
-      int run = 0;
-      for (int x = 0; x < tiles_x; x++) { run += g[y * gw + x]; g[y * gw + x] = run; }
+    // warp-parallel prefix sums: a warp scans a row (then a column) 32 cells
+    // at a time with shuffles, carrying the running total
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int y = warp; y < tiles_y; y += nwarps) {  // prefix along x
+      int carry = 0;
+      for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+        const int x = x0 + lane;
+        int v = x < tiles_x ? g[y * gw + x] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += t;
+        }
+        v += carry;
+        if (x < tiles_x) g[y * gw + x] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
     }
     __syncthreads();
-    for (int x = threadIdx.x; x < tiles_x; x += blockDim.x) {  // prefix along y
-      int run = 0;
-      for (int y = 0; y < tiles_y; y++) { run += g[y * gw + x]; g[y * gw + x] = run; }
+    for (int x = warp; x < tiles_x; x += nwarps) {  // prefix along y
+      int carry = 0;
+      for (int y0 = 0; y0 < tiles_y; y0 += 32) {
+        const int y = y0 + lane;
+        int v = y < tiles_y ? g[y * gw + x] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += t;
+        }
+        v += carry;
+        if (y < tiles_y) g[y * gw + x] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
     }
   } else {
     for (int y = threadIdx.x; y < tiles_y; y += blockDim.x) {  // prefix along x, 32 cells per round
@@ -1220,7 +1298,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.control_bytes = off - ctl0;
   t.rs_tile_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(3 * parts_k));
   t.dk[0] = (uint64_t*)take(8 * nn);
-  t.dk[1] = (uint64_t*)take(8 * nn);
+  t.dk[1] = (uint64_t*)take(8 * nn + 16);  // two 32-bit key arrays, the second 16-B aligned (cp.async staging)
   t.dv[0] = (uint32_t*)take(4 * nn);
   t.dv[1] = (uint32_t*)take(4 * nn);
   t.offsets = (uint32_t*)take(4 * nn);
@@ -1272,6 +1350,7 @@ static int persistent_grid(const void* fn, int threads, size_t smem) {
 // pcnt != nullptr: reduce-then-scan passes (upsweep counts, one scan CTA,
 // rank + scatter from precomputed offsets; pcnt holds parts x 256 words)
 // instead of the single-pass decoupled look-back.
+// implicit_vals: the first pass's values are the input positions (v0 unread).
 // counted: reduce-then-scan without upsweeps -- status holds npasses x parts
 // x 256 count words, zero except the first pass's, which the
 // caller wrote (depth_remap_kernel); each pass counts the next one's as it
@@ -1280,7 +1359,8 @@ template <typename K, int IPT = RS_IPT>
 static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_vals, const int64_t* count_ptr,
                       int64_t cap, int shift0, int npasses, uint32_t* hist, bool hist_ready, uint32_t* status,
                       int64_t parts, uint32_t* part_ctr, cudaStream_t st, K** keys_result, bool last_keys,
-                      uint32_t** vals_result = nullptr, uint32_t* pcnt = nullptr, bool counted = false) {
+                      uint32_t** vals_result = nullptr, uint32_t* pcnt = nullptr, bool counted = false,
+                      bool implicit_vals = false) {
   const size_t smem = sizeof(RadixSmem<K, IPT>);
   static int grid = 0;
   if (grid == 0) {
@@ -1323,7 +1403,8 @@ static int radix_sort(K* k0, K* k1, uint32_t* v0, uint32_t* v1, uint32_t* final_
       HGS_CHECK_LAUNCH();
       poff = pcnt;
     }
-    launch_pdl(radix_pass_kernel<K, IPT>, dim3(g), dim3(RS_THREADS), smem, st, kin, vin, kout, vdst, count_ptr, cap, shift0 + 8 * p,
+    launch_pdl(radix_pass_kernel<K, IPT>, dim3(g), dim3(RS_THREADS), smem, st, kin,
+               (const uint32_t*)(p == 0 && implicit_vals ? nullptr : vin), kout, vdst, count_ptr, cap, shift0 + 8 * p,
                                                       (const uint32_t*)(hist + RADIX * p), status + (size_t)p * parts * RADIX, (int)parts,
                                                       part_ctr + p, (!last || last_keys) ? 1 : 0, (const uint32_t*)poff, pnext);
     HGS_CHECK_LAUNCH();
@@ -1376,7 +1457,11 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   static int scan_grid_cap = 0;
   if (scan_grid_cap == 0) scan_grid_cap = persistent_grid((const void*)compact_kernel, SCAN_THREADS, 0);
   const int scan_grid = (int)tmax<int64_t>(1, tmin<int64_t>(scan_grid_cap, (n + SCAN_TILE - 1) / SCAN_TILE));
-  if (n > 0) {
+  if (n > 0 && HGS_SORT_ALL) {
+    launch_pdl(depth_stats_kernel, dim3(2 * sm_count()), dim3(256), 0, st, (const uint64_t*)proj->sort_keys, n,
+               tiles->counters, reinterpret_cast<unsigned long long*>(s.part_ctr + 24));
+    HGS_CHECK_LAUNCH();
+  } else if (n > 0) {
     launch_pdl(compact_kernel, dim3(scan_grid), dim3(SCAN_THREADS), 0, st, proj->sort_keys, n, s.dk[0], s.dv[0], s.scan_status,
                                                        s.part_ctr + 20, tiles->counters,
                                                        reinterpret_cast<unsigned long long*>(s.part_ctr + 24));
@@ -1408,17 +1493,18 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   // 3. stable sort of the visible rows by fp64 depth bits (result in dk[0]/dv[0])
   // order-preserving remap of the depth keys to DEPTH_KEY_BITS, LSD passes, exact fix-up of truncation ties
   uint32_t* k32a = reinterpret_cast<uint32_t*>(s.dk[1]);
-  uint32_t* k32b = k32a + (n > 0 ? n : 1);
+  uint32_t* k32b = k32a + ((n + 3) & ~(int64_t)3);  // 16-B aligned: the radix passes stage their input with cp.async
   unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
   const bool rts = HGS_SORT_RTS != 0;
-  launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, s.dk[0], tiles->counters, minmax, k32a, s.hist,
-             rts ? s.rs_status : (uint32_t*)nullptr);
+  const bool all = HGS_SORT_ALL != 0;  // every row sorted (culled ones last) instead of the compacted visible rows
+  launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, all ? (const uint64_t*)proj->sort_keys : s.dk[0],
+             tiles->counters, minmax, k32a, s.hist, rts ? s.rs_status : (uint32_t*)nullptr, all ? n : (int64_t)-1);
   HGS_CHECK_LAUNCH();
   uint32_t* k32res = nullptr;
-  uint32_t* rows = nullptr;  // visible rows in (depth, row) order
-  int rc = radix_sort<uint32_t, RS_DEPTH_IPT>(k32a, k32b, s.dv[0], s.dv[1], nullptr, tiles->counters, n, 0,
-                                              DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr, st,
-                                              &k32res, true, &rows, nullptr, rts);
+  uint32_t* rows = nullptr;  // visible rows in (depth, row) order (then the culled ones)
+  int rc = radix_sort<uint32_t, RS_DEPTH_IPT>(k32a, k32b, s.dv[0], s.dv[1], nullptr, all ? nullptr : tiles->counters, n,
+                                              0, DEPTH_KEY_BITS / 8, s.hist, true, s.rs_status, s.parts_n, s.part_ctr,
+                                              st, &k32res, true, &rows, nullptr, rts, all);
   if (rc) return rc;
   launch_pdl(
 #if HGS_FIXUP_V2

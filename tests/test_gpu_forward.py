@@ -189,6 +189,35 @@ def test_depth_order_exact_under_key_truncation(cuda_device):
     assert np.array_equal(np_(dt.entries), t_ref.entries)
 
 
+@pytest.mark.parametrize("n", [2051, 4099, 6147])
+def test_partially_culled_odd_count_bins_match_oracle(n, cuda_device):
+    """Every row's depth key is sorted, the culled rows (behind the camera,
+    past the far plane) with the reserved top key behind the visible ones;
+    counts that are not multiples of 4 or of the 2048-key sort partition
+    exercise the staged (cp.async) radix passes' tails and the second key
+    array's alignment.  Bins bit-exact against the oracle, M = visible rows."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import synthetic as syn
+    rng = np.random.default_rng(n)
+    cam = syn.look_at((0.0, 0.0, 0.0), (0.0, 0.0, 1.0), width=96, height=80)
+    z = rng.uniform(-20.0, 400.0, n)  # near 0.01 / far 100 (look_at): a third culled
+    xy = rng.uniform(-0.7, 0.7, (n, 2)) * np.abs(z)[:, None] * 0.5
+    pc = np.column_stack([xy, z])
+    R, t = cam.rotation, cam.translation
+    gs = syn.HostGaussians(syn.q32((pc - t) @ R), syn.q32(rng.normal(size=(n, 4))),
+                           syn.q32(rng.uniform(-4.0, -2.0, (n, 3))), syn.q32(rng.uniform(-2, 1, n)),
+                           syn.q32(rng.uniform(-1, 1, (n, 3))))
+    p = orc.project(gs, cam)
+    t_ref = orc.build_tiles(p, 96, 80)
+    g, c, _ = dev_scene(gs, cam, None)
+    dp = hgs.project(g, c)
+    dt = hgs.build_tiles(dp, 96, 80)
+    assert 0 < len(p.kept) < n
+    assert int(dt.counters[0].item()) == len(p.kept)
+    assert np.array_equal(np_(dt.tile_starts), t_ref.tile_starts)
+    assert np.array_equal(np_(dt.entries), t_ref.entries)
+
+
 @pytest.mark.parametrize("wh,n", [((7680, 4320), 60_000), ((5120, 2880), 60_000), ((3840, 2160), 120_000),
                                   ((1920, 1080), 60_000), ((1200, 680), 3_000)])
 def test_large_grid_bins_and_blend_match_oracle(wh, n, cuda_device):
