@@ -612,7 +612,10 @@ struct __align__(16) WalkRec {
   double2 a;  // mean x, y
   double2 b;  // U conic xx, U 2xy (U = log2(e)/2: the conic form is the exp2 argument)
   double2 c;  // U conic yy, depth
-  double alpha;
+  union {
+    double alpha;  // PREC: the fp64 alpha (T64 recurrence)
+    float a32;     // otherwise |fp32 alpha| (saves the walk a conversion per entry)
+  };
   float ucut;  // the entry's cut (entry_ucut)
   int k;       // entry index relative to the tile start
   float4 col;  // r, g, b, depth (fp32)
@@ -622,6 +625,7 @@ static_assert(sizeof(WalkRec) == 80, "walk record is 80 B");
 struct TileSmem {
   StageEntry ent[TB_NSTAGE][TB_BATCH];
   WalkRec walk[TB_CONSUMERS][TB_BATCH];
+  float tout[TB_CONSUMERS][2][32];  // transmittance of finished pixels (TbPix)
   unsigned long long full[TB_NSTAGE];
   unsigned long long empty[TB_NSTAGE];
   double exp2tab[EXP2_N];
@@ -632,13 +636,26 @@ struct TileSmem {
   unsigned long long stats[2];
 };
 
+// Per-pixel walk state.  A finished pixel is made inert instead of being
+// tested per entry: T = 0 (its blend terms vanish), e2 = -inf (no early-stop
+// region: the threshold below is -inf and stays so), lim_hi = INT_MAX (no
+// depth stop); its transmittance is parked in shared memory.  Only an entry
+// inside the cut band still sends it to the (then immediate) general path.
 struct TbPix {
-  float T, eT, acc, r, g, b, dacc;
+  float T, e2, acc, r, g, b, dacc;  // e2 = 2 eT: twice the bound on |T - T_reference| (exact scaling)
   int last;
   int lim_hi;  // high word of the mesh depth limit (positive fp64: the word order is the value order)
-  bool done, flagged;
+  bool flagged;
   double T64;
+  __device__ __forceinline__ bool done() const { return T == 0.0f; }
 };
+
+__device__ __forceinline__ void tb_finish(TbPix& q, float* tout) {
+  *tout = q.T;
+  q.T = 0.0f;
+  q.e2 = -__int_as_float(0x7f800000);
+  q.lim_hi = 0x7fffffff;
+}
 
 // The general (sequential, exact where needed) treatment of one entry for
 // one pixel: depth stop, exact re-evaluation inside the cut band, the
@@ -661,13 +678,13 @@ template <bool STATS, bool PREC>
 __device__ __forceinline__ void tb_slow(TbPix& q, const WalkRec& E, double fx, double fy, const double* limit,
                                         float uu, double um, float sg, float d, int k, const double* tab,
                                         const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
-                                        int64_t s, unsigned& walked, unsigned& blended) {
-  if (q.done) return;
+                                        int64_t s, unsigned& walked, unsigned& blended, float* tout) {
+  if (q.done()) return;
   if (STATS) walked++;
   // list is depth sorted; mesh is opaque.  Equal high words: the full fp64
   // compare (limit NULL: no mesh here, +inf)
   if (__double2hiint(E.c.y) >= q.lim_hi && limit && E.c.y >= *limit) {
-    q.done = true;
+    tb_finish(q, tout);
     return;
   }
   bool ok = d < -U_BAND;
@@ -678,17 +695,17 @@ __device__ __forceinline__ void tb_slow(TbPix& q, const WalkRec& E, double fx, d
     sg = (float)sx;
   }
   if (!ok) {
-    q.eT = fmaf(q.T, 1.1920929e-7f, q.eT);
+    q.e2 = fmaf(q.T, 2.3841858e-7f, q.e2);
     return;
   }
   const float om = 1.0f - sg;
   const float test = q.T * om;
   const float w = q.T * sg;
-  q.eT = fmaf(w, EPS_SIG, fmaf(q.eT, om, test * 1.1920929e-7f));
-  if (fmaf(-2.0f, q.eT, test) < STOP_NEAR) {  // the early-stop region
-    if (fabsf(test - STOP_F) <= fmaf(q.eT, 1.001f, 3e-12f)) q.flagged = true;
+  q.e2 = fmaf(w, 2.0f * EPS_SIG, fmaf(q.e2, om, test * 2.3841858e-7f));
+  if (test - q.e2 < STOP_NEAR) {  // the early-stop region
+    if (fabsf(test - STOP_F) <= fmaf(q.e2, 0.5005f, 3e-12f)) q.flagged = true;
     if (test < STOP_F) {
-      q.done = true;
+      tb_finish(q, tout);
       return;
     }
   }
@@ -834,11 +851,11 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     mesh_here[h] = mesh.color != nullptr && inside[h] && mesh.triangle_id[pix[h]] >= 0;
     q[h].lim_hi = __double2hiint(mesh_here[h] ? mesh.depth[pix[h]] : inf);
     q[h].T = 1.0f;
-    q[h].eT = q[h].acc = q[h].r = q[h].g = q[h].b = q[h].dacc = 0.0f;
+    q[h].e2 = q[h].acc = q[h].r = q[h].g = q[h].b = q[h].dacc = 0.0f;
     q[h].last = -1;
-    q[h].done = !inside[h];
     q[h].flagged = false;
     q[h].T64 = 1.0;
+    if (!inside[h]) tb_finish(q[h], &sm.tout[warp][h][lane]);
   }
   bool warp_done = false;
   unsigned walked = 0, blended = 0;
@@ -872,7 +889,10 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         W.a = S.a;
         W.b = make_double2(S.b.x * U_SCALE, S.b.y * U_SCALE);
         W.c = make_double2(S.c.x * U_SCALE, S.c.y);
-        W.alpha = S.d.x;
+        if (PREC)
+          W.alpha = S.d.x;
+        else
+          W.a32 = fabsf(S.f.col.x);  // == |(float)alpha| (the cull record's sign only flags the conic)
         W.ucut = entry_ucut(S.f.col.x);
         W.k = bb + i;
         W.col = make_float4(S.f.col.y, S.f.col.z, S.f.col.w, S.f.con.w);
@@ -885,17 +905,17 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       const WalkRec& E = sm.walk[warp][li];
       const double2 A = E.a, B = E.b, C = E.c;
       const float ucut = E.ucut;
-      const float aabs = fabsf((float)E.alpha);
+      const float aabs = PREC ? fabsf((float)E.alpha) : E.a32;
       const double dx = fx - A.x;
       const double adx = B.x * dx;
       const int zhi = __double2hiint(C.y);
-      float uu[2], sg[2], dd[2], sv[2], Tn[2], eTn[2], w[2];
+      float uu[2], sg[2], dd[2], sv[2], Tn[2], e2n[2], w[2];
       double um[2];
       bool spec[2];
       double dy = fy0 - A.y;
       float thr[2];
 #pragma unroll
-      for (int h = 0; h < 2; h++) thr[h] = fmaf(2.0f, fmaf(q[h].T, EPS_SIG + 1.1920929e-7f, q[h].eT), STOP_NEAR);
+      for (int h = 0; h < 2; h++) thr[h] = fmaf(q[h].T, 2.0f * (EPS_SIG + 1.1920929e-7f), q[h].e2) + STOP_NEAR;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         if (h) dy = dy + 4.0;  // (x, y + 4): within the guard band of the direct difference
@@ -903,48 +923,50 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         uu[h] = __double2float_rn(um[h]);
         sg[h] = fminf(aabs * ex2_neg(uu[h]), CLAMP_F);
         dd[h] = uu[h] - ucut;
-        const bool ok = dd[h] < -U_BAND && !q[h].done;
-        sv[h] = ok ? sg[h] : 0.0f;
+        // (a finished pixel has T = 0: whatever sv is, its terms vanish)
+        sv[h] = dd[h] < -U_BAND ? sg[h] : 0.0f;
         const float om = 1.0f - sv[h];
         Tn[h] = q[h].T * om;
         w[h] = q[h].T * sv[h];
-        eTn[h] = fmaf(w[h], EPS_SIG, fmaf(q[h].eT, om, Tn[h] * 1.1920929e-7f));
+        e2n[h] = fmaf(w[h], 2.0f * EPS_SIG, fmaf(q[h].e2, om, Tn[h] * 2.3841858e-7f));
         // a decision this entry could get wrong: depth stop, the cut band
         // (or a NaN cut), the early-stop region.  The last is tested as
         // Tn < STOP_NEAR + 2 (eT + T (EPS_SIG + 2^-23)) >= STOP_NEAR + 2 eTn
         // (om <= 1, w <= T): the threshold comes from the state before the
-        // entry, off the entry's dependency chain.
-        spec[h] = !q[h].done && (zhi >= q[h].lim_hi || !(fabsf(dd[h]) > U_BAND) || Tn[h] < thr[h]);
+        // entry, off the entry's dependency chain.  An inert (finished)
+        // pixel only meets the cut band (rare; tb_slow returns at once).
+        spec[h] = zhi >= q[h].lim_hi || !(fabsf(dd[h]) > U_BAND) || Tn[h] < thr[h];
       }
       if (!__any_sync(0xffffffffu, spec[0] || spec[1])) {
         const float4 col = E.col;
         const int k = E.k;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-          if (STATS && !q[h].done) {
+          if (STATS && !q[h].done()) {
             walked++;
             blended += sv[h] > 0.0f;
           }
           q[h].T = Tn[h];
-          q[h].eT = eTn[h];
+          q[h].e2 = e2n[h];
           q[h].r = fmaf(col.x, w[h], q[h].r);
           q[h].g = fmaf(col.y, w[h], q[h].g);
           q[h].b = fmaf(col.z, w[h], q[h].b);
           q[h].dacc = fmaf(col.w, w[h], q[h].dacc);
           q[h].acc += w[h];
-          q[h].last = sv[h] > 0.0f ? k : q[h].last;
-          if (PREC && sv[h] > 0.0f)
+          q[h].last = w[h] > 0.0f ? k : q[h].last;  // (w > 0 <=> sv > 0 on a live pixel, never on a finished one)
+          if (PREC && w[h] > 0.0f)
             q[h].T64 *= 1.0 - fmin(E.alpha * exp2_neg64(um[h], uu[h], sm.exp2tab), ALPHA_CLAMP);
         }
       } else {
 #pragma unroll
         for (int h = 0; h < 2; h++)
           tb_slow<STATS, PREC>(q[h], E, fx, fy0 + 4.0 * h, mesh_here[h] ? mesh.depth + pix[h] : nullptr, uu[h],
-                               um[h], sg[h], dd[h], E.k, sm.exp2tab, rec, entries, s, walked, blended);
-        if (__all_sync(0xffffffffu, q[0].done && q[1].done)) break;
+                               um[h], sg[h], dd[h], E.k, sm.exp2tab, rec, entries, s, walked, blended,
+                               &sm.tout[warp][h][lane]);
+        if (__all_sync(0xffffffffu, q[0].done() && q[1].done())) break;
       }
     }
-    if (__all_sync(0xffffffffu, q[0].done && q[1].done)) {
+    if (__all_sync(0xffffffffu, q[0].done() && q[1].done())) {
       warp_done = true;
       if (lane == 0) atomicAdd(&sm.done_warps, 1);
     }
@@ -967,9 +989,10 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       fixup[FIX_SLOTS + slot] = (int32_t)pix[h] + 1;
       continue;
     }
-    write_pixel(out, mesh, mesh_here[h], pix[h], q[h].T, q[h].r, q[h].g, q[h].b, q[h].dacc, q[h].acc,
+    const float Tfin = q[h].done() ? sm.tout[warp][h][lane] : q[h].T;
+    write_pixel(out, mesh, mesh_here[h], pix[h], Tfin, q[h].r, q[h].g, q[h].b, q[h].dacc, q[h].acc,
                 q[h].last >= 0 ? s + q[h].last : -1, bg0, bg1, bg2, mask_variant, mask_k,
-                PREC ? q[h].T64 : (double)q[h].T);
+                PREC ? q[h].T64 : (double)Tfin);
   }
   // the tile is finished once its last consumer warp is: count it for the
   // exact-walk kernel, which drains the queue while the blend still runs
