@@ -625,7 +625,7 @@ static_assert(sizeof(WalkRec) == 80, "walk record is 80 B");
 struct TileSmem {
   StageEntry ent[TB_NSTAGE][TB_BATCH];
   WalkRec walk[TB_CONSUMERS][TB_BATCH];
-  float tout[TB_CONSUMERS][2][32];  // transmittance of finished pixels (TbPix)
+  float tout[2][TB_CONSUMERS][2][32];  // transmittance and last entry of finished pixels (TbPix, tb_finish)
   unsigned long long full[TB_NSTAGE];
   unsigned long long empty[TB_NSTAGE];
   double exp2tab[EXP2_N];
@@ -651,7 +651,8 @@ struct TbPix {
 };
 
 __device__ __forceinline__ void tb_finish(TbPix& q, float* tout) {
-  *tout = q.T;
+  tout[0] = q.T;
+  reinterpret_cast<int*>(tout)[TB_CONSUMERS * 2 * 32] = q.last;  // (the walk keeps updating an inert pixel's last)
   q.T = 0.0f;
   q.e2 = -__int_as_float(0x7f800000);
   q.lim_hi = 0x7fffffff;
@@ -855,7 +856,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     q[h].last = -1;
     q[h].flagged = false;
     q[h].T64 = 1.0;
-    if (!inside[h]) tb_finish(q[h], &sm.tout[warp][h][lane]);
+    if (!inside[h]) tb_finish(q[h], &sm.tout[0][warp][h][lane]);
   }
   bool warp_done = false;
   unsigned walked = 0, blended = 0;
@@ -911,7 +912,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       const int zhi = __double2hiint(C.y);
       float uu[2], sg[2], dd[2], sv[2], Tn[2], e2n[2], w[2];
       double um[2];
-      bool spec[2];
+      bool spec[2], ok[2];
       double dy = fy0 - A.y;
       float thr[2];
 #pragma unroll
@@ -924,7 +925,8 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         sg[h] = fminf(aabs * ex2_neg(uu[h]), CLAMP_F);
         dd[h] = uu[h] - ucut;
         // (a finished pixel has T = 0: whatever sv is, its terms vanish)
-        sv[h] = dd[h] < -U_BAND ? sg[h] : 0.0f;
+        ok[h] = dd[h] < -U_BAND;
+        sv[h] = ok[h] ? sg[h] : 0.0f;
         const float om = 1.0f - sv[h];
         Tn[h] = q[h].T * om;
         w[h] = q[h].T * sv[h];
@@ -953,7 +955,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
           q[h].b = fmaf(col.z, w[h], q[h].b);
           q[h].dacc = fmaf(col.w, w[h], q[h].dacc);
           q[h].acc += w[h];
-          q[h].last = w[h] > 0.0f ? k : q[h].last;  // (w > 0 <=> sv > 0 on a live pixel, never on a finished one)
+          q[h].last = ok[h] ? k : q[h].last;  // (garbage on a finished pixel: tb_finish parked its last)
           if (PREC && w[h] > 0.0f)
             q[h].T64 *= 1.0 - fmin(E.alpha * exp2_neg64(um[h], uu[h], sm.exp2tab), ALPHA_CLAMP);
         }
@@ -962,7 +964,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         for (int h = 0; h < 2; h++)
           tb_slow<STATS, PREC>(q[h], E, fx, fy0 + 4.0 * h, mesh_here[h] ? mesh.depth + pix[h] : nullptr, uu[h],
                                um[h], sg[h], dd[h], E.k, sm.exp2tab, rec, entries, s, walked, blended,
-                               &sm.tout[warp][h][lane]);
+                               &sm.tout[0][warp][h][lane]);
         if (__all_sync(0xffffffffu, q[0].done() && q[1].done())) break;
       }
     }
@@ -989,7 +991,8 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       fixup[FIX_SLOTS + slot] = (int32_t)pix[h] + 1;
       continue;
     }
-    const float Tfin = q[h].done() ? sm.tout[warp][h][lane] : q[h].T;
+    const float Tfin = q[h].done() ? sm.tout[0][warp][h][lane] : q[h].T;
+    if (q[h].done()) q[h].last = __float_as_int(sm.tout[1][warp][h][lane]);
     write_pixel(out, mesh, mesh_here[h], pix[h], Tfin, q[h].r, q[h].g, q[h].b, q[h].dacc, q[h].acc,
                 q[h].last >= 0 ? s + q[h].last : -1, bg0, bg1, bg2, mask_variant, mask_k,
                 PREC ? q[h].T64 : (double)Tfin);
