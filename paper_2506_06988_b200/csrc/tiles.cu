@@ -93,48 +93,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) compact_kernel(const uint64_t* _
   }
 }
 
-// HGS_SORT_ALL: no compaction -- every row's key is sorted, the culled rows
-// (key ~0) with the reserved largest 24-bit key, so they end up behind the
-// M visible rows in the sorted order.  This kernel only gathers what the
-// compaction did on the side: M and the min / max of the visible keys.
-__global__ void __launch_bounds__(256) depth_stats_kernel(const uint64_t* __restrict__ keys, int64_t n,
-                                                          int64_t* counters, unsigned long long* minmax) {
-  pdl_enter();
-  __shared__ unsigned long long s_min[8], s_max[8];
-  __shared__ long long s_cnt[8];
-  unsigned long long nmin = 0, kmax = 0;
-  long long cnt = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; j < n; j += 2 * stride) {
-    uint64_t k0, k1;
-    if (j + 1 < n) {
-      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + j));
-      k0 = v.x, k1 = v.y;
-    } else {
-      k0 = keys[j], k1 = ~0ull;
-    }
-    if (k0 != ~0ull) { nmin = max(nmin, (unsigned long long)~k0); kmax = max(kmax, (unsigned long long)k0); cnt++; }
-    if (k1 != ~0ull) { nmin = max(nmin, (unsigned long long)~k1); kmax = max(kmax, (unsigned long long)k1); cnt++; }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nmin = max(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) s_min[warp] = nmin, s_max[warp] = kmax, s_cnt[warp] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; w++) nmin = max(nmin, s_min[w]), kmax = max(kmax, s_max[w]), cnt += s_cnt[w];
-    if (cnt) {
-      atomicMax(&minmax[0], nmin);
-      atomicMax(&minmax[1], kmax);
-      atomicAdd((unsigned long long*)&counters[0], (unsigned long long)cnt);
-    }
-  }
-}
-
 // Depth keys -> DEPTH_KEY_BITS bits, order preserving: (bits - min) >> shift, where
 // shift drops the low bits the visible range does not need.  Equal 32-bit
 // keys from distinct fp64 depths are re-ordered exactly by depth_fixup_kernel.
@@ -143,9 +101,18 @@ __global__ void __launch_bounds__(256) depth_stats_kernel(const uint64_t* __rest
 // depth_fixup_kernel (1M keys: ~1e4 short runs).
 constexpr int DEPTH_KEY_BITS = 24;
 constexpr uint32_t KEY_CULLED = (1u << DEPTH_KEY_BITS) - 1;
-#ifndef HGS_SORT_ALL
-#define HGS_SORT_ALL 1
+// Depth-order front end (hgs_build_tiles step 3):
+//  0: compact_kernel (chained-scan compaction of the visible rows), remap
+//  1: no compaction -- every row's key is sorted, the culled rows (key ~0)
+//     under the reserved largest 24-bit key, i.e. behind the M visible rows
+//  2: compaction fused into the remap: depth_stats_kernel counts each
+//     partition's visible rows (and M, the key range), the remap places a
+//     partition's visible keys after its predecessors' (one read of their
+//     counts) -- no look-back chain, no culled keys in the sort
+#ifndef HGS_DEPTH_MODE
+#define HGS_DEPTH_MODE 2
 #endif
+#define HGS_SORT_ALL (HGS_DEPTH_MODE == 1)
 // depth sort partition (radix_pass_kernel<uint32_t, 8>: 256 threads x 8 keys)
 constexpr int RS_DEPTH_IPT = 8;
 constexpr int RS_PART = RS_THREADS * RS_DEPTH_IPT;
@@ -155,6 +122,63 @@ constexpr int RS_PART = RS_THREADS * RS_DEPTH_IPT;
 #ifndef HGS_SORT_RTS
 #define HGS_SORT_RTS 1
 #endif
+// Modes 1 / 2: M and the min / max of the visible keys (what the compaction
+// gathered on the side), per partition of RS_PART rows; mode 2 also stores
+// each partition's visible count (vis_cnt).
+__global__ void __launch_bounds__(256) depth_stats_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                                          int64_t* counters, unsigned long long* minmax,
+                                                          uint32_t* __restrict__ vis_cnt) {
+  pdl_enter();
+  __shared__ unsigned long long s_min[8], s_max[8];
+  __shared__ uint32_t s_cnt[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long nmin = 0, kmax = 0;
+  long long total = 0;
+  const int64_t nparts = (n + RS_PART - 1) / RS_PART;
+  for (int64_t part = blockIdx.x; part < nparts; part += gridDim.x) {
+    const int64_t base = part * RS_PART + (int64_t)threadIdx.x * 8;  // 8 consecutive keys per thread
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      uint64_t k0 = ~0ull, k1 = ~0ull;
+      if (base + j + 1 < n) {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + j));
+        k0 = v.x, k1 = v.y;
+      } else if (base + j < n) {
+        k0 = keys[base + j];
+      }
+      if (k0 != ~0ull) { nmin = max(nmin, (unsigned long long)~k0); kmax = max(kmax, (unsigned long long)k0); cnt++; }
+      if (k1 != ~0ull) { nmin = max(nmin, (unsigned long long)~k1); kmax = max(kmax, (unsigned long long)k1); cnt++; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t c = 0;
+      for (int w = 0; w < 8; w++) c += s_cnt[w];
+      if (vis_cnt) vis_cnt[part] = c;
+      total += c;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nmin = max(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) s_min[warp] = nmin, s_max[warp] = kmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; w++) nmin = max(nmin, s_min[w]), kmax = max(kmax, s_max[w]);
+    if (total) {
+      atomicMax(&minmax[0], nmin);
+      atomicMax(&minmax[1], kmax);
+      atomicAdd((unsigned long long*)&counters[0], (unsigned long long)total);
+    }
+  }
+}
+
 __device__ __forceinline__ int depth_shift(const unsigned long long* minmax) {
   const unsigned long long lo = ~minmax[0], hi = minmax[1];
   const unsigned long long range = hi > lo ? hi - lo : 0;
@@ -215,6 +239,81 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
     }
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) {
+    const uint32_t c = (&sh_h[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+// Mode 2: the compaction fused into the remap.  One CTA per partition of
+// RS_PART rows (8 consecutive per thread): the visible rows before it are the
+// sum of its predecessors' counts (depth_stats_kernel), its own are ranked
+// by a block scan, staged in shared memory and written out contiguously --
+// the remapped key and the row -- together with the digit histograms and
+// the first sort pass's per-partition digit counts (the partition's output
+// range spans at most two sort partitions: counted in shared memory).
+__global__ void __launch_bounds__(256) depth_compact_remap_kernel(
+    const uint64_t* __restrict__ keys, int64_t n, const unsigned long long* __restrict__ minmax,
+    const uint32_t* __restrict__ vis_cnt, uint32_t* __restrict__ k32, uint32_t* __restrict__ rows,
+    uint32_t* __restrict__ hist, uint32_t* __restrict__ pcnt0) {
+  pdl_enter();
+  constexpr int NP = DEPTH_KEY_BITS / 8;
+  __shared__ uint32_t sh_h[NP][256];
+  __shared__ uint32_t sh_p[2][256];
+  __shared__ uint32_t s_k[RS_PART], s_r[RS_PART];
+  __shared__ uint32_t s_warp[8];
+  for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) (&sh_h[0][0])[i] = 0;
+  const unsigned long long lo = ~minmax[0];
+  const int sh = depth_shift(minmax);
+  const int64_t nparts = (n + RS_PART - 1) / RS_PART;
+  for (int64_t part = blockIdx.x; part < nparts; part += gridDim.x) {
+    uint32_t pre = 0;  // visible rows in the earlier partitions
+    for (int64_t q = threadIdx.x; q < part; q += blockDim.x) pre += vis_cnt[q];
+    sh_p[0][threadIdx.x] = sh_p[1][threadIdx.x] = 0;
+    const int64_t base = part * RS_PART + (int64_t)threadIdx.x * 8;
+    uint64_t kk[8];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      if (base + j + 1 < n) {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + j));
+        kk[j] = v.x, kk[j + 1] = v.y;
+      } else {
+        kk[j] = base + j < n ? keys[base + j] : ~0ull;
+        kk[j + 1] = ~0ull;
+      }
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) cnt += kk[j] != ~0ull;
+    uint32_t tot_pre;
+    pre = block_exclusive_scan<uint32_t>(pre, s_warp, tot_pre);  // (only the total is used)
+    pre = tot_pre;
+    uint32_t tot;
+    uint32_t r = block_exclusive_scan<uint32_t>(cnt, s_warp, tot);
+    const uint32_t p0 = pre / RS_PART;  // first sort partition of this output range
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      if (kk[j] == ~0ull) continue;
+      const uint32_t k = (uint32_t)((kk[j] - lo) >> sh);
+      s_k[r] = k;
+      s_r[r] = (uint32_t)(base + j);
+#pragma unroll
+      for (int p = 0; p < NP; p++) atomicAdd(&sh_h[p][(k >> (8 * p)) & 255u], 1u);
+      atomicAdd(&sh_p[(pre + r) / RS_PART - p0][k & 255u], 1u);
+      r++;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tot; i += blockDim.x) {
+      k32[pre + i] = s_k[i];
+      rows[pre + i] = s_r[i];
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t c = sh_p[h][threadIdx.x];
+      if (c) atomicAdd(&pcnt0[(size_t)(p0 + h) * RADIX + threadIdx.x], c);
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < NP * 256; i += blockDim.x) {
     const uint32_t c = (&sh_h[0][0])[i];
     if (c) atomicAdd(&hist[i], c);
@@ -1254,6 +1353,7 @@ struct TilesScratch {
   uint32_t* bin_slot;     // parts_bin x BIN_MAX_SUPER: slot per (partition, super-tile)
   uint32_t* bin_wmat;     // parts_bin x 8 x BIN_MAX_SUPER: per-warp exclusive counts
   uint32_t* chist;        // BIN_MAX_SUPER (zeroed)
+  uint32_t* vis_cnt;      // 2 parts_n: visible rows per RS_PART-row partition (HGS_DEPTH_MODE 2)
   uint32_t* cstart;       // BIN_MAX_SUPER + 1: super-tile list starts
   ushort4* rsort;         // n: tile rectangles in depth order
   uint32_t* pair_off;     // n + 1: coarse pair offsets in depth order
@@ -1297,6 +1397,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.chist = binned ? (uint32_t*)take(sizeof(uint32_t) * BIN_MAX_SUPER) : nullptr;
   t.control_bytes = off - ctl0;
   t.rs_tile_status = (uint32_t*)take(sizeof(uint32_t) * RADIX * (size_t)(3 * parts_k));
+  t.vis_cnt = (uint32_t*)take(sizeof(uint32_t) * (size_t)(2 * parts_n));
   t.dk[0] = (uint64_t*)take(8 * nn);
   t.dk[1] = (uint64_t*)take(8 * nn + 16);  // two 32-bit key arrays, the second 16-B aligned (cp.async staging)
   t.dv[0] = (uint32_t*)take(4 * nn);
@@ -1457,9 +1558,10 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   static int scan_grid_cap = 0;
   if (scan_grid_cap == 0) scan_grid_cap = persistent_grid((const void*)compact_kernel, SCAN_THREADS, 0);
   const int scan_grid = (int)tmax<int64_t>(1, tmin<int64_t>(scan_grid_cap, (n + SCAN_TILE - 1) / SCAN_TILE));
-  if (n > 0 && HGS_SORT_ALL) {
+  if (n > 0 && HGS_DEPTH_MODE != 0) {
     launch_pdl(depth_stats_kernel, dim3(2 * sm_count()), dim3(256), 0, st, (const uint64_t*)proj->sort_keys, n,
-               tiles->counters, reinterpret_cast<unsigned long long*>(s.part_ctr + 24));
+               tiles->counters, reinterpret_cast<unsigned long long*>(s.part_ctr + 24),
+               HGS_DEPTH_MODE == 2 ? s.vis_cnt : (uint32_t*)nullptr);
     HGS_CHECK_LAUNCH();
   } else if (n > 0) {
     launch_pdl(compact_kernel, dim3(scan_grid), dim3(SCAN_THREADS), 0, st, proj->sort_keys, n, s.dk[0], s.dv[0], s.scan_status,
@@ -1496,9 +1598,16 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   uint32_t* k32b = k32a + ((n + 3) & ~(int64_t)3);  // 16-B aligned: the radix passes stage their input with cp.async
   unsigned long long* minmax = reinterpret_cast<unsigned long long*>(s.part_ctr + 24);
   const bool rts = HGS_SORT_RTS != 0;
-  const bool all = HGS_SORT_ALL != 0;  // every row sorted (culled ones last) instead of the compacted visible rows
-  launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, all ? (const uint64_t*)proj->sort_keys : s.dk[0],
-             tiles->counters, minmax, k32a, s.hist, rts ? s.rs_status : (uint32_t*)nullptr, all ? n : (int64_t)-1);
+  const bool all = HGS_SORT_ALL;  // every row sorted (culled ones last) instead of the compacted visible rows
+  if (HGS_DEPTH_MODE == 2) {
+    launch_pdl(depth_compact_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st, (const uint64_t*)proj->sort_keys, n,
+               (const unsigned long long*)minmax, (const uint32_t*)s.vis_cnt, k32a, s.dv[0], s.hist,
+               rts ? s.rs_status : (uint32_t*)nullptr);
+  } else {
+    launch_pdl(depth_remap_kernel, dim3(4 * sm_count()), dim3(256), 0, st,
+               all ? (const uint64_t*)proj->sort_keys : s.dk[0], tiles->counters, minmax, k32a, s.hist,
+               rts ? s.rs_status : (uint32_t*)nullptr, all ? n : (int64_t)-1);
+  }
   HGS_CHECK_LAUNCH();
   uint32_t* k32res = nullptr;
   uint32_t* rows = nullptr;  // visible rows in (depth, row) order (then the culled ones)

@@ -191,11 +191,12 @@ def test_depth_order_exact_under_key_truncation(cuda_device):
 
 @pytest.mark.parametrize("n", [2051, 4099, 6147])
 def test_partially_culled_odd_count_bins_match_oracle(n, cuda_device):
-    """Every row's depth key is sorted, the culled rows (behind the camera,
-    past the far plane) with the reserved top key behind the visible ones;
-    counts that are not multiples of 4 or of the 2048-key sort partition
-    exercise the staged (cp.async) radix passes' tails and the second key
-    array's alignment.  Bins bit-exact against the oracle, M = visible rows."""
+    """A third of the rows culled (behind the camera, past the far plane):
+    the compaction fused into the depth remap (per-partition visible counts)
+    must keep the visible rows in row order; counts that are not multiples of
+    4 or of the 2048-key sort partition exercise the staged (cp.async) radix
+    passes' tails and the second key array's alignment.  Bins bit-exact
+    against the oracle, M = visible rows."""
     import paper_2506_06988_b200 as hgs
     from paper_2506_06988_b200 import synthetic as syn
     rng = np.random.default_rng(n)
