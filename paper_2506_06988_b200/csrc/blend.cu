@@ -622,13 +622,14 @@ struct __align__(16) WalkRec {
 };
 static_assert(sizeof(WalkRec) == 80, "walk record is 80 B");
 
+template <bool PREC>
 struct TileSmem {
   StageEntry ent[TB_NSTAGE][TB_BATCH];
   WalkRec walk[TB_CONSUMERS][TB_BATCH];
   float tout[2][TB_CONSUMERS][2][32];  // transmittance and last entry of finished pixels (TbPix, tb_finish)
   unsigned long long full[TB_NSTAGE];
   unsigned long long empty[TB_NSTAGE];
-  double exp2tab[EXP2_N];
+  double exp2tab[PREC ? EXP2_N : 1];  // (the fp64 exp2 table: training state only)
   int done_warps;
   int end_batch;
   int finished_warps;
@@ -736,7 +737,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     pdl_enter();
   if (counters && counters[2]) return;  // entry buffer overflowed: bins are invalid, the caller re-renders
   extern __shared__ __align__(128) unsigned char tile_smem_raw[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(tile_smem_raw);
+  TileSmem<PREC>& sm = *reinterpret_cast<TileSmem<PREC>*>(tile_smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < TB_NSTAGE; i++) {
@@ -1168,12 +1169,15 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup, tiles->counters);
 #else
     (void)smem;
-    const size_t tsmem = sizeof(TileSmem);
+    const size_t tsmem = out->final_t != nullptr ? sizeof(TileSmem<true>) : sizeof(TileSmem<false>);
     static bool tattr = false;
     if (!tattr) {
-      for (auto fn : {blend_tile_kernel<false, false>, blend_tile_kernel<true, false>, blend_tile_kernel<false, true>,
-                      blend_tile_kernel<true, true>}) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+      for (auto fn : {blend_tile_kernel<false, false>, blend_tile_kernel<true, false>}) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<false>));
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      }
+      for (auto fn : {blend_tile_kernel<false, true>, blend_tile_kernel<true, true>}) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<true>));
         cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       }
       tattr = true;
