@@ -335,7 +335,7 @@ def run_ours(args):
     from paper_2506_06988_b200.splat import _c_f64_3  # noqa: F401
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     blend_ms, tiles_ms, reps = 0.0, 0.0, max(3, min(args.steps, 10))
-    r.stats = torch.zeros(2, dtype=torch.int64, device=dev)
+    r.stats = torch.zeros(3, dtype=torch.int64, device=dev)
     import ctypes
     L = _lib.load()
     for i in range(reps):

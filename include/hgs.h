@@ -159,7 +159,8 @@ typedef struct hgs_blend_out {
   double* final_t;      /* H x W fp64 residual T, backward state (may be NULL) */
   int32_t* last;        /* H x W global entry index or -1 (may be NULL) */
   float* mask;          /* H x W transmittance_mask(T) (losses.py:79-91), may be NULL */
-  int64_t* stats;       /* device int64[2]: += evaluations walked, += blended (may be NULL) */
+  int64_t* stats;       /* device int64[3]: += evaluations walked, += blended, += pixels handed to the exact fp64
+                           walk (may be NULL) */
   int32_t* fixup;       /* device int32[H*W + 4] scratch, ZERO at first use (the call leaves it zero again):
                            the queue of pixels the fast path hands to the exact fp64 walk (may be NULL: exact
                            walk for every pixel) */

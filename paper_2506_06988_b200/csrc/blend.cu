@@ -696,14 +696,10 @@ __device__ __forceinline__ void tb_slow(TbPix& q, const WalkRec& E, double fx, d
     ok = sx >= 0.0;
     sg = (float)sx;
   }
-  if (!ok) {
-    q.e2 = fmaf(q.T, 2.3841858e-7f, q.e2);
-    return;
-  }
-  const float om = 1.0f - sg;
-  const float test = q.T * om;
+  if (!ok) return;  // not blended: T is unchanged (exactly), so is the bound
+  const float test = fmaf(-q.T, sg, q.T);
   const float w = q.T * sg;
-  q.e2 = fmaf(w, 2.0f * EPS_SIG, fmaf(q.e2, om, test * 2.3841858e-7f));
+  q.e2 = fmaf(w, 2.0f * EPS_SIG, fmaf(-q.e2, sg, fmaf(test, 1.1920929e-7f, q.e2)));
   if (test - q.e2 < STOP_NEAR) {  // the early-stop region
     if (fabsf(test - STOP_F) <= fmaf(q.e2, 0.5005f, 3e-12f)) q.flagged = true;
     if (test < STOP_F) {
@@ -928,10 +924,11 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         // (a finished pixel has T = 0: whatever sv is, its terms vanish)
         ok[h] = dd[h] < -U_BAND;
         sv[h] = ok[h] ? sg[h] : 0.0f;
-        const float om = 1.0f - sv[h];
-        Tn[h] = q[h].T * om;
+        // T (1 - sv) with one rounding (|err| <= 2^-24 T'), so the bound grows
+        // by e (1 - sv) + w EPS_SIG + 2^-24 T' (doubled: e2)
+        Tn[h] = fmaf(-q[h].T, sv[h], q[h].T);
         w[h] = q[h].T * sv[h];
-        e2n[h] = fmaf(w[h], 2.0f * EPS_SIG, fmaf(q[h].e2, om, Tn[h] * 2.3841858e-7f));
+        e2n[h] = fmaf(w[h], 2.0f * EPS_SIG, fmaf(-q[h].e2, sv[h], fmaf(Tn[h], 1.1920929e-7f, q[h].e2)));
         // a decision this entry could get wrong: depth stop, the cut band
         // (or a NaN cut), the early-stop region.  The last is tested as
         // Tn < STOP_NEAR + 2 (eT + T (EPS_SIG + 2^-23)) >= STOP_NEAR + 2 eTn
@@ -990,6 +987,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     if (q[h].flagged) {  // queue the pixel for the exact walk (slot value pixel + 1; 0 = empty)
       const int slot = atomicAdd(&fixup[FIX_RESERVED], 1);
       fixup[FIX_SLOTS + slot] = (int32_t)pix[h] + 1;
+      if (STATS) atomicAdd((unsigned long long*)&out.stats[2], 1ull);
       continue;
     }
     const float Tfin = q[h].done() ? sm.tout[0][warp][h][lane] : q[h].T;

@@ -67,7 +67,7 @@ class HybridRenderer:
         self.final_t = torch.empty(h, w, dtype=torch.float64, device=dev) if keep_state else None
         self.last = torch.empty(h, w, dtype=torch.int32, device=dev) if keep_state else None
         self.mask_out = torch.empty(h, w, dtype=torch.float32, device=dev) if mask is not None else None
-        self.stats = torch.zeros(2, dtype=torch.int64, device=dev) if collect_stats else None
+        self.stats = torch.zeros(3, dtype=torch.int64, device=dev) if collect_stats else None
         if mesh is not None:
             self.frag_tri = torch.empty(h, w, dtype=torch.int32, device=dev)
             self.frag_depth = torch.empty(h, w, dtype=torch.float64, device=dev)

@@ -27,7 +27,7 @@ m = hgs.TexturedMesh.from_any(sc.mesh)
 dev = g.device
 cam_dev = sp._upload_camera(c, dev)
 W, H = c.width, c.height
-stats = torch.zeros(2, dtype=torch.int64, device=dev)
+stats = torch.zeros(3, dtype=torch.int64, device=dev)
 
 
 def frame(stats_t=None):
