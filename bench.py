@@ -359,7 +359,7 @@ def run_ours(args):
         blend_ms += ev[1].elapsed_time(ev[2])
     blend_ms /= reps
     tiles_ms /= reps
-    walked, blended = (int(x) for x in r.stats.cpu())
+    walked, blended, flagged = (int(x) for x in r.stats.cpu())
     npix = W * H
     # K4 is rated against its compute bound: evaluations/s
     # vs min(FP32 rate / 14 ops, ex2 rate), peaks microbenchmarked on the box
@@ -394,7 +394,8 @@ def run_ours(args):
                        "gaussians": len(gs), "visible": m_vis, "tile_entries": k_entries, "triangles": mesh.n_faces,
                        "texture": list(mesh.texture.shape), "resolution": [W, H],
                        "l2": "flushed between frames (256 MB write)", "parallelism": f"replicas x{world}",
-                       "evaluations_walked_per_px": walked / npix, "blended_per_px": blended / npix},
+                       "evaluations_walked_per_px": walked / npix, "blended_per_px": blended / npix,
+                       "exact_replay_px": flagged},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 200,
                     "d2h_bytes_per_step": int(H * W * 5 * 4),
                     "note": "scene resident; serving loop HybridRenderer.render_to_host: per frame camera H2D (pinned) + "
