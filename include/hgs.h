@@ -128,7 +128,11 @@ typedef struct hgs_projected {
    re-enqueue. */
 typedef struct hgs_tiles {
   int32_t tiles_x, tiles_y, tile_px;
-  int32_t reserved;
+  int32_t flags;        /* HGS_TILES_BLEND_ONLY (binned tile grids): hgs_build_tiles stops at the coarse
+                           (super-tile) lists and does not write `entries`; hgs_blend_forward reads each
+                           tile's list straight from its super-tile's coarse list.  For a renderer that
+                           only needs the images (no backward, no TileBins): the blend reads only the
+                           prefix of every list it walks before T falls under 1e-4 */
   int64_t capacity;
   uint32_t* entries;    /* capacity */
   int64_t* tile_starts; /* tiles_x * tiles_y + 1 */
@@ -141,7 +145,11 @@ typedef struct hgs_tiles {
   void* join_event;     /* cudaEvent_t or NULL: hgs_build_tiles makes its last (fine binning) kernel wait for it.
                            Joins an independent branch the blend needs (the mesh layer) there, so that the blend
                            itself has the fine binning as its only dependency and can start programmatically */
+  const void* coarse_rows;   /* written by hgs_build_tiles (binned grids): the super-tile lists of original rows */
+  const void* coarse_rects;  /* ... their tile rectangles (u16 x 4) */
+  const void* coarse_starts; /* ... and the lists' starts (u32, one per super-tile + 1) */
 } hgs_tiles;
+#define HGS_TILES_BLEND_ONLY 1
 #define HGS_READY_INTS (2 + 2048)
 
 /* MeshLayer (splat/render.py:26-41).  color == NULL means "no mesh". */

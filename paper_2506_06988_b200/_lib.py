@@ -59,10 +59,13 @@ class HGSProjected(ctypes.Structure):
 
 
 class HGSTiles(ctypes.Structure):
-    _fields_ = [("tiles_x", c_i32), ("tiles_y", c_i32), ("tile_px", c_i32), ("reserved", c_i32),
+    _fields_ = [("tiles_x", c_i32), ("tiles_y", c_i32), ("tile_px", c_i32), ("flags", c_i32),
                 ("capacity", c_i64), ("entries", c_void_p), ("tile_starts", c_void_p), ("counters", c_void_p),
                 ("scratch", c_void_p), ("scratch_bytes", ctypes.c_size_t), ("ready", c_void_p),
-                ("join_event", c_void_p)]
+                ("join_event", c_void_p), ("coarse_rows", c_void_p), ("coarse_rects", c_void_p),
+                ("coarse_starts", c_void_p)]
+
+TILES_BLEND_ONLY = 1  # HGS_TILES_BLEND_ONLY
 
 READY_INTS = 2 + 2048  # HGS_READY_INTS
 

@@ -301,6 +301,183 @@ __device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec,
   return ExactPixel{T, pr, pg, pb, pd, last};
 }
 
+// The exact walk of one pixel over a super-tile's coarse list (blend-only
+// bins): the entries whose rectangle covers the pixel's tile are its tile
+// list, in order.  Two list entries per lane per round (64 per round), the
+// next round's rectangles and rows and this round's matching records in
+// flight while a round is evaluated; the tile-list index of every entry from
+// a running count of the matches.  Otherwise the reference's walk as in
+// exact_walk2 (depth stop, shuffle prefix product of 1 - sigma, serial replay
+// of a round with a value within 1e-12 of the early-stop threshold).
+__device__ __noinline__ ExactPixel exact_walk_coarse(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ crow,
+                                                     const uint2* __restrict__ crect, uint32_t cb, uint32_t ce, int tx,
+                                                     int ty, int64_t s, double fx, double fy, double limit, int lane) {
+  constexpr int EW = 2, RW = 32 * EW;
+  double T = 1.0, pr = 0.0, pg = 0.0, pb = 0.0, pd = 0.0;
+  int64_t last = -1;
+  bool done = false;
+  int kcount = 0;
+  auto covers = [&](uint2 r) {
+    return (int)(r.x & 0xffffu) <= tx && tx <= (int)(r.x >> 16) && (int)(r.y & 0xffffu) <= ty &&
+           ty <= (int)(r.y >> 16);
+  };
+  // software pipeline: while round r is evaluated, the matching records of
+  // round r + 1 and the rectangles / rows of round r + 2 are in flight
+  uint2 rn[EW];
+  uint32_t gn[EW];
+  auto load_rects = [&](uint32_t b) {
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      const uint32_t i = b + EW * lane + u;
+      rn[u] = i < ce ? __ldcg(crect + i) : make_uint2(0xffffu, 0xffffu);  // (x0 = 65535 > x1: no match)
+      gn[u] = i < ce ? __ldcg(crow + i) : 0u;
+    }
+  };
+  bool mnext[EW];
+  BlendRec cnext[EW];
+  auto load_recs = [&]() {
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      mnext[u] = covers(rn[u]);
+      if (mnext[u]) cnext[u] = rec[gn[u]];
+    }
+  };
+  load_rects(cb);
+  load_recs();
+  load_rects(cb + RW);
+  for (uint32_t base = cb; base < ce && !done; base += RW) {
+    bool match[EW];
+    BlendRec c[EW];
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      match[u] = mnext[u];
+      c[u] = cnext[u];
+    }
+    load_recs();                // round + 1
+    load_rects(base + 2 * RW);  // round + 2
+    const unsigned m0 = __ballot_sync(0xffffffffu, match[0]), m1 = __ballot_sync(0xffffffffu, match[1]);
+    const int kl = kcount + __popc(m0 & lanemask_lt()) + __popc(m1 & lanemask_lt());
+    int krank[EW] = {kl, kl + (match[0] ? 1 : 0)};
+    kcount += __popc(m0) + __popc(m1);
+    double sig[EW];
+    bool use[EW];
+    int us = EW;  // first depth stop of this lane
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      use[u] = false;
+      sig[u] = 0.0;
+      if (match[u]) {
+        if (c[u].depth >= limit && us == EW) us = u;
+        const double dx = fx - c[u].mx, dy = fy - c[u].my;
+        const double m = c[u].ca * dx * dx + c[u].cb2 * dx * dy + c[u].cc * dy * dy;
+        if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
+          double sg = c[u].alpha * exp(-0.5 * m);
+          if (sg > ALPHA_CLAMP) sg = ALPHA_CLAMP;
+          use[u] = !(sg < SIGMA_SKIP);
+          sig[u] = sg;
+        }
+      }
+    }
+    const unsigned smask = __ballot_sync(0xffffffffu, us < EW);
+    const int ls = smask ? __ffs(smask) - 1 : 32;
+    const int lsu = __shfl_sync(0xffffffffu, us, ls & 31);
+#pragma unroll
+    for (int u = 0; u < EW; u++)
+      if (lane > ls || (lane == ls && u >= lsu)) use[u] = false;
+    if (ls < 32) done = true;
+    double f[EW];
+    double q = 1.0;
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      f[u] = use[u] ? 1.0 - sig[u] : 1.0;
+      q *= f[u];
+    }
+    double P = q;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, P, d);
+      if (lane >= d) P *= t;
+    }
+    double Pex = __shfl_up_sync(0xffffffffu, P, 1);
+    if (lane == 0) Pex = 1.0;
+    double ta[EW];
+    double run = T * Pex;
+    bool near = false;
+#pragma unroll
+    for (int u = 0; u < EW; u++) {
+      run *= f[u];
+      ta[u] = run;
+      near = near || (use[u] && fabs(run - EARLY_STOP_T) <= 1e-12 * EARLY_STOP_T);
+    }
+    if (!__any_sync(0xffffffffu, near)) {
+      int ue = EW;
+#pragma unroll
+      for (int u = 0; u < EW; u++)
+        if (use[u] && ta[u] < EARLY_STOP_T && ue == EW) ue = u;
+      const unsigned emask = __ballot_sync(0xffffffffu, ue < EW);
+      const int le = emask ? __ffs(emask) - 1 : 32;
+      const int leu = __shfl_sync(0xffffffffu, ue, le & 31);
+      int lastk = -1;
+      double tb = T * Pex, tl = 0.0;
+#pragma unroll
+      for (int u = 0; u < EW; u++) {
+        const bool valid = use[u] && (lane < le || (lane == le && u < leu));
+        if (valid) {
+          const double w = sig[u] * tb;
+          pr += c[u].r * w;
+          pg += c[u].g * w;
+          pb += c[u].b * w;
+          pd += c[u].depth * w;
+          lastk = krank[u];
+          tl = ta[u];
+        }
+        tb = ta[u];
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, lastk >= 0);
+      if (vmask) {
+        const int lv = 31 - __clz(vmask);
+        T = __shfl_sync(0xffffffffu, tl, lv);
+        last = s + __shfl_sync(0xffffffffu, lastk, lv);
+      }
+      if (le < 32) done = true;
+    } else {
+      bool stop = false;
+      for (int i = 0; i < 32 && !stop; i++) {
+#pragma unroll
+        for (int u = 0; u < EW; u++) {
+          const bool ui = __shfl_sync(0xffffffffu, use[u], i);
+          const int ki = __shfl_sync(0xffffffffu, krank[u], i);
+          if (!ui || stop) continue;
+          const double sg = __shfl_sync(0xffffffffu, sig[u], i);
+          const double test_t = T * (1.0 - sg);
+          if (test_t < EARLY_STOP_T) {
+            stop = true;
+            continue;
+          }
+          if (lane == i) {
+            const double w = sg * T;
+            pr += c[u].r * w;
+            pg += c[u].g * w;
+            pb += c[u].b * w;
+            pd += c[u].depth * w;
+          }
+          T = test_t;
+          last = s + ki;
+        }
+      }
+      if (stop) done = true;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    pr += __shfl_xor_sync(0xffffffffu, pr, d);
+    pg += __shfl_xor_sync(0xffffffffu, pg, d);
+    pb += __shfl_xor_sync(0xffffffffu, pb, d);
+    pd += __shfl_xor_sync(0xffffffffu, pd, d);
+  }
+  return ExactPixel{T, pr, pg, pb, pd, last};
+}
+
 // PREC (the caller asked for the backward state final_t): T is also carried
 // in fp64 with sigma from the fp64 exp2 (stage.cuh) for every blended entry,
 // i.e. the reference's T recurrence to ~1e-11 relative; only final_t takes
@@ -614,7 +791,10 @@ struct __align__(16) WalkRec {
   double2 c;  // U conic yy, depth
   union {
     double alpha;  // PREC: the fp64 alpha (T64 recurrence)
-    float a32;     // otherwise |fp32 alpha| (saves the walk a conversion per entry)
+    struct {
+      float a32;     // otherwise |fp32 alpha| (saves the walk a conversion per entry)
+      uint32_t row;  // ... and the Gaussian's row (blend-only bins: the exact re-evaluation's record)
+    };
   };
   float ucut;  // the entry's cut (entry_ucut)
   int k;       // entry index relative to the tile start
@@ -627,6 +807,11 @@ struct TileSmem {
   StageEntry ent[TB_NSTAGE][TB_BATCH];
   WalkRec walk[TB_CONSUMERS][TB_BATCH];
   float tout[2][TB_CONSUMERS][2][32];  // transmittance and last entry of finished pixels (TbPix, tb_finish)
+  // blend-only bins (coarse-fed producer): per ring slot the entry count,
+  // the tile-list index of its first entry, and every entry's row
+  int nbs[TB_NSTAGE];
+  int kbase[TB_NSTAGE];
+  uint32_t gid[TB_NSTAGE][TB_BATCH];
   unsigned long long full[TB_NSTAGE];
   unsigned long long empty[TB_NSTAGE];
   double exp2tab[PREC ? EXP2_N : 1];  // (the fp64 exp2 table: training state only)
@@ -665,9 +850,8 @@ __device__ __forceinline__ void tb_finish(TbPix& q, float* tout) {
 // tile start.
 // exact re-evaluation from the Gaussian's fp64 record in global memory (the
 // walk record holds the scaled conic)
-__device__ __noinline__ double exact_global(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
-                                            int64_t k, double fx, double fy) {
-  const BlendRec& R = rec[entries[k]];
+__device__ __noinline__ double exact_global(const BlendRec* __restrict__ rec, uint32_t row, double fx, double fy) {
+  const BlendRec& R = rec[row];
   const double dx = fx - R.mx, dy = fy - R.my;
   const double m = R.ca * dx * dx + R.cb2 * dx * dy + R.cc * dy * dy;
   if (m > SUPPORT_MAHAL2 || m < 0.0) return -1.0;
@@ -692,7 +876,7 @@ __device__ __forceinline__ void tb_slow(TbPix& q, const WalkRec& E, double fx, d
   bool ok = d < -U_BAND;
   double sx = -1.0;
   if (!(fabsf(d) > U_BAND)) {  // within the cut band (or a NaN cut): decide exactly
-    sx = exact_global(rec, entries, s + k, fx, fy);
+    sx = exact_global(rec, entries ? entries[s + k] : E.row, fx, fy);  // (entries NULL: coarse-fed)
     ok = sx >= 0.0;
     sg = (float)sx;
   }
@@ -723,7 +907,11 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     const BlendRec* __restrict__ rec, const CullRec* __restrict__ cull, const uint32_t* __restrict__ entries,
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
-    const int64_t* __restrict__ counters, int* ready, int qs, int sx_super) {
+    const int64_t* __restrict__ counters, int* ready, int qs, int sx_super, const uint32_t* __restrict__ crow,
+    const uint2* __restrict__ crect, const uint32_t* __restrict__ cstart, int css) {
+  // crow != NULL (blend-only bins, never PREC): the producer filters the
+  // tile's super-tile coarse list (super-tiles of 2^css tiles, sx_super per
+  // row) into the ring instead of reading `entries`.
   // ready != NULL: launched behind the fine binning without waiting for its
   // grid; each CTA claims the next tile of the quads it has published
   // (common.cuh).  Otherwise: one CTA per tile after the binning completed.
@@ -772,8 +960,82 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     return;
   }
   const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
-  const int nbatches = (int)((e - s + TB_BATCH - 1) / TB_BATCH);
+  const bool coarse = !PREC && crow != nullptr;
+  const int nbatches = coarse ? 0x7fffffff : (int)((e - s + TB_BATCH - 1) / TB_BATCH);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+
+  if (warp == TB_CONSUMERS && coarse) {
+    // ------------------------------------------- producer, coarse-fed
+    // the super-tile's list in depth order; the entries whose rectangle
+    // covers this tile are this tile's list (fine_bin_kernel's filter), in
+    // order.  A batch takes rounds of 32 list entries while at most 32 of
+    // its 64 slots are filled; the next rounds' loads are in flight.
+    const int sup = (ty >> css) * sx_super + (tx >> css);
+    const uint32_t cb = counters[0] > 0 ? cstart[sup] : 0u, ce = counters[0] > 0 ? cstart[sup + 1] : 0u;
+    const uint32_t clast = ce > cb ? ce - 1 : cb;
+    constexpr int PD = 4;  // rounds in flight
+    uint2 rq[PD];
+    uint32_t gq[PD];
+#pragma unroll
+    for (int d = 0; d < PD; d++) {
+      const uint32_t i = min(cb + 32 * d + lane, clast);
+      rq[d] = __ldg(crect + i);
+      gq[d] = __ldg(crow + i);
+    }
+    uint32_t pos = cb;
+    int kcount = 0;
+    for (int b = 0;; b++) {
+      const int slot = b % TB_NSTAGE;
+      if (b >= TB_NSTAGE) warp_wait(&sm.empty[slot], ((b / TB_NSTAGE) - 1) & 1, lane);
+      if (*(volatile int*)&sm.done_warps == TB_CONSUMERS || pos >= ce) {
+        if (lane == 0) *(volatile int*)&sm.end_batch = b;
+        __syncwarp();
+        mbar_arrive(&sm.full[slot]);  // 32 plain arrivals complete the phase
+        break;
+      }
+      int filled = 0;
+      while (filled <= TB_BATCH - 32 && pos < ce) {
+        const uint32_t i = pos + lane;
+        const uint32_t lo = rq[0].x, hi = rq[0].y;  // (x0 | x1 << 16, y0 | y1 << 16)
+        const bool hit = i < ce && (int)(lo & 0xffffu) <= tx && tx <= (int)(lo >> 16) && (int)(hi & 0xffffu) <= ty &&
+                         ty <= (int)(hi >> 16);
+        const uint32_t g = gq[0];
+#pragma unroll
+        for (int d = 0; d < PD - 1; d++) rq[d] = rq[d + 1], gq[d] = gq[d + 1];
+        {
+          const uint32_t inext = min(pos + 32 * PD + lane, clast);
+          rq[PD - 1] = __ldg(crect + inext);
+          gq[PD - 1] = __ldg(crow + inext);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int j = filled + __popc(bal & lanemask_lt());
+          StageEntry* dst = &sm.ent[slot][j];
+          const char* src = reinterpret_cast<const char*>(rec + g);
+          const char* cs = reinterpret_cast<const char*>(cull + g);
+          cp_async16(&dst->a, src);
+          cp_async16(&dst->b, src + 16);
+          cp_async16(&dst->c, src + 32);
+          cp_async16(&dst->d, src + 48);
+          cp_async16(&dst->f.box, cs);
+          cp_async16(&dst->f.con, cs + 16);
+          cp_async16(&dst->f.col, cs + 32);
+          sm.gid[slot][j] = g;
+        }
+        filled += __popc(bal);
+        pos += 32;
+      }
+      if (lane == 0) {
+        sm.nbs[slot] = filled;
+        sm.kbase[slot] = kcount;
+      }
+      kcount += filled;
+      __syncwarp();
+      __threadfence_block();  // the slot's count / rows before the arrivals that publish it
+      cp_async_arrive_noinc(&sm.full[slot]);
+    }
+    return;
+  }
 
   if (warp == TB_CONSUMERS) {
     // ------------------------------------------------------------ producer
@@ -866,8 +1128,8 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       if (lane == 0) mbar_arrive(&sm.empty[slot]);
       continue;
     }
-    const int nb = (int)min((int64_t)TB_BATCH, e - (s + (int64_t)b * TB_BATCH));
-    const int bb = b * TB_BATCH;
+    const int nb = coarse ? sm.nbs[slot] : (int)min((int64_t)TB_BATCH, e - (s + (int64_t)b * TB_BATCH));
+    const int bb = coarse ? sm.kbase[slot] : b * TB_BATCH;
     // order-preserving compaction of the stage to the entries whose effective
     // ellipse touches the sub-tile, copied with their cut into the warp's
     // walk buffer; then the ring slot is released
@@ -887,10 +1149,12 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         W.a = S.a;
         W.b = make_double2(S.b.x * U_SCALE, S.b.y * U_SCALE);
         W.c = make_double2(S.c.x * U_SCALE, S.c.y);
-        if (PREC)
+        if (PREC) {
           W.alpha = S.d.x;
-        else
+        } else {
           W.a32 = fabsf(S.f.col.x);  // == |(float)alpha| (the cull record's sign only flags the conic)
+          W.row = coarse ? sm.gid[slot][i] : 0u;
+        }
         W.ucut = entry_ucut(S.f.col.x);
         W.k = bb + i;
         W.col = make_float4(S.f.col.y, S.f.col.z, S.f.col.w, S.f.con.w);
@@ -961,7 +1225,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
 #pragma unroll
         for (int h = 0; h < 2; h++)
           tb_slow<STATS, PREC>(q[h], E, fx, fy0 + 4.0 * h, mesh_here[h] ? mesh.depth + pix[h] : nullptr, uu[h],
-                               um[h], sg[h], dd[h], E.k, sm.exp2tab, rec, entries, s, walked, blended,
+                               um[h], sg[h], dd[h], E.k, sm.exp2tab, rec, coarse ? nullptr : entries, s, walked, blended,
                                &sm.tout[0][warp][h][lane]);
         if (__all_sync(0xffffffffu, q[0].done() && q[1].done())) break;
       }
@@ -1042,7 +1306,9 @@ __global__ void __launch_bounds__(256) blend_exact_kernel(
 __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
     const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
     int tiles_x, int n_tiles, int width, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
-    double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters, int* ready) {
+    double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters, int* ready,
+    const uint32_t* __restrict__ crow, const uint2* __restrict__ crect, const uint32_t* __restrict__ cstart, int css,
+    int sx_super) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (counters && counters[2]) return;  // overflowed bins: the blend wrote nothing
   const int lane = threadIdx.x & 31;
@@ -1096,8 +1362,15 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
     const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
     const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
     const double limit = mesh_here ? mesh.depth[p] : __longlong_as_double(0x7ff0000000000000LL);
-    const ExactPixel q = exact_walk2(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5,
-                                    limit, lane);
+    ExactPixel q;
+    if (crow) {  // blend-only bins: the tile's list is filtered out of its super-tile's coarse list
+      const int tx = px / BLEND_TILE, ty = py / BLEND_TILE;
+      const int sup = (ty >> css) * sx_super + (tx >> css);
+      q = exact_walk_coarse(rec, crow, crect, cstart[sup], cstart[sup + 1], tx, ty, tile_starts[tile], px + 0.5,
+                            py + 0.5, limit, lane);
+    } else {
+      q = exact_walk2(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5, limit, lane);
+    }
     if (lane == 0)
       write_pixel(out, mesh, mesh_here, p, q.T, q.r, q.g, q.b, q.dacc, 1.0 - q.T, q.last, bg0, bg1, bg2,
                   mask_variant, mask_k, q.T);
@@ -1185,16 +1458,24 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     // binned tile grids: claim tiles from the fine binning's ready queue (at
     // the scratch base, common.cuh), starting while the last quads are binned
     const int ss = super_shift(tiles->tiles_x, tiles->tiles_y);
-    const bool queued = ss >= 0 && HGS_BLEND_QUEUE && tiles->ready != nullptr;
+    // blend-only bins (hgs.h): the blend filters the coarse lists itself and
+    // starts behind the coarse scatter (there is no fine binning to queue on)
+    const bool coarse = ss >= 0 && (tiles->flags & HGS_TILES_BLEND_ONLY) && tiles->coarse_rows && !prec;
+    if ((tiles->flags & HGS_TILES_BLEND_ONLY) && !coarse)
+      return hgs_set_error(HGS_ERR_INVALID, "hgs_blend_forward: blend-only bins need a binned tile grid and no final_t");
+    const bool queued = !coarse && ss >= 0 && HGS_BLEND_QUEUE && tiles->ready != nullptr;
     int* ready = queued ? reinterpret_cast<int*>(tiles->ready) : nullptr;
     const int qs = queued ? ss - 2 : 0;
-    const int sxs = queued ? (tiles->tiles_x + (1 << ss) - 1) >> ss : 0;
+    const int sxs = (queued || coarse) ? (tiles->tiles_x + (1 << ss) - 1) >> ss : 0;
     const int sys = queued ? (tiles->tiles_y + (1 << ss) - 1) >> ss : 0;
     const int n_cta = queued ? (sxs * sys << (2 * qs)) * 16 : n_tiles;
+    const uint32_t* crow = coarse ? (const uint32_t*)tiles->coarse_rows : nullptr;
+    const uint2* crect = coarse ? (const uint2*)tiles->coarse_rects : nullptr;
+    const uint32_t* cstart = coarse ? (const uint32_t*)tiles->coarse_starts : nullptr;
     launch_pdl(fn, dim3(n_cta), dim3(TB_THREADS), tsmem, st, (const BlendRec*)proj->rec, (const CullRec*)proj->cull,
                (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, width, height, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
-               (const int64_t*)tiles->counters, ready, qs, sxs);
+               (const int64_t*)tiles->counters, ready, qs, sxs, crow, crect, cstart, coarse ? ss : 0);
 #endif
     HGS_CHECK_LAUNCH();
 #if HGS_BLEND_V1
@@ -1210,7 +1491,7 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     launch_pdl(blend_exact_queue_kernel, dim3(8 * NUM_SMS), dim3(64), 0, st, (const BlendRec*)proj->rec,
                (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_cta, width, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
-               (const int64_t*)tiles->counters, ready);
+               (const int64_t*)tiles->counters, ready, crow, crect, cstart, coarse ? ss : 0, sxs);
 #endif
     HGS_CHECK_LAUNCH();
   } else {

@@ -1552,6 +1552,9 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   cudaStream_t st = (cudaStream_t)stream;
   TilesScratch s;
   carve(n, tiles->capacity, tx, ty, (unsigned char*)tiles->scratch, &s);
+  tiles->coarse_rows = s.crow;
+  tiles->coarse_rects = s.crect;
+  tiles->coarse_starts = s.cstart;
   zero_pdl(st, s.control_begin, s.control_bytes, tiles->counters, 4 * sizeof(int64_t));
   HGS_CHECK_LAUNCH();
   // 1. order-preserving compaction of the visible rows' depth keys
@@ -1669,6 +1672,8 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     HGS_CHECK_LAUNCH();
     if (ss != 2 && ss != 3) return hgs_set_error(HGS_ERR_INVALID, "hgs_build_tiles: tile grid too large for binning");
     if (const int jr = join()) return jr;  // before the fine binning: the blend then depends on it alone
+    // blend-only bins: the blend reads the coarse lists itself (no entries)
+    if (tiles->flags & HGS_TILES_BLEND_ONLY) return HGS_OK;
     // 8x8 super-tiles: four 4x4-tile CTAs each (parallelism at 1080p)
     launch_pdl(fine_bin_kernel<4>, dim3(n_super << (2 * (ss - 2))), dim3(fine_warps(4) * 32), 0, st, s.crow,
                s.crect, s.cstart, tiles->tile_starts, tiles->counters, tiles->capacity, tx, ty, sx, tiles->entries,

@@ -15,6 +15,7 @@ automatically.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Optional
 
 import numpy as np
@@ -24,6 +25,9 @@ from . import _lib
 from .scene import CAMERA_BYTES, GaussianSet, TexturedMesh, camera_struct
 from .splat import (REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, TileBins, _c_f64_3,
                     MASK_VARIANTS)
+
+
+BLEND_ONLY_ENTRIES_PER_TILE = 8192  # average tile list beyond which the serving path skips the fine binning
 
 
 class HybridRenderer:
@@ -39,6 +43,14 @@ class HybridRenderer:
         self.tiles_y = (self.height + TILE_PX - 1) // TILE_PX
         self.n_tiles = self.tiles_x * self.tiles_y
         self.keep_state = keep_state
+        # blend-only bins (hgs.h HGS_TILES_BLEND_ONLY) for a pure serving
+        # renderer once the entry count is known: the fine binning writes every
+        # tile list in full, the coarse-fed blend reads only the prefix it
+        # walks but replays its exact pixels over the coarse lists.  Measured
+        # (one B200): c5 (17k entries / tile) 2.55 vs 2.93 ms, c3 (4.1k) 815 vs
+        # 805 us -- so by the average list length (HGS_BLEND_ONLY=0/1 forces)
+        self._blend_only_env = os.environ.get("HGS_BLEND_ONLY")
+        self.blend_only = not keep_state and self._blend_only_env == "1"
         self.mask = mask
         dev = self.dev
         n = max(len(gs), 1)
@@ -164,6 +176,11 @@ class HybridRenderer:
         ts.entries, ts.tile_starts, ts.counters = _lib.ptr(self.entries), _lib.ptr(self.tile_starts), _lib.ptr(self.counters)
         ts.scratch, ts.scratch_bytes = _lib.ptr(self.tiles_scratch), self.tiles_scratch.numel()
         ts.ready = _lib.ptr(self.ready)
+        # a pure serving renderer (no backward state) needs only the images:
+        # blend-only bins skip the fine binning, the blend filters the
+        # super-tile lists itself and reads only the prefix it walks (hgs.h)
+        if self.blend_only:
+            ts.flags = _lib.TILES_BLEND_ONLY
         return ps, ts
 
     def enqueue(self, rasterize_mesh: bool = True, mesh_layer: Optional[MeshLayer] = None, out_set: int = 0) -> None:
@@ -235,6 +252,8 @@ class HybridRenderer:
         m, k, ovf = (int(x) for x in self.counters_host[:3])
         if ovf:
             self._alloc_entries(int(k * 1.25) + 1024)
+        if not self.keep_state and self._blend_only_env is None:
+            self.blend_only = k > BLEND_ONLY_ENTRIES_PER_TILE * self.tiles_x * self.tiles_y
         return m, k, bool(ovf)
 
     def frame(self, cam, rasterize_mesh: bool = True, sync_check: bool = True):
@@ -302,6 +321,9 @@ class HybridRenderer:
                                   self.height, TILE_PX, self.cull, self.sort_keys, self.tile_diff)
 
     def tiles(self) -> TileBins:
+        if self.blend_only:
+            raise RuntimeError("HybridRenderer(keep_state=False) builds blend-only bins (no tile entries): "
+                               "use keep_state=True for TileBins / the backward")
         return TileBins(self.tile_starts, self.entries, self.tiles_x, self.tiles_y, TILE_PX, self.projected(),
                         counters=self.counters, capacity=int(self.entries.numel()), ready=self.ready)
 

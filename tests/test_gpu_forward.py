@@ -337,6 +337,43 @@ def test_engine_render_to_host_matches_functional_render(cuda_device):
         assert torch.equal(ht, out.transmittance.cpu())
 
 
+@pytest.mark.parametrize("cfg,wh", [("c4", None), ("c2", (3840, 2160))])
+def test_blend_only_bins_match_full_bins(cfg, wh, cuda_device, monkeypatch):
+    """Blend-only bins (hgs.h HGS_TILES_BLEND_ONLY): no fine binning, the blend
+    filters every tile's list out of its super-tile's coarse list (and the
+    exact replay of ambiguous pixels walks the coarse list).  The images are
+    bit-identical to the fully binned frame -- at 1200x680 (4x4-tile
+    super-tiles) and at 4K (8x8-tile super-tiles) -- with pixels replayed
+    exactly among them."""
+    import paper_2506_06988_b200 as hgs
+    from paper_2506_06988_b200 import synthetic as syn
+    from paper_2506_06988_b200.engine import HybridRenderer
+    sc = syn.make_config(cfg, seed=0) if cfg != "c4" else syn.make_config("c4", seed=0, n_views=2)
+    g = hgs.GaussianSet.from_any(sc.gaussians)
+    m = hgs.TexturedMesh.from_any(sc.mesh)
+    c = hgs.Camera.from_any(sc.cameras[0])
+    if wh is not None:
+        eye = np.asarray(sc.cameras[0].center())
+        cam = syn.look_at(eye, eye + np.asarray(sc.cameras[0].world_to_camera)[2, :3], width=wh[0], height=wh[1])
+        c = hgs.Camera.from_any(cam)
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HGS_BLEND_ONLY", mode)
+        r = HybridRenderer(g, m, c.width, c.height, collect_stats=True)
+        r.frame(c, sync_check=True)
+        r.stats.zero_()
+        r.frame(c, sync_check=True)
+        torch.cuda.synchronize()
+        assert r.blend_only == (mode == "1")
+        outs[mode] = (r.color.clone(), r.depth.clone(), r.trans.clone(), int(r.stats[2]))
+    (c0, d0, t0, f0), (c1, d1, t1, f1) = outs["0"], outs["1"]
+    assert torch.equal(c0, c1) and torch.equal(t0, t1)
+    assert torch.equal(d0.isnan(), d1.isnan()) and torch.equal(torch.nan_to_num(d0), torch.nan_to_num(d1))
+    assert f0 == f1
+    if cfg == "c4":
+        assert f1 > 0  # the coarse-list exact replay ran
+
+
 @pytest.mark.parametrize("view", [0, 17])
 def test_c4_training_view_matches_oracle(view, cuda_device):
     """A c4 training camera inside the room (1M Gaussians, most rows culled:
