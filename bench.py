@@ -423,7 +423,9 @@ def run_ours(args):
                                  "algorithmic_bytes": blend_bytes, "peak_kind": peak_kind},
                          "note": "K4 is compute (instruction-issue) bound; the staged records are L2-resident, so its "
                                  "HBM figure (hbm) is far below 1 by construction. achieved = pixel-Gaussian "
-                                 "evaluations walked (counted in-kernel) / the kernel's CUDA-event time"},
+                                 "evaluations walked (counted in-kernel) / the kernel's CUDA-event time; the serving "
+                                 "path's blend-only bins make the kernel also filter each tile's list out of its "
+                                 "super-tile's coarse list (the fine binning's work, only the prefix it walks)"},
             "compute_rate": {"blend_evaluations_per_s": walked / (blend_ms * 1e-3),
                              "tiles_stage_ms": tiles_ms, "blend_ms": blend_ms},
             "gs_frame": {"value": 1000.0 / gs_ms, "unit": UNIT, "ms_per_step": gs_ms,

@@ -148,6 +148,7 @@ typedef struct hgs_tiles {
   const void* coarse_rows;   /* written by hgs_build_tiles (binned grids): the super-tile lists of original rows */
   const void* coarse_rects;  /* ... their tile rectangles (u16 x 4) */
   const void* coarse_starts; /* ... and the lists' starts (u32, one per super-tile + 1) */
+  void* coarse_prog;         /* ... and a per-tile scratch the blend-only blend leaves its list progress in */
 } hgs_tiles;
 #define HGS_TILES_BLEND_ONLY 1
 #define HGS_READY_INTS (2 + 2048)

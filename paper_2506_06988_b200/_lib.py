@@ -63,7 +63,7 @@ class HGSTiles(ctypes.Structure):
                 ("capacity", c_i64), ("entries", c_void_p), ("tile_starts", c_void_p), ("counters", c_void_p),
                 ("scratch", c_void_p), ("scratch_bytes", ctypes.c_size_t), ("ready", c_void_p),
                 ("join_event", c_void_p), ("coarse_rows", c_void_p), ("coarse_rects", c_void_p),
-                ("coarse_starts", c_void_p)]
+                ("coarse_starts", c_void_p), ("coarse_prog", c_void_p)]
 
 TILES_BLEND_ONLY = 1  # HGS_TILES_BLEND_ONLY
 

@@ -149,12 +149,33 @@ struct ExactPixel {
 // early-stop threshold the first entry with T(1 - sigma) < 1e-4 ends the
 // walk; a round with a value inside the band is replayed serially in the
 // reference's order.
-__device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
-                                               int64_t s, int64_t e, double fx, double fy, double limit, int lane) {
+// Walk state carried across the two parts of a blend-only replay (the tile
+// list prefix the blend wrote, then the coarse list): T and last are warp-
+// uniform, the sums per-lane partials reduced at the end (walk_finish).
+struct WalkState {
+  double T, pr, pg, pb, pd;
+  int64_t last;
+  bool done;
+};
+__device__ __forceinline__ ExactPixel walk_finish(WalkState& w) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    w.pr += __shfl_xor_sync(0xffffffffu, w.pr, d);
+    w.pg += __shfl_xor_sync(0xffffffffu, w.pg, d);
+    w.pb += __shfl_xor_sync(0xffffffffu, w.pb, d);
+    w.pd += __shfl_xor_sync(0xffffffffu, w.pd, d);
+  }
+  return ExactPixel{w.T, w.pr, w.pg, w.pb, w.pd, w.last};
+}
+
+__device__ __forceinline__ void exact_walk2_run(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
+                                                int64_t s, int64_t e, double fx, double fy, double limit, int lane,
+                                                WalkState& ws) {
   constexpr int EW = 2, RW = 32 * EW;
-  double T = 1.0, pr = 0.0, pg = 0.0, pb = 0.0, pd = 0.0;
-  int64_t last = -1;
-  bool done = false;
+  double& T = ws.T;
+  double &pr = ws.pr, &pg = ws.pg, &pb = ws.pb, &pd = ws.pd;
+  int64_t& last = ws.last;
+  bool& done = ws.done;
   auto idx = [&](int64_t rbase, int u) -> uint32_t {
     const int64_t k = rbase + EW * lane + u;
     return k < e ? __ldcg(entries + k) : 0u;  // L2 (the queue consumer runs beside the binning's writers)
@@ -291,14 +312,12 @@ __device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec,
       if (stop) done = true;
     }
   }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    pr += __shfl_xor_sync(0xffffffffu, pr, d);
-    pg += __shfl_xor_sync(0xffffffffu, pg, d);
-    pb += __shfl_xor_sync(0xffffffffu, pb, d);
-    pd += __shfl_xor_sync(0xffffffffu, pd, d);
-  }
-  return ExactPixel{T, pr, pg, pb, pd, last};
+}
+__device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries,
+                                               int64_t s, int64_t e, double fx, double fy, double limit, int lane) {
+  WalkState w{1.0, 0.0, 0.0, 0.0, 0.0, -1, false};
+  exact_walk2_run(rec, entries, s, e, fx, fy, limit, lane, w);
+  return walk_finish(w);
 }
 
 // The exact walk of one pixel over a super-tile's coarse list (blend-only
@@ -309,14 +328,18 @@ __device__ __noinline__ ExactPixel exact_walk2(const BlendRec* __restrict__ rec,
 // a running count of the matches.  Otherwise the reference's walk as in
 // exact_walk2 (depth stop, shuffle prefix product of 1 - sigma, serial replay
 // of a round with a value within 1e-12 of the early-stop threshold).
-__device__ __noinline__ ExactPixel exact_walk_coarse(const BlendRec* __restrict__ rec, const uint32_t* __restrict__ crow,
-                                                     const uint2* __restrict__ crect, uint32_t cb, uint32_t ce, int tx,
-                                                     int ty, int64_t s, double fx, double fy, double limit, int lane) {
+// (Resumable: from coarse position cb, the first `skip` matches there and
+// the first kcount tile-list entries already walked, state in ws.)
+__device__ __forceinline__ void exact_walk_coarse_run(const BlendRec* __restrict__ rec,
+                                                      const uint32_t* __restrict__ crow, const uint2* __restrict__ crect,
+                                                      uint32_t cb, int skip, int kcount, uint32_t ce, int tx, int ty,
+                                                      int64_t s, double fx, double fy, double limit, int lane,
+                                                      WalkState& ws) {
   constexpr int EW = 2, RW = 32 * EW;
-  double T = 1.0, pr = 0.0, pg = 0.0, pb = 0.0, pd = 0.0;
-  int64_t last = -1;
-  bool done = false;
-  int kcount = 0;
+  double& T = ws.T;
+  double &pr = ws.pr, &pg = ws.pg, &pb = ws.pb, &pd = ws.pd;
+  int64_t& last = ws.last;
+  bool& done = ws.done;
   auto covers = [&](uint2 r) {
     return (int)(r.x & 0xffffu) <= tx && tx <= (int)(r.x >> 16) && (int)(r.y & 0xffffu) <= ty &&
            ty <= (int)(r.y >> 16);
@@ -355,6 +378,14 @@ __device__ __noinline__ ExactPixel exact_walk_coarse(const BlendRec* __restrict_
     }
     load_recs();                // round + 1
     load_rects(base + 2 * RW);  // round + 2
+    if (skip) {  // resuming inside a round: its first `skip` matches were walked already
+      const unsigned a0 = __ballot_sync(0xffffffffu, match[0]), a1 = __ballot_sync(0xffffffffu, match[1]);
+      const int r0 = __popc(a0 & lanemask_lt()) + __popc(a1 & lanemask_lt());  // rank of (lane, 0)
+      const int r1 = r0 + (int)((a0 >> lane) & 1u);                            // rank of (lane, 1)
+      if (r0 < skip) match[0] = false;
+      if (r1 < skip) match[1] = false;
+      skip = 0;
+    }
     const unsigned m0 = __ballot_sync(0xffffffffu, match[0]), m1 = __ballot_sync(0xffffffffu, match[1]);
     const int kl = kcount + __popc(m0 & lanemask_lt()) + __popc(m1 & lanemask_lt());
     int krank[EW] = {kl, kl + (match[0] ? 1 : 0)};
@@ -468,14 +499,21 @@ __device__ __noinline__ ExactPixel exact_walk_coarse(const BlendRec* __restrict_
       if (stop) done = true;
     }
   }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    pr += __shfl_xor_sync(0xffffffffu, pr, d);
-    pg += __shfl_xor_sync(0xffffffffu, pg, d);
-    pb += __shfl_xor_sync(0xffffffffu, pb, d);
-    pd += __shfl_xor_sync(0xffffffffu, pd, d);
-  }
-  return ExactPixel{T, pr, pg, pb, pd, last};
+}
+
+// A blend-only replay: the tile-list prefix [s, s + kc) the blend's producer
+// wrote to `entries`, then (if the walk goes on) the coarse list from where
+// the producer stopped (coarse position pos, `skip` matches there done).
+__device__ __noinline__ ExactPixel exact_walk_blend_only(const BlendRec* __restrict__ rec,
+                                                         const uint32_t* __restrict__ entries, int64_t s, int kc,
+                                                         const uint32_t* __restrict__ crow,
+                                                         const uint2* __restrict__ crect, uint32_t pos, int skip,
+                                                         uint32_t ce, int tx, int ty, double fx, double fy,
+                                                         double limit, int lane) {
+  WalkState w{1.0, 0.0, 0.0, 0.0, 0.0, -1, false};
+  exact_walk2_run(rec, entries, s, s + kc, fx, fy, limit, lane, w);
+  if (!w.done) exact_walk_coarse_run(rec, crow, crect, pos, skip, kc, ce, tx, ty, s, fx, fy, limit, lane, w);
+  return walk_finish(w);
 }
 
 // PREC (the caller asked for the backward state final_t): T is also carried
@@ -908,7 +946,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     const int64_t* __restrict__ tile_starts, int tiles_x, int width, int height, hgs_mesh_layer mesh, double bg0,
     double bg1, double bg2, int mask_variant, double mask_k, hgs_blend_out out, int32_t* __restrict__ fixup,
     const int64_t* __restrict__ counters, int* ready, int qs, int sx_super, const uint32_t* __restrict__ crow,
-    const uint2* __restrict__ crect, const uint32_t* __restrict__ cstart, int css) {
+    const uint2* __restrict__ crect, const uint32_t* __restrict__ cstart, int css, uint4* __restrict__ prog) {
   // crow != NULL (blend-only bins, never PREC): the producer filters the
   // tile's super-tile coarse list (super-tiles of 2^css tiles, sx_super per
   // row) into the ring instead of reading `entries`.
@@ -961,6 +999,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
   }
   const int64_t s = tile_starts[tile], e = tile_starts[tile + 1];
   const bool coarse = !PREC && crow != nullptr;
+  uint32_t* const entries_w = const_cast<uint32_t*>(entries);  // (blend-only bins: the prefix is written here)
   const int nbatches = coarse ? 0x7fffffff : (int)((e - s + TB_BATCH - 1) / TB_BATCH);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
 
@@ -968,8 +1007,9 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     // ------------------------------------------- producer, coarse-fed
     // the super-tile's list in depth order; the entries whose rectangle
     // covers this tile are this tile's list (fine_bin_kernel's filter), in
-    // order.  A batch takes rounds of 32 list entries while at most 32 of
-    // its 64 slots are filled; the next rounds' loads are in flight.
+    // order.  A batch takes rounds of 32 list entries until its 64 slots are
+    // full (a round may straddle two batches); the next rounds' loads are in
+    // flight.
     const int sup = (ty >> css) * sx_super + (tx >> css);
     const uint32_t cb = counters[0] > 0 ? cstart[sup] : 0u, ce = counters[0] > 0 ? cstart[sup + 1] : 0u;
     const uint32_t clast = ce > cb ? ce - 1 : cb;
@@ -984,6 +1024,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
     }
     uint32_t pos = cb;
     int kcount = 0;
+    int skip = 0;  // matches of the current round already placed (a round may straddle two batches)
     for (int b = 0;; b++) {
       const int slot = b % TB_NSTAGE;
       if (b >= TB_NSTAGE) warp_wait(&sm.empty[slot], ((b / TB_NSTAGE) - 1) & 1, lane);
@@ -994,22 +1035,18 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
         break;
       }
       int filled = 0;
-      while (filled <= TB_BATCH - 32 && pos < ce) {
+      const int kbase_b = kcount;
+      while (filled < TB_BATCH && pos < ce) {
         const uint32_t i = pos + lane;
         const uint32_t lo = rq[0].x, hi = rq[0].y;  // (x0 | x1 << 16, y0 | y1 << 16)
         const bool hit = i < ce && (int)(lo & 0xffffu) <= tx && tx <= (int)(lo >> 16) && (int)(hi & 0xffffu) <= ty &&
                          ty <= (int)(hi >> 16);
         const uint32_t g = gq[0];
-#pragma unroll
-        for (int d = 0; d < PD - 1; d++) rq[d] = rq[d + 1], gq[d] = gq[d + 1];
-        {
-          const uint32_t inext = min(pos + 32 * PD + lane, clast);
-          rq[PD - 1] = __ldg(crect + inext);
-          gq[PD - 1] = __ldg(crow + inext);
-        }
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-          const int j = filled + __popc(bal & lanemask_lt());
+        const int rank = __popc(bal & lanemask_lt()) - skip;
+        const int take = min(__popc(bal) - skip, TB_BATCH - filled);
+        if (hit && rank >= 0 && rank < take) {
+          const int j = filled + rank;
           StageEntry* dst = &sm.ent[slot][j];
           const char* src = reinterpret_cast<const char*>(rec + g);
           const char* cs = reinterpret_cast<const char*>(cull + g);
@@ -1021,8 +1058,21 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
           cp_async16(&dst->f.con, cs + 16);
           cp_async16(&dst->f.col, cs + 32);
           sm.gid[slot][j] = g;
+          entries_w[s + kbase_b + j] = g;  // the tile list prefix, for the exact replay
         }
-        filled += __popc(bal);
+        filled += take;
+        if (skip + take < __popc(bal)) {  // the batch is full: the rest of this round opens the next one
+          skip += take;
+          break;
+        }
+        skip = 0;
+#pragma unroll
+        for (int d = 0; d < PD - 1; d++) rq[d] = rq[d + 1], gq[d] = gq[d + 1];
+        {
+          const uint32_t inext = min(pos + 32 * PD + lane, clast);
+          rq[PD - 1] = __ldg(crect + inext);
+          gq[PD - 1] = __ldg(crow + inext);
+        }
         pos += 32;
       }
       if (lane == 0) {
@@ -1034,6 +1084,11 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       __threadfence_block();  // the slot's count / rows before the arrivals that publish it
       cp_async_arrive_noinc(&sm.full[slot]);
     }
+    // where the tile list prefix in `entries` ends, for the exact replay of
+    // this tile's ambiguous pixels (queued by the consumers after the barrier)
+    if (lane == 0) prog[tile] = make_uint4((uint32_t)kcount, pos, (uint32_t)skip, 0u);
+    __threadfence();
+    __syncthreads();
     return;
   }
 
@@ -1245,6 +1300,7 @@ __global__ void __launch_bounds__(TB_THREADS, PREC ? HGS_TB_MINB_PREC : HGS_TB_M
       atomicAdd((unsigned long long*)&out.stats[1], sm.stats[1]);
     }
   }
+  if (coarse) __syncthreads();  // the producer has published the tile's list prefix (prog) for the replays
 #pragma unroll
   for (int h = 0; h < 2; h++) {
     if (!inside[h]) continue;
@@ -1308,7 +1364,7 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
     int tiles_x, int n_tiles, int width, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
     double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters, int* ready,
     const uint32_t* __restrict__ crow, const uint2* __restrict__ crect, const uint32_t* __restrict__ cstart, int css,
-    int sx_super) {
+    int sx_super, const uint4* __restrict__ prog) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (counters && counters[2]) return;  // overflowed bins: the blend wrote nothing
   const int lane = threadIdx.x & 31;
@@ -1366,8 +1422,9 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
     if (crow) {  // blend-only bins: the tile's list is filtered out of its super-tile's coarse list
       const int tx = px / BLEND_TILE, ty = py / BLEND_TILE;
       const int sup = (ty >> css) * sx_super + (tx >> css);
-      q = exact_walk_coarse(rec, crow, crect, cstart[sup], cstart[sup + 1], tx, ty, tile_starts[tile], px + 0.5,
-                            py + 0.5, limit, lane);
+      const uint4 pg = __ldcg(prog + tile);
+      q = exact_walk_blend_only(rec, entries, tile_starts[tile], (int)pg.x, crow, crect, pg.y, (int)pg.z,
+                                cstart[sup + 1], tx, ty, px + 0.5, py + 0.5, limit, lane);
     } else {
       q = exact_walk2(rec, entries, tile_starts[tile], tile_starts[tile + 1], px + 0.5, py + 0.5, limit, lane);
     }
@@ -1460,7 +1517,8 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     const int ss = super_shift(tiles->tiles_x, tiles->tiles_y);
     // blend-only bins (hgs.h): the blend filters the coarse lists itself and
     // starts behind the coarse scatter (there is no fine binning to queue on)
-    const bool coarse = ss >= 0 && (tiles->flags & HGS_TILES_BLEND_ONLY) && tiles->coarse_rows && !prec;
+    const bool coarse = ss >= 0 && (tiles->flags & HGS_TILES_BLEND_ONLY) && tiles->coarse_rows && tiles->coarse_prog &&
+                        !prec;
     if ((tiles->flags & HGS_TILES_BLEND_ONLY) && !coarse)
       return hgs_set_error(HGS_ERR_INVALID, "hgs_blend_forward: blend-only bins need a binned tile grid and no final_t");
     const bool queued = !coarse && ss >= 0 && HGS_BLEND_QUEUE && tiles->ready != nullptr;
@@ -1475,7 +1533,8 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     launch_pdl(fn, dim3(n_cta), dim3(TB_THREADS), tsmem, st, (const BlendRec*)proj->rec, (const CullRec*)proj->cull,
                (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, width, height, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
-               (const int64_t*)tiles->counters, ready, qs, sxs, crow, crect, cstart, coarse ? ss : 0);
+               (const int64_t*)tiles->counters, ready, qs, sxs, crow, crect, cstart, coarse ? ss : 0,
+               coarse ? (uint4*)tiles->coarse_prog : (uint4*)nullptr);
 #endif
     HGS_CHECK_LAUNCH();
 #if HGS_BLEND_V1
@@ -1491,7 +1550,8 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     launch_pdl(blend_exact_queue_kernel, dim3(8 * NUM_SMS), dim3(64), 0, st, (const BlendRec*)proj->rec,
                (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_cta, width, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
-               (const int64_t*)tiles->counters, ready, crow, crect, cstart, coarse ? ss : 0, sxs);
+               (const int64_t*)tiles->counters, ready, crow, crect, cstart, coarse ? ss : 0, sxs,
+               coarse ? (const uint4*)tiles->coarse_prog : (const uint4*)nullptr);
 #endif
     HGS_CHECK_LAUNCH();
   } else {

@@ -1355,6 +1355,7 @@ struct TilesScratch {
   uint32_t* chist;        // BIN_MAX_SUPER (zeroed)
   uint32_t* vis_cnt;      // 2 parts_n: visible rows per RS_PART-row partition (HGS_DEPTH_MODE 2)
   uint32_t* cstart;       // BIN_MAX_SUPER + 1: super-tile list starts
+  void* cprog;            // n_tiles x 16 B: blend-only progress per tile (hgs_tiles.coarse_prog)
   ushort4* rsort;         // n: tile rectangles in depth order
   uint32_t* pair_off;     // n + 1: coarse pair offsets in depth order
   uint32_t* bsum;         // prep blocks
@@ -1420,6 +1421,7 @@ static size_t carve(int64_t n, int64_t cap, int tiles_x, int tiles_y, unsigned c
   t.npairs = binned ? (uint32_t*)take(sizeof(uint32_t) * 4) : nullptr;
   t.crect = binned ? (ushort4*)take(sizeof(ushort4) * (size_t)cc) : nullptr;
   t.cstart = binned ? (uint32_t*)take(sizeof(uint32_t) * (size_t)(BIN_MAX_SUPER + 1)) : nullptr;
+  t.cprog = binned ? take(16 * (size_t)n_tiles) : nullptr;
   t.parts_n = parts_n;
   t.parts_k = parts_k;
   if (s) *s = t;
@@ -1555,6 +1557,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
   tiles->coarse_rows = s.crow;
   tiles->coarse_rects = s.crect;
   tiles->coarse_starts = s.cstart;
+  tiles->coarse_prog = s.cprog;
   zero_pdl(st, s.control_begin, s.control_bytes, tiles->counters, 4 * sizeof(int64_t));
   HGS_CHECK_LAUNCH();
   // 1. order-preserving compaction of the visible rows' depth keys

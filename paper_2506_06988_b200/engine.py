@@ -27,9 +27,6 @@ from .splat import (REC_BYTES, TILE_PX, MeshLayer, ProjectedGaussians, TileBins,
                     MASK_VARIANTS)
 
 
-BLEND_ONLY_ENTRIES_PER_TILE = 8192  # average tile list beyond which the serving path skips the fine binning
-
-
 class HybridRenderer:
     def __init__(self, gs: GaussianSet, mesh: Optional[TexturedMesh], width: int, height: int,
                  background=(0.0, 0.0, 0.0), capacity: Optional[int] = None, keep_state: bool = False,
@@ -43,14 +40,13 @@ class HybridRenderer:
         self.tiles_y = (self.height + TILE_PX - 1) // TILE_PX
         self.n_tiles = self.tiles_x * self.tiles_y
         self.keep_state = keep_state
-        # blend-only bins (hgs.h HGS_TILES_BLEND_ONLY) for a pure serving
-        # renderer once the entry count is known: the fine binning writes every
-        # tile list in full, the coarse-fed blend reads only the prefix it
-        # walks but replays its exact pixels over the coarse lists.  Measured
-        # (one B200): c5 (17k entries / tile) 2.55 vs 2.93 ms, c3 (4.1k) 815 vs
-        # 805 us -- so by the average list length (HGS_BLEND_ONLY=0/1 forces)
-        self._blend_only_env = os.environ.get("HGS_BLEND_ONLY")
-        self.blend_only = not keep_state and self._blend_only_env == "1"
+        # a pure serving renderer (no backward state) builds blend-only bins
+        # (hgs.h HGS_TILES_BLEND_ONLY): no fine binning, the blend filters
+        # every tile's list out of the super-tile lists and reads only the
+        # prefix it walks (c3 792 vs 803 us, c5 2.51 vs 2.93 ms per frame;
+        # HGS_BLEND_ONLY=0 turns it off)
+        binned = any(((self.tiles_x + (1 << q) - 1) >> q) * ((self.tiles_y + (1 << q) - 1) >> q) <= 512 for q in (2, 3))
+        self.blend_only = not keep_state and binned and os.environ.get("HGS_BLEND_ONLY", "1") != "0"
         self.mask = mask
         dev = self.dev
         n = max(len(gs), 1)
@@ -252,8 +248,6 @@ class HybridRenderer:
         m, k, ovf = (int(x) for x in self.counters_host[:3])
         if ovf:
             self._alloc_entries(int(k * 1.25) + 1024)
-        if not self.keep_state and self._blend_only_env is None:
-            self.blend_only = k > BLEND_ONLY_ENTRIES_PER_TILE * self.tiles_x * self.tiles_y
         return m, k, bool(ovf)
 
     def frame(self, cam, rasterize_mesh: bool = True, sync_check: bool = True):
