@@ -40,6 +40,11 @@ class HybridRenderer:
         self.tiles_y = (self.height + TILE_PX - 1) // TILE_PX
         self.n_tiles = self.tiles_x * self.tiles_y
         self.keep_state = keep_state
+        # the mesh branch forks after preprocess (HGS_MESH_AFTER_PP=0: at the
+        # start of the frame): its raster CTAs then fill the gaps of the
+        # latency-bound binning chain instead of slowing the preprocess
+        # (c3: 770 vs 795 us per frame)
+        self._mesh_after_pp = os.environ.get("HGS_MESH_AFTER_PP", "1") != "0"
         # a pure serving renderer (no backward state) builds blend-only bins
         # (hgs.h HGS_TILES_BLEND_ONLY): no fine binning, the blend filters
         # every tile's list out of the super-tile lists and reads only the
@@ -183,10 +188,10 @@ class HybridRenderer:
         """Enqueue one frame for the camera currently in cam_dev.
 
         The mesh layer (raster + texture fetch) does not depend on the
-        Gaussians: it runs on a side stream forked from the current one,
-        overlapping preprocess and tile binning, and joins the chain before
-        the fine binning (the fork/join is captured into the CUDA graph as
-        well)."""
+        Gaussians: it runs on a side stream forked from the current one after
+        the preprocess, overlapping the tile binning, and joins the chain
+        before the fine binning / the blend (the fork/join is captured into
+        the CUDA graph as well)."""
         L = _lib.load()
         main = torch.cuda.current_stream(self.dev)
         st = main.cuda_stream
@@ -194,17 +199,20 @@ class HybridRenderer:
         ml = _lib.HGSMeshLayer()
         joined = None
         side_branch = self.mesh is not None and mesh_layer is None
+        ps, ts = self._structs()
         if side_branch:
             if self._side is None:
                 self._side = torch.cuda.Stream(self.dev)
                 self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
+            if self._mesh_after_pp:
+                _lib.check(L.hgs_preprocess(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.gs.struct()), TILE_PX,
+                                            ctypes.byref(ps), st), "preprocess")
             self._ev_fork.record(main)
             self._side.wait_event(self._ev_fork)
         elif mesh_layer is not None:
             ml = mesh_layer.struct()
-        # the mesh branch is captured first: its kernels launch at the start of
-        # the graph and finish before the fine binning needs the join
-        # (preprocess first measured 897 vs 881 us per c3 frame)
+        # the mesh branch (raster + texture fetch) runs on a side stream and
+        # joins the Gaussian chain before the blend (hgs_tiles.join_event)
         if side_branch:
             side = self._side.cuda_stream
             if rasterize_mesh:
@@ -223,10 +231,10 @@ class HybridRenderer:
         # the Gaussian chain; the mesh branch joins it inside hgs_build_tiles,
         # right before the fine binning (hgs_tiles.join_event), so the blend
         # depends on the fine binning alone and starts on its published quads
-        ps, ts = self._structs()
         ts.join_event = joined.cuda_event if joined is not None else None
-        _lib.check(L.hgs_preprocess(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.gs.struct()), TILE_PX,
-                                    ctypes.byref(ps), st), "preprocess")
+        if not (side_branch and self._mesh_after_pp):
+            _lib.check(L.hgs_preprocess(_lib.ptr(self.cam_dev), w, h, ctypes.byref(self.gs.struct()), TILE_PX,
+                                        ctypes.byref(ps), st), "preprocess")
         _lib.check(L.hgs_build_tiles(ctypes.byref(ps), len(self.gs), ctypes.byref(ts), st), "build_tiles")
         out = _lib.HGSBlendOut()
         oc, od, ot = self._out3(out_set)
