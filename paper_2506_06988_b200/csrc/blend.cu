@@ -1514,7 +1514,7 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
                          : (prec ? blend_tile_kernel<false, true> : blend_tile_kernel<false, false>);
     // binned tile grids: claim tiles from the fine binning's ready queue (at
     // the scratch base, common.cuh), starting while the last quads are binned
-    const int ss = super_shift(tiles->tiles_x, tiles->tiles_y);
+    const int ss = super_shift(tiles->tiles_x, tiles->tiles_y, (tiles->flags & HGS_TILES_BLEND_ONLY) != 0);
     // blend-only bins (hgs.h): the blend filters the coarse lists itself and
     // starts behind the coarse scatter (there is no fine binning to queue on)
     const bool coarse = ss >= 0 && (tiles->flags & HGS_TILES_BLEND_ONLY) && tiles->coarse_rows && tiles->coarse_prog &&

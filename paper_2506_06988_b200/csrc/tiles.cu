@@ -1576,7 +1576,8 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     HGS_CHECK_LAUNCH();
   }
   // 2. per-tile counts -> tile_starts, K, overflow, tile-key histograms
-  const int ss_all = super_shift(tx, ty);
+  const bool blend_only = (tiles->flags & HGS_TILES_BLEND_ONLY) != 0;
+  const int ss_all = super_shift(tx, ty, blend_only);
   const int n_quads_all = ss_all >= 0 ? (((tx + (1 << ss_all) - 1) >> ss_all) * ((ty + (1 << ss_all) - 1) >> ss_all))
                                             << (2 * (ss_all - 2))
                                       : 0;
@@ -1630,7 +1631,7 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
       dim3(4 * sm_count()), dim3(256), 0, st, k32res, rows, (const uint64_t*)proj->sort_keys, tiles->counters,
                                                      minmax);
   HGS_CHECK_LAUNCH();
-  const int ss = super_shift(tx, ty);
+  const int ss = super_shift(tx, ty, blend_only);
   if (ss >= 0) {
     // 4. two-level rect binning straight into the final (tile, depth, row) order
     const int sx = (tx + (1 << ss) - 1) >> ss, sy = (ty + (1 << ss) - 1) >> ss, n_super = sx * sy;
