@@ -1434,6 +1434,274 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
   }
 }
 
+// CTA-parallel exact replay (one CTA of EXW warps per queued pixel): a
+// replay is one warp's sequential walk of up to ~1000 entries (~24 us on
+// average at c3), and the last replays are the frame's tail.  Here the warps
+// take interleaved rounds of 64 entries: each evaluates its round (records,
+// fp64 exp, depth stop, the in-round prefix products) in parallel, then the
+// rounds are committed in order, warp after warp, with the T the previous
+// round left -- the same arithmetic per round as exact_walk2.  Blend-only
+// bins: the tile-list prefix in `entries`, then warp 0 continues over the
+// coarse list (exact_walk_coarse_run).
+constexpr int EXW = 4;
+__global__ void __launch_bounds__(EXW * 32) blend_exact_cta_kernel(
+    const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
+    int tiles_x, int n_tiles, int width, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
+    double mask_k, hgs_blend_out out, int32_t* fixup, const int64_t* __restrict__ counters, int* ready,
+    const uint32_t* __restrict__ crow, const uint2* __restrict__ crect, const uint32_t* __restrict__ cstart, int css,
+    int sx_super, const uint4* __restrict__ prog) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (counters && counters[2]) return;  // overflowed bins: the blend wrote nothing
+  constexpr int EW = 2, RW = 32 * EW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  volatile int32_t* vf = fixup;
+  __shared__ int s_claim, s_quit;
+  __shared__ double s_T;
+  __shared__ long long s_last;
+  __shared__ int s_done;
+  __shared__ double s_sum[EXW][4];
+  struct Leave {  // the last CTA to leave puts the queue back to zero (zero at rest)
+    int32_t* f;
+    int* r;
+    int tid, n;
+    __device__ ~Leave() {
+      if (tid == 0 && atomicAdd(&f[FIX_EXITED], 1) == n - 1) {
+        f[FIX_RESERVED] = 0;
+        f[FIX_DONE] = 0;
+        f[FIX_CLAIMED] = 0;
+        f[FIX_EXITED] = 0;
+        if (r) r[1] = 0;
+        __threadfence();
+      }
+    }
+  } leave{fixup, ready, tid, (int)gridDim.x};
+  while (true) {
+    if (tid == 0) {
+      int idx = atomicAdd(&fixup[FIX_CLAIMED], 1), quit = 0;
+      for (uint32_t spin = 0;; spin++) {
+        if (spin > QUEUE_SPIN_LIMIT) __trap();
+        if (idx < vf[FIX_RESERVED]) break;
+        if (vf[FIX_DONE] == n_tiles) {
+          __threadfence();
+          if (idx >= vf[FIX_RESERVED]) quit = 1;
+          break;
+        }
+        __nanosleep(500);
+      }
+      int32_t v = 0;
+      if (!quit) {
+        for (uint32_t spin = 0; (v = vf[FIX_SLOTS + idx]) == 0; spin++) {
+          if (spin > QUEUE_SPIN_LIMIT) __trap();
+          __nanosleep(100);
+        }
+        vf[FIX_SLOTS + idx] = 0;
+      }
+      s_quit = quit;
+      s_claim = v;
+      s_T = 1.0;
+      s_last = -1;
+      s_done = 0;
+    }
+    __syncthreads();
+    if (s_quit) break;
+    const int64_t p = (int64_t)s_claim - 1;
+    const int px = (int)(p % width), py = (int)(p / width);
+    const int tile = (py / BLEND_TILE) * tiles_x + px / BLEND_TILE;
+    const bool mesh_here = mesh.color != nullptr && mesh.triangle_id[p] >= 0;
+    const double limit = mesh_here ? mesh.depth[p] : __longlong_as_double(0x7ff0000000000000LL);
+    const double fx = px + 0.5, fy = py + 0.5;
+    const int64_t s = tile_starts[tile];
+    uint4 pg = make_uint4(0u, 0u, 0u, 0u);
+    if (crow) pg = __ldcg(prog + tile);
+    const int64_t e = crow ? s + (int64_t)pg.x : tile_starts[tile + 1];  // (blend-only: the written prefix)
+    double pr = 0.0, pgc = 0.0, pb = 0.0, pd = 0.0;  // this warp's per-lane partial sums
+    // prefetch: my first round's records and the next round's indices
+    auto idx = [&](int64_t rb, int u) -> uint32_t {
+      const int64_t k = rb + EW * lane + u;
+      return k < e ? __ldcg(entries + k) : 0u;
+    };
+    BlendRec c[EW], cn[EW];
+    uint32_t ixn[EW];
+    {
+      const int64_t b0 = s + (int64_t)warp * RW;
+#pragma unroll
+      for (int u = 0; u < EW; u++) {
+        const uint32_t i0 = idx(b0, u);
+        if (b0 + EW * lane + u < e) cn[u] = rec[i0];
+        ixn[u] = idx(b0 + EXW * RW, u);
+      }
+    }
+    for (int64_t sb = s; sb < e; sb += (int64_t)EXW * RW) {
+      if (s_done) break;  // (uniform: read after the last barrier)
+      const int64_t base = sb + (int64_t)warp * RW;
+#pragma unroll
+      for (int u = 0; u < EW; u++) {
+        c[u] = cn[u];
+        if (base + EXW * RW + EW * lane + u < e) cn[u] = rec[ixn[u]];
+        ixn[u] = idx(base + 2 * EXW * RW, u);
+      }
+      // phase A (all warps): evaluate this warp's round
+      double sig[EW];
+      bool use[EW];
+      int us = EW;
+#pragma unroll
+      for (int u = 0; u < EW; u++) {
+        const int64_t k = base + EW * lane + u;
+        use[u] = false;
+        sig[u] = 0.0;
+        if (k < e) {
+          if (c[u].depth >= limit && us == EW) us = u;
+          const double dx = fx - c[u].mx, dy = fy - c[u].my;
+          const double m = c[u].ca * dx * dx + c[u].cb2 * dx * dy + c[u].cc * dy * dy;
+          if (!(m > SUPPORT_MAHAL2 || m < 0.0)) {
+            double sg = c[u].alpha * exp(-0.5 * m);
+            if (sg > ALPHA_CLAMP) sg = ALPHA_CLAMP;
+            use[u] = !(sg < SIGMA_SKIP);
+            sig[u] = sg;
+          }
+        }
+      }
+      const unsigned smask = __ballot_sync(0xffffffffu, us < EW);
+      const int ls = smask ? __ffs(smask) - 1 : 32;
+      const int lsu = __shfl_sync(0xffffffffu, us, ls & 31);
+#pragma unroll
+      for (int u = 0; u < EW; u++)
+        if (lane > ls || (lane == ls && u >= lsu)) use[u] = false;
+      double f[EW];
+      double q = 1.0;
+#pragma unroll
+      for (int u = 0; u < EW; u++) {
+        f[u] = use[u] ? 1.0 - sig[u] : 1.0;
+        q *= f[u];
+      }
+      double P = q;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, P, d);
+        if (lane >= d) P *= t;
+      }
+      double Pex = __shfl_up_sync(0xffffffffu, P, 1);
+      if (lane == 0) Pex = 1.0;
+      // phase B: commit the rounds in order (exact_walk2's arithmetic with the
+      // T the previous round left)
+      for (int w = 0; w < EXW; w++) {
+        if (warp == w && !s_done && base < e) {
+          double T = s_T;
+          int64_t last = s_last;
+          bool done = false;
+          double ta[EW];
+          double run = T * Pex;
+          bool near = false;
+#pragma unroll
+          for (int u = 0; u < EW; u++) {
+            run *= f[u];
+            ta[u] = run;
+            near = near || (use[u] && fabs(run - EARLY_STOP_T) <= 1e-12 * EARLY_STOP_T);
+          }
+          if (!__any_sync(0xffffffffu, near)) {
+            int ue = EW;
+#pragma unroll
+            for (int u = 0; u < EW; u++)
+              if (use[u] && ta[u] < EARLY_STOP_T && ue == EW) ue = u;
+            const unsigned emask = __ballot_sync(0xffffffffu, ue < EW);
+            const int le = emask ? __ffs(emask) - 1 : 32;
+            const int leu = __shfl_sync(0xffffffffu, ue, le & 31);
+            int lastu = -1;
+            double tb = T * Pex, tl = 0.0;
+#pragma unroll
+            for (int u = 0; u < EW; u++) {
+              const bool valid = use[u] && (lane < le || (lane == le && u < leu));
+              if (valid) {
+                const double wv = sig[u] * tb;
+                pr += c[u].r * wv;
+                pgc += c[u].g * wv;
+                pb += c[u].b * wv;
+                pd += c[u].depth * wv;
+                lastu = u;
+                tl = ta[u];
+              }
+              tb = ta[u];
+            }
+            const unsigned vmask = __ballot_sync(0xffffffffu, lastu >= 0);
+            if (vmask) {
+              const int lv = 31 - __clz(vmask);
+              T = __shfl_sync(0xffffffffu, tl, lv);
+              last = base + (int64_t)EW * lv + __shfl_sync(0xffffffffu, lastu, lv);
+            }
+            if (le < 32) done = true;
+          } else {
+            bool stop = false;
+            for (int i = 0; i < 32 && !stop; i++) {
+#pragma unroll
+              for (int u = 0; u < EW; u++) {
+                const bool ui = __shfl_sync(0xffffffffu, use[u], i);
+                if (!ui || stop) continue;
+                const double sg = __shfl_sync(0xffffffffu, sig[u], i);
+                const double test_t = T * (1.0 - sg);
+                if (test_t < EARLY_STOP_T) {
+                  stop = true;
+                  continue;
+                }
+                if (lane == i) {
+                  const double wv = sg * T;
+                  pr += c[u].r * wv;
+                  pgc += c[u].g * wv;
+                  pb += c[u].b * wv;
+                  pd += c[u].depth * wv;
+                }
+                T = test_t;
+                last = base + (int64_t)EW * i + u;
+              }
+            }
+            if (stop) done = true;
+          }
+          if (ls < 32) done = true;
+          if (lane == 0) {
+            s_T = T;
+            s_last = last;
+            s_done = done ? 1 : 0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    // blend-only bins: the walk goes on past the written prefix (warp 0)
+    if (crow && !s_done && warp == 0) {
+      const int txx = px / BLEND_TILE, tyy = py / BLEND_TILE;
+      const int sup = (tyy >> css) * sx_super + (txx >> css);
+      WalkState ws{s_T, pr, pgc, pb, pd, s_last, false};
+      exact_walk_coarse_run(rec, crow, crect, pg.y, (int)pg.z, (int)pg.x, cstart[sup + 1], txx, tyy, s, fx, fy, limit,
+                            lane, ws);
+      pr = ws.pr, pgc = ws.pg, pb = ws.pb, pd = ws.pd;
+      if (lane == 0) {
+        s_T = ws.T;
+        s_last = ws.last;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      pr += __shfl_xor_sync(0xffffffffu, pr, d);
+      pgc += __shfl_xor_sync(0xffffffffu, pgc, d);
+      pb += __shfl_xor_sync(0xffffffffu, pb, d);
+      pd += __shfl_xor_sync(0xffffffffu, pd, d);
+    }
+    if (lane == 0) {
+      s_sum[warp][0] = pr;
+      s_sum[warp][1] = pgc;
+      s_sum[warp][2] = pb;
+      s_sum[warp][3] = pd;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double r = 0.0, g = 0.0, b = 0.0, dd = 0.0;
+      for (int w = 0; w < EXW; w++) r += s_sum[w][0], g += s_sum[w][1], b += s_sum[w][2], dd += s_sum[w][3];
+      const double T = s_T;
+      write_pixel(out, mesh, mesh_here, p, T, r, g, b, dd, 1.0 - T, s_last, bg0, bg1, bg2, mask_variant, mask_k, T);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace hgs
 
 // Is f one of the blend kernels that consume the fine binning's ready queue?
@@ -1547,7 +1815,12 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
     // exact fix-up: queue consumer beside the blend (one warp per flagged pixel)
     // small CTAs (2 warps, ~11k registers): they fit beside the blend's
     // resident CTAs as soon as its last wave starts retiring
-    launch_pdl(blend_exact_queue_kernel, dim3(8 * NUM_SMS), dim3(64), 0, st, (const BlendRec*)proj->rec,
+#ifndef HGS_EXACT_CTA
+#define HGS_EXACT_CTA 1
+#endif
+    launch_pdl(HGS_EXACT_CTA ? blend_exact_cta_kernel : blend_exact_queue_kernel,
+               dim3(HGS_EXACT_CTA ? 2 * NUM_SMS : 8 * NUM_SMS), dim3(HGS_EXACT_CTA ? EXW * 32 : 64), 0, st,
+               (const BlendRec*)proj->rec,
                (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_cta, width, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
                (const int64_t*)tiles->counters, ready, crow, crect, cstart, coarse ? ss : 0, sxs,
