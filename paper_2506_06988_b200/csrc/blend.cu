@@ -1443,7 +1443,13 @@ __global__ void __launch_bounds__(64) blend_exact_queue_kernel(
 // round left -- the same arithmetic per round as exact_walk2.  Blend-only
 // bins: the tile-list prefix in `entries`, then warp 0 continues over the
 // coarse list (exact_walk_coarse_run).
-constexpr int EXW = 4;
+#ifndef HGS_EXW
+#define HGS_EXW 4
+#endif
+#ifndef HGS_EX_CTAS_PER_SM
+#define HGS_EX_CTAS_PER_SM 2
+#endif
+constexpr int EXW = HGS_EXW;
 __global__ void __launch_bounds__(EXW * 32) blend_exact_cta_kernel(
     const BlendRec* __restrict__ rec, const uint32_t* __restrict__ entries, const int64_t* __restrict__ tile_starts,
     int tiles_x, int n_tiles, int width, hgs_mesh_layer mesh, double bg0, double bg1, double bg2, int mask_variant,
@@ -1819,7 +1825,7 @@ extern "C" int hgs_blend_forward(const hgs_projected* proj, const hgs_tiles* til
 #define HGS_EXACT_CTA 1
 #endif
     launch_pdl(HGS_EXACT_CTA ? blend_exact_cta_kernel : blend_exact_queue_kernel,
-               dim3(HGS_EXACT_CTA ? 2 * NUM_SMS : 8 * NUM_SMS), dim3(HGS_EXACT_CTA ? EXW * 32 : 64), 0, st,
+               dim3(HGS_EXACT_CTA ? HGS_EX_CTAS_PER_SM * NUM_SMS : 8 * NUM_SMS), dim3(HGS_EXACT_CTA ? EXW * 32 : 64), 0, st,
                (const BlendRec*)proj->rec,
                (const uint32_t*)tiles->entries, (const int64_t*)tiles->tile_starts, tiles->tiles_x, n_cta, width, ml,
                bg_host3[0], bg_host3[1], bg_host3[2], mask_variant, mask_k, *out, out->fixup,
