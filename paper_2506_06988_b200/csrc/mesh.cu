@@ -31,17 +31,10 @@ struct TriSetup {
 };
 
 // Per-triangle setup, meshraster.py:50-84.  Returns false if culled/empty.
-__device__ __forceinline__ double3 ld_cg3(const double3* p) {
-  return make_double3(__ldcg(&p->x), __ldcg(&p->y), __ldcg(&p->z));
-}
-// L2 = true: vertex reads bypass L1 (kernels that start without waiting for
-// the grid that wrote this frame's projected vertices)
-template <bool L2 = false>
 __device__ __forceinline__ bool tri_setup(const double3* __restrict__ vproj, const int32_t* __restrict__ tris, int64_t f,
                                           int width, int height, double near_, TriSetup& t) {
   const int ia = tris[3 * f], ib = tris[3 * f + 1], ic = tris[3 * f + 2];
-  const double3 A = L2 ? ld_cg3(vproj + ia) : vproj[ia], B = L2 ? ld_cg3(vproj + ib) : vproj[ib],
-                C = L2 ? ld_cg3(vproj + ic) : vproj[ic];
+  const double3 A = vproj[ia], B = vproj[ib], C = vproj[ic];
   if (A.z <= near_ || B.z <= near_ || C.z <= near_) return false;
   double ax = A.x, ay = A.y, bx = B.x, by = B.y, cx = C.x, cy = C.y;
   double area2 = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
@@ -154,9 +147,6 @@ __global__ void __launch_bounds__(256) raster_small_kernel(const double3* __rest
                                                            int height, const hgs_camera* __restrict__ cam,
                                                            unsigned long long* zbuf, int32_t* idbuf, int32_t* lists,
                                                            int32_t* list_counts) {
-  // PASS 1: the larger triangles were binned by raster_bin_kernel (the group
-  // kernels run beside this one); PASS 0: bin them here
-  if (PASS == 1) pdl_enter();
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   TriSetup t;
@@ -173,40 +163,21 @@ __global__ void __launch_bounds__(256) raster_small_kernel(const double3* __rest
     for (int px = t.x0; px <= t.x1; px++) raster_pixel<PASS>(t, f, px, py, width, zbuf, idbuf);
 }
 
-// The medium / large triangle lists alone (so that the small-triangle and
-// group rasterisers can run side by side).
-__global__ void __launch_bounds__(256) raster_bin_kernel(const double3* __restrict__ vproj,
-                                                         const int32_t* __restrict__ tris, int64_t nf, int width,
-                                                         int height, const hgs_camera* __restrict__ cam,
-                                                         int32_t* lists, int32_t* list_counts) {
-  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
-  TriSetup t;
-  if (!tri_setup(vproj, tris, f, width, height, cam->near_, t)) return;
-  const int64_t area = (int64_t)(t.x1 - t.x0 + 1) * (t.y1 - t.y0 + 1);
-  if (area <= SMALL_TRI_PIXELS) return;
-  const int which = area > BIG_TRI_PIXELS ? 1 : 0;
-  lists[which * nf + atomicAdd(&list_counts[which], 1)] = (int32_t)f;
-}
-
 // GROUP threads per triangle (32: one warp; 256: one CTA), striding the box.
-// PASS 1: launched behind raster_small_kernel<1> without waiting for it (the
-// lists were complete before it started): lists and vertices read from L2.
 template <int PASS, int GROUP>
 __global__ void __launch_bounds__(256) raster_group_kernel(const double3* __restrict__ vproj,
                                                            const int32_t* __restrict__ tris, int width, int height,
                                                            const hgs_camera* __restrict__ cam,
                                                            unsigned long long* zbuf, int32_t* idbuf,
                                                            const int32_t* list, const int32_t* list_count) {
-  if (PASS == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int nlist = PASS == 1 ? __ldcg(list_count) : *list_count;
+  const int nlist = *list_count;
   const int groups_per_block = 256 / GROUP;
   const int gid = blockIdx.x * groups_per_block + threadIdx.x / GROUP;
   const int r = threadIdx.x % GROUP;
   for (int b = gid; b < nlist; b += gridDim.x * groups_per_block) {
-    const int64_t f = PASS == 1 ? __ldcg(list + b) : list[b];
+    const int64_t f = list[b];
     TriSetup t;
-    if (!tri_setup<PASS == 1>(vproj, tris, f, width, height, cam->near_, t)) continue;
+    if (!tri_setup(vproj, tris, f, width, height, cam->near_, t)) continue;
     const int bw = t.x1 - t.x0 + 1;
     const int area = bw * (t.y1 - t.y0 + 1);  // < 2^31: clipped to the image
     // box position of q without a division: a running (column, row) pair
@@ -234,7 +205,6 @@ __global__ void __launch_bounds__(256) raster_resolve_kernel(const double3* __re
                                                              const hgs_camera* __restrict__ cam,
                                                              const unsigned long long* __restrict__ zbuf,
                                                              hgs_fragments out) {
-  pdl_enter();  // (launched with PDL only behind the side-by-side rasterisers)
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (int64_t)width * height) return;
   const int32_t f = (int32_t)zbuf[2 * p + 1];
@@ -409,33 +379,6 @@ extern "C" int hgs_rasterize_fragments(const hgs_camera* cam, int32_t width, int
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-#ifndef HGS_RASTER_SIDE_BY_SIDE_ABOVE
-#define HGS_RASTER_SIDE_BY_SIDE_ABOVE 500000  // triangles (c5, 1M: 2.15 vs 2.20 ms; c3, 200k: 770 vs 756 us)
-#endif
-    if (nf > HGS_RASTER_SIDE_BY_SIDE_ABOVE && pdl_enabled()) {
-      // bin first; then the small-triangle pass and the two group passes run
-      // side by side (programmatic launches, the group passes without a grid
-      // wait: the lists were complete before the small pass started), and the
-      // resolve waits for all three (completion stays in stream order)
-      raster_bin_kernel<<<gf, 256, 0, st>>>(vproj, mesh->triangles, nf, width, height, cam, lists, list_counts);
-      HGS_CHECK_LAUNCH();
-      launch_pdl(raster_small_kernel<1>, dim3(gf), dim3(256), 0, st, (const double3*)vproj, (const int32_t*)mesh->triangles,
-                 nf, width, height, cam, zbuf, idbuf, lists, list_counts);
-      HGS_CHECK_LAUNCH();
-      launch_pdl(raster_group_kernel<1, 32>, dim3(8 * sms), dim3(256), 0, st, (const double3*)vproj,
-                 (const int32_t*)mesh->triangles, width, height, cam, zbuf, idbuf, (const int32_t*)lists,
-                 (const int32_t*)list_counts);
-      HGS_CHECK_LAUNCH();
-      launch_pdl(raster_group_kernel<1, 256>, dim3(2 * sms), dim3(256), 0, st, (const double3*)vproj,
-                 (const int32_t*)mesh->triangles, width, height, cam, zbuf, idbuf, (const int32_t*)(lists + nf),
-                 (const int32_t*)(list_counts + 1));
-      HGS_CHECK_LAUNCH();
-      launch_pdl(raster_resolve_kernel, dim3(ceil_div(npix, 256)), dim3(256), 0, st, (const double3*)vproj,
-                 (const int32_t*)mesh->triangles, (const float*)mesh->uvs, width, height, cam,
-                 (const unsigned long long*)zbuf, *out);
-      HGS_CHECK_LAUNCH();
-      return HGS_OK;
     }
     raster_small_kernel<0><<<gf, 256, 0, st>>>(vproj, mesh->triangles, nf, width, height, cam, zbuf, idbuf, lists,
                                               list_counts);
