@@ -114,8 +114,12 @@ constexpr uint32_t KEY_CULLED = (1u << DEPTH_KEY_BITS) - 1;
 #endif
 #define HGS_SORT_ALL (HGS_DEPTH_MODE == 1)
 // depth sort partition (radix_pass_kernel<uint32_t, 8>: 256 threads x 8 keys)
-constexpr int RS_DEPTH_IPT = 8;
+#ifndef HGS_RS_DEPTH_IPT
+#define HGS_RS_DEPTH_IPT 8
+#endif
+constexpr int RS_DEPTH_IPT = HGS_RS_DEPTH_IPT;
 constexpr int RS_PART = RS_THREADS * RS_DEPTH_IPT;
+constexpr int RS_KPT = RS_PART / 256;  // keys per thread of the 256-thread stats / compaction kernels
 // HGS_SORT_RTS=1: reduce-then-scan depth passes (every pass counts the next
 // pass's per-partition digits as it scatters; a scan kernel turns them into
 // offsets) instead of the onesweep decoupled look-back
@@ -136,10 +140,10 @@ __global__ void __launch_bounds__(256) depth_stats_kernel(const uint64_t* __rest
   long long total = 0;
   const int64_t nparts = (n + RS_PART - 1) / RS_PART;
   for (int64_t part = blockIdx.x; part < nparts; part += gridDim.x) {
-    const int64_t base = part * RS_PART + (int64_t)threadIdx.x * 8;  // 8 consecutive keys per thread
+    const int64_t base = part * RS_PART + (int64_t)threadIdx.x * RS_KPT;  // RS_KPT consecutive keys per thread
     uint32_t cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
+    for (int j = 0; j < RS_KPT; j += 2) {
       uint64_t k0 = ~0ull, k1 = ~0ull;
       if (base + j + 1 < n) {
         const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + j));
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(256) depth_remap_kernel(const uint64_t* __rest
 }
 
 // Mode 2: the compaction fused into the remap.  One CTA per partition of
-// RS_PART rows (8 consecutive per thread): the visible rows before it are the
+// RS_PART rows (RS_KPT consecutive per thread): the visible rows before it are the
 // sum of its predecessors' counts (depth_stats_kernel), its own are ranked
 // by a block scan, staged in shared memory and written out contiguously --
 // the remapped key and the row -- together with the digit histograms and
@@ -270,10 +274,10 @@ __global__ void __launch_bounds__(256) depth_compact_remap_kernel(
     uint32_t pre = 0;  // visible rows in the earlier partitions
     for (int64_t q = threadIdx.x; q < part; q += blockDim.x) pre += vis_cnt[q];
     sh_p[0][threadIdx.x] = sh_p[1][threadIdx.x] = 0;
-    const int64_t base = part * RS_PART + (int64_t)threadIdx.x * 8;
-    uint64_t kk[8];
+    const int64_t base = part * RS_PART + (int64_t)threadIdx.x * RS_KPT;
+    uint64_t kk[RS_KPT];
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
+    for (int j = 0; j < RS_KPT; j += 2) {
       if (base + j + 1 < n) {
         const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(keys + base + j));
         kk[j] = v.x, kk[j + 1] = v.y;
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(256) depth_compact_remap_kernel(
     }
     uint32_t cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 8; j++) cnt += kk[j] != ~0ull;
+    for (int j = 0; j < RS_KPT; j++) cnt += kk[j] != ~0ull;
     uint32_t tot_pre;
     pre = block_exclusive_scan<uint32_t>(pre, s_warp, tot_pre);  // (only the total is used)
     pre = tot_pre;
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(256) depth_compact_remap_kernel(
     uint32_t r = block_exclusive_scan<uint32_t>(cnt, s_warp, tot);
     const uint32_t p0 = pre / RS_PART;  // first sort partition of this output range
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
+    for (int j = 0; j < RS_KPT; j++) {
       if (kk[j] == ~0ull) continue;
       const uint32_t k = (uint32_t)((kk[j] - lo) >> sh);
       s_k[r] = k;
