@@ -496,11 +496,25 @@ __global__ void __launch_bounds__(1024) tile_counts_kernel(int* __restrict__ dif
   const int cells = gw * (tiles_y + 1);
   const int n_tiles = tiles_x * tiles_y;
   for (int i = threadIdx.x; i < 3 * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
-  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
-    int v = 0;
+  if (!in_global && (cells & 3) == 0 && cells <= 4 * (int)blockDim.x) {
+    // one round: every thread sums four cells of the 16 copies with 16-byte loads
+    const int c4 = threadIdx.x * 4;
+    if (c4 < cells) {
+      int4 v = make_int4(0, 0, 0, 0);
 #pragma unroll
-    for (int k = 0; k < TILE_DIFF_COPIES; k++) v += diff[(size_t)k * cells + c];
-    g[c] = v;  // (global path: copy 0 in place -- each cell is read and written by one thread)
+      for (int k = 0; k < TILE_DIFF_COPIES; k++) {
+        const int4 d = *reinterpret_cast<const int4*>(diff + (size_t)k * cells + c4);
+        v.x += d.x, v.y += d.y, v.z += d.z, v.w += d.w;
+      }
+      g[c4] = v.x, g[c4 + 1] = v.y, g[c4 + 2] = v.z, g[c4 + 3] = v.w;
+    }
+  } else {
+    for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+      int v = 0;
+#pragma unroll
+      for (int k = 0; k < TILE_DIFF_COPIES; k++) v += diff[(size_t)k * cells + c];
+      g[c] = v;  // (global path: copy 0 in place -- each cell is read and written by one thread)
+    }
   }
   __syncthreads();
   if (!in_global) {
@@ -575,7 +589,7 @@ __global__ void __launch_bounds__(1024) tile_counts_kernel(int* __restrict__ dif
   for (int t = t0; t < t1; t++) {
     const int c = g[(t / tiles_x) * gw + t % tiles_x];
     local_sum += c;
-    if (c) {
+    if (c && hist) {  // (the tile-key histograms: non-binned grids only)
       atomicAdd(&sh[0][t & 255], (uint32_t)c);
       atomicAdd(&sh[1][(t >> 8) & 255], (uint32_t)c);
       atomicAdd(&sh[2][(t >> 16) & 255], (uint32_t)c);
@@ -612,7 +626,8 @@ __global__ void __launch_bounds__(1024) tile_counts_kernel(int* __restrict__ dif
     tile_starts[t] = run;
     run += g[(t / tiles_x) * gw + t % tiles_x];
   }
-  for (int i = threadIdx.x; i < 3 * RADIX; i += blockDim.x) hist[i] = (&sh[0][0])[i];
+  if (hist)
+    for (int i = threadIdx.x; i < 3 * RADIX; i += blockDim.x) hist[i] = (&sh[0][0])[i];
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) offsets_kernel(const int32_t* __restrict__ count,
@@ -1594,7 +1609,8 @@ extern "C" int hgs_build_tiles(const hgs_projected* proj, int64_t n, hgs_tiles* 
     tc_attr = true;
   }
   launch_pdl(tile_counts_kernel, dim3(1), dim3(1024), grid_smem, st, proj->tile_diff, tx, ty, tiles->capacity, tiles->tile_starts,
-                                                 tiles->counters, s.hist + 8 * RADIX, tc_global, (int*)tiles->ready,
+                                                 tiles->counters, ss_all >= 0 ? (uint32_t*)nullptr : s.hist + 8 * RADIX,
+                                                 tc_global, (int*)tiles->ready,
                                                  n == 0 && ss_all >= 0 ? n_quads_all : 0);
   HGS_CHECK_LAUNCH();
   auto join = [&]() -> int {  // the caller's independent branch joins the stream (hgs.h join_event)
